@@ -1,0 +1,64 @@
+"""oracle/dense.py — TEST INFRASTRUCTURE ONLY.  O0: Table 2's "Matrix notation" column evaluated
+literally on a dense traffic matrix.
+
+PAPER.md (arXiv 2509.03653) Table 2, defines the scalars on the traffic matrix A_t;
+the caption (line 173) adds the destination mirrors by swapping src and dst.  Because every quantity
+is invariant under a bijective relabelling of addresses (the paper's own anonymisation argument,
+lines 195-203), the window's distinct addresses are relabelled 0..V-1 (np.unique) and A_t is built
+as a dense V x V integer matrix by counting packets.  Then, literally:
+
+    valid packets             sum_i sum_j A_t(i,j)          (:180)
+    unique links              sum_i sum_j |A_t(i,j)|_0      (:181)
+    max link packets          max_ij A_t(i,j)               (:183)
+    unique sources            sum_i |sum_j A_t(i,j)|_0      (:184)
+    max source packets        max_i sum_j A_t(i,j)          (:186)
+    max source fan-out        max_i sum_j |A_t(i,j)|_0      (:188)
+    unique destinations / max destination packets / max destination fan-in: the same on A_t^T (:173)
+
+Only for tiny windows (V <= max_vertices).  Empty max = 0 (reading R7).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def _one_window(s: np.ndarray, d: np.ndarray, max_vertices: int) -> list[int]:
+    if s.size == 0:
+        return [0] * 9
+    labels, inv = np.unique(np.concatenate([s, d]), return_inverse=True)
+    V = labels.size
+    if V > max_vertices:
+        raise ValueError(f"dense oracle is for tiny windows (V={V} > {max_vertices})")
+    i, j = inv[: s.size], inv[s.size:]
+    A = np.zeros((V, V), dtype=np.int64)
+    np.add.at(A, (i, j), 1)                      # A_t(i,j) = packets i -> j
+    nz = (A != 0).astype(np.int64)               # |A_t|_0
+    row_sum, col_sum = A.sum(axis=1), A.sum(axis=0)          # A_t 1, 1^T A_t
+    row_nnz, col_nnz = nz.sum(axis=1), nz.sum(axis=0)        # |A_t|_0 1, 1^T |A_t|_0
+    return [
+        int(A.sum()),
+        int(nz.sum()),
+        int(A.max()),
+        int((row_sum != 0).sum()),
+        int(row_sum.max()),
+        int(row_nnz.max()),
+        int((col_sum != 0).sum()),
+        int(col_sum.max()),
+        int(col_nnz.max()),
+    ]
+
+
+def window_stats_dense(src, dst, window: int, *, max_vertices: int = 256) -> np.ndarray:
+    """O0 over every window of (src, dst).  Returns uint64 [n_windows, 9]."""
+    s = np.asarray(src, dtype=np.int64).ravel()
+    d = np.asarray(dst, dtype=np.int64).ravel()
+    if s.shape != d.shape:
+        raise ValueError("src and dst must have the same length")
+    if window < 1:
+        raise ValueError("window must be >= 1")
+    n = s.size
+    nw = 0 if n == 0 else (n + window - 1) // window
+    out = np.zeros((nw, 9), dtype=np.uint64)
+    for w in range(nw):
+        out[w] = _one_window(s[w * window:(w + 1) * window], d[w * window:(w + 1) * window], max_vertices)
+    return out

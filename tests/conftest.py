@@ -1,0 +1,33 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU; runs the CUDA path")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+def pytest_sessionstart(session):
+    # Build the native artefacts in-tree (idempotent; nvcc cross-compiles without a GPU).
+    import gen
+    import oracle
+
+    gen.build()
+    oracle.build()
+
+
+@pytest.fixture(scope="session")
+def cuda_device():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.fail("gpu tests need a CUDA device (the CUDA path has no CPU fallback)")
+    return torch.device("cuda", 0)
