@@ -1,0 +1,125 @@
+/* include/nsg.h — C ABI of libnsg, the B200 (sm_100a) per-window Network Sensing Graph Challenge path.
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, arXiv 2509.03653):
+ *   The packet stream (src_p, dst_p), p = 0..n-1, is cut into windows of `window` consecutive packets
+ *   (window w holds packets [w*window, min((w+1)*window, n)); the last window may be shorter).  For
+ *   window w, A_t is the traffic matrix of Table 2 (caption line 173):
+ *       A_t(i,j) = number of packets of the window with src = i and dst = j      (raw packets, weight 1)
+ *   and the library returns the nine scalars of Table 2 and its destination mirrors, in this column
+ *   order (north_star order):
+ *       [0] valid packets            1^T A_t 1
+ *       [1] unique links             1^T |A_t|_0 1
+ *       [2] max link packets         max(A_t)
+ *       [3] unique sources           1^T |A_t 1|_0
+ *       [4] max source packets       max(A_t 1)
+ *       [5] max source fan-out       max(|A_t|_0 1)
+ *       [6] unique destinations      mirror of [3]      PAPER.md:173 ("replace src and dst"), :241
+ *       [7] max destination packets  mirror of [4]
+ *       [8] max destination fan-in   mirror of [5]
+ *   Readings of the paper where it is silent or garbled are listed in DESIGN.md ("Readings"): directed
+ *   links, self-loops are ordinary entries, every 32-bit address value is a vertex, empty max = 0.
+ *
+ * Addresses are IPv4 in host integer order (a.b.c.d <-> a<<24|b<<16|c<<8|d).  The packed form of a
+ * packet is the u64 key (src << 32) | dst.
+ *
+ * Conventions for every entry point:
+ *   - Ownership: the caller allocates every buffer; the library never allocates device memory and keeps
+ *     no pointer after returning.  Device work is ASYNCHRONOUS on `stream` (a cudaStream_t passed as
+ *     void*; NULL = legacy default stream): buffers must stay alive and unmodified until the stream
+ *     reaches that point.  out[] is only valid once the stream has completed the call.
+ *   - Arguments: window >= 1 and window <= NSG_MAX_WINDOW; n_packets == 0 -> NSG_OK with no launch;
+ *     NULL data/out/workspace pointers with n_packets > 0 -> NSG_ERR_INVALID_ARGUMENT, nothing launched.
+ *     Pointers need only natural alignment (4 B for src/dst, 8 B for keys, 8 B for out, 256 B for the
+ *     workspace); wider vector loads are used internally when the data happens to be 16 B aligned.
+ *   - Output: out is device memory, row-major [nsg_num_windows(n, window)][NSG_NUM_STATS] u64.
+ *   - Errors: argument errors and launch errors are returned synchronously; nothing is launched on an
+ *     argument error.  There is no CPU fallback: a device that is not sm_100 returns
+ *     NSG_ERR_UNSUPPORTED_DEVICE.
+ *   - Thread safety: calls are independent; two concurrent calls must not share a workspace.
+ */
+#ifndef NSG_H
+#define NSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { NSG_NUM_STATS = 9 };
+
+/* Column index of each statistic in an out row. */
+enum nsg_stat {
+  NSG_VALID_PACKETS = 0,
+  NSG_UNIQUE_LINKS = 1,
+  NSG_MAX_LINK_PACKETS = 2,
+  NSG_UNIQUE_SOURCES = 3,
+  NSG_MAX_SOURCE_PACKETS = 4,
+  NSG_MAX_SOURCE_FANOUT = 5,
+  NSG_UNIQUE_DESTINATIONS = 6,
+  NSG_MAX_DESTINATION_PACKETS = 7,
+  NSG_MAX_DESTINATION_FANIN = 8
+};
+
+typedef enum {
+  NSG_OK = 0,
+  NSG_ERR_INVALID_ARGUMENT = 1,
+  NSG_ERR_CUDA = 2,
+  NSG_ERR_WORKSPACE_TOO_SMALL = 3,
+  NSG_ERR_UNSUPPORTED_DEVICE = 4,
+  NSG_ERR_INTERNAL = 5
+} nsg_status;
+
+/* Largest supported window (per-window counts are kept in 32 bits on the device). */
+#define NSG_MAX_WINDOW (1ull << 31)
+
+/* Flags for nsg_window_stats_ex (testing / fault injection; 0 = normal operation). */
+enum {
+  NSG_FLAG_FORCE_GLOBAL = 1u << 0,     /* run every window on the L2 (global-table) path */
+  NSG_FLAG_INJECT_OVERFLOW = 1u << 1,  /* mark every odd window as overflowed on the fast path, so the
+                                          overflow hand-off to the L2 path is exercised */
+  NSG_FLAG_NO_FALLBACK_CHECK = 1u << 2 /* internal/benchmark: skip the fallback launch; results of an
+                                          overflowed window are then undefined (never use for results) */
+};
+
+/* Number of windows: ceil(n_packets / window); 0 if n_packets == 0 or window == 0. */
+uint64_t nsg_num_windows(uint64_t n_packets, uint64_t window);
+
+/* Device scratch (bytes) the caller must pass as `workspace` for (n_packets, window); 0 when
+ * n_packets == 0.  Depends only on (n_packets, window) and the device's SM count. */
+size_t nsg_workspace_bytes(uint64_t n_packets, uint64_t window);
+
+/* SoA input: src[n_packets], dst[n_packets] device u32 arrays. */
+nsg_status nsg_window_stats(const uint32_t* src, const uint32_t* dst, uint64_t n_packets, uint64_t window,
+                            uint64_t* out, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Packed input: keys[n_packets] device u64 array, keys[p] = (u64)src_p << 32 | dst_p. */
+nsg_status nsg_window_stats_packed(const uint64_t* keys, uint64_t n_packets, uint64_t window, uint64_t* out,
+                                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* Either input form (exactly one of keys / (src,dst) non-NULL) plus test flags. */
+nsg_status nsg_window_stats_ex(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
+                               uint64_t window, uint64_t* out, void* workspace, size_t workspace_bytes,
+                               void* stream, uint32_t flags);
+
+/* Diagnostics of the last call that used `workspace` (device memory; read it after the stream has
+ * completed the call): byte offset inside the workspace of a u32[4] =
+ *   {windows the fast path handed to the L2 path because an SMEM table would overflow,
+ *    windows whose self-check failed (sum of link counts != window length; 0 unless there is a bug),
+ *    reserved, reserved}. */
+size_t nsg_diag_offset(void);
+
+/* Number of kernels the calling host thread's most recent nsg_window_stats* call launched. */
+unsigned nsg_last_launches(void);
+
+/* Human-readable name of a status code (static storage). */
+const char* nsg_status_string(nsg_status s);
+
+/* Library build identification (static storage), e.g. "libnsg sm_100a <date>". */
+const char* nsg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NSG_H */

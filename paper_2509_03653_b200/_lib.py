@@ -1,0 +1,86 @@
+"""ctypes loader for libnsg.so (the C ABI declared in include/nsg.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (``build_libnsg`` below).  There is no
+fallback of any kind: if libnsg.so is missing or cannot be loaded, importing the binding raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(_PKG)
+LIB_PATH = os.path.join(_PKG, "libnsg.so")
+SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("nsg.cu", "nsg_common.cuh")]
+HEADER = os.path.join(ROOT, "include", "nsg.h")
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+# Every symbol include/nsg.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "nsg_num_windows",
+    "nsg_workspace_bytes",
+    "nsg_window_stats",
+    "nsg_window_stats_packed",
+    "nsg_window_stats_ex",
+    "nsg_diag_offset",
+    "nsg_last_launches",
+    "nsg_status_string",
+    "nsg_version",
+)
+
+STATUS = {
+    0: "NSG_OK",
+    1: "NSG_ERR_INVALID_ARGUMENT",
+    2: "NSG_ERR_CUDA",
+    3: "NSG_ERR_WORKSPACE_TOO_SMALL",
+    4: "NSG_ERR_UNSUPPORTED_DEVICE",
+    5: "NSG_ERR_INTERNAL",
+}
+
+
+def build_libnsg(force: bool = False, verbose: bool = False) -> str:
+    """nvcc -gencode arch=compute_100a,code=sm_100a ... -> paper_2509_03653_b200/libnsg.so"""
+    newest = max(os.path.getmtime(p) for p in SOURCES + [HEADER])
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
+        tmp = LIB_PATH + f".tmp{os.getpid()}"
+        cmd = ["nvcc", *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, SOURCES[0]]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.check_call(cmd)
+        os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+class NsgError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        super().__init__(f"{what}: {STATUS.get(status, status)}")
+        self.status = status
+
+
+def load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    u64, sz, vp, u32 = ctypes.c_uint64, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_uint32
+    lib.nsg_num_windows.restype = u64
+    lib.nsg_num_windows.argtypes = [u64, u64]
+    lib.nsg_workspace_bytes.restype = sz
+    lib.nsg_workspace_bytes.argtypes = [u64, u64]
+    lib.nsg_window_stats.restype = ctypes.c_int
+    lib.nsg_window_stats.argtypes = [vp, vp, u64, u64, vp, vp, sz, vp]
+    lib.nsg_window_stats_packed.restype = ctypes.c_int
+    lib.nsg_window_stats_packed.argtypes = [vp, u64, u64, vp, vp, sz, vp]
+    lib.nsg_window_stats_ex.restype = ctypes.c_int
+    lib.nsg_window_stats_ex.argtypes = [vp, vp, vp, u64, u64, vp, vp, sz, vp, u32]
+    lib.nsg_diag_offset.restype = sz
+    lib.nsg_diag_offset.argtypes = []
+    lib.nsg_last_launches.restype = ctypes.c_uint
+    lib.nsg_last_launches.argtypes = []
+    lib.nsg_status_string.restype = ctypes.c_char_p
+    lib.nsg_status_string.argtypes = [ctypes.c_int]
+    lib.nsg_version.restype = ctypes.c_char_p
+    lib.nsg_version.argtypes = []
+    return lib

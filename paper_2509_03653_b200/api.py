@@ -1,0 +1,179 @@
+"""Python binding of libnsg (include/nsg.h): argument marshalling only.
+
+Every step of the per-window computation runs in libnsg's sm_100a kernels; this module only checks
+tensors, hands raw device pointers and the current CUDA stream to the C ABI, and manages the
+caller-owned workspace.  PyTorch supplies device memory and streams.
+
+The nine output columns (north_star order; Table 2 lines 180-188 and the destination
+mirrors of line 173):
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import torch
+
+from ._lib import NsgError, load
+
+_lib = load()  # raises ImportError if libnsg.so is missing: there is no fallback
+
+NUM_STATS = 9
+STAT_NAMES = (
+    "valid_packets",
+    "unique_links",
+    "max_link_packets",
+    "unique_sources",
+    "max_source_packets",
+    "max_source_fanout",
+    "unique_destinations",
+    "max_destination_packets",
+    "max_destination_fanin",
+)
+DEFAULT_WINDOW = 1 << 17
+MAX_WINDOW = 1 << 31
+
+FLAG_FORCE_GLOBAL = 1
+FLAG_INJECT_OVERFLOW = 2
+FLAG_NO_FALLBACK_CHECK = 4
+
+_U32_TYPES = (torch.int32, torch.uint32)
+_U64_TYPES = (torch.int64, torch.uint64)
+
+
+def num_windows(n_packets: int, window: int = DEFAULT_WINDOW) -> int:
+    return int(_lib.nsg_num_windows(int(n_packets), int(window)))
+
+
+def workspace_bytes(n_packets: int, window: int = DEFAULT_WINDOW) -> int:
+    return int(_lib.nsg_workspace_bytes(int(n_packets), int(window)))
+
+
+def version() -> str:
+    return _lib.nsg_version().decode()
+
+
+def last_launches() -> int:
+    """Kernels launched by this thread's most recent window_stats* call."""
+    return int(_lib.nsg_last_launches())
+
+
+class Workspace:
+    """Caller-owned device scratch for one (n_packets, window) shape, reusable across calls."""
+
+    def __init__(self, n_packets: int, window: int = DEFAULT_WINDOW, device=None):
+        self.n_packets, self.window = int(n_packets), int(window)
+        self.nbytes = workspace_bytes(self.n_packets, self.window)
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        # + 256 so the pointer can be aligned to 256 B
+        self.buffer = torch.empty(max(self.nbytes, 1) + 256, dtype=torch.uint8, device=dev)
+        base = self.buffer.data_ptr()
+        self.offset = (-base) % 256
+        self.ptr = base + self.offset
+
+    def fits(self, n_packets: int, window: int) -> bool:
+        return workspace_bytes(n_packets, window) <= self.nbytes
+
+    def diag(self) -> list:
+        """u32[4] diagnostics of the last call (synchronises the buffer's device)."""
+        off = self.offset + int(_lib.nsg_diag_offset())
+        return [int(x) for x in self.buffer[off:off + 16].view(torch.int32).cpu().tolist()]
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(n: int, window: int, device: torch.device, workspace: Optional[Workspace]) -> Workspace:
+    if workspace is not None:
+        if not workspace.fits(n, window):
+            raise NsgError(3, "workspace too small")
+        return workspace
+    key = (device.index, n, window)
+    ws = _ws_cache.get(key)
+    if ws is None:
+        if len(_ws_cache) > 8:
+            _ws_cache.clear()
+        ws = Workspace(n, window, device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def _check(t: torch.Tensor, name: str, dtypes) -> None:
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if t.dtype not in dtypes:
+        raise TypeError(f"{name} has dtype {t.dtype}; expected one of {dtypes}")
+    if t.dim() != 1 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous 1-D tensor")
+
+
+def _launch(src, dst, keys, n, window, out, workspace, stream, flags, device):
+    window = int(window)
+    if window < 1 or window > MAX_WINDOW:
+        raise ValueError(f"window must be in [1, 2^31], got {window}")
+    nw = num_windows(n, window)
+    if out is None:
+        out = torch.empty((nw, NUM_STATS), dtype=torch.int64, device=device)
+    else:
+        if out.dtype not in _U64_TYPES or not out.is_contiguous() or out.numel() < nw * NUM_STATS or not out.is_cuda:
+            raise ValueError("out must be a contiguous CUDA int64/uint64 tensor with >= n_windows*9 elements")
+    if n == 0:
+        return out
+    ws = _workspace(n, window, device, workspace)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_window_stats_ex(
+        None if src is None else src.data_ptr(),
+        None if dst is None else dst.data_ptr(),
+        None if keys is None else keys.data_ptr(),
+        n, window, out.data_ptr(), ws.ptr, ws.nbytes, ctypes.c_void_p(s.cuda_stream), int(flags))
+    if rc != 0:
+        raise NsgError(rc, "nsg_window_stats_ex")
+    return out
+
+
+def window_stats(src: torch.Tensor, dst: torch.Tensor, window: int = DEFAULT_WINDOW, *, out=None,
+                 workspace: Optional[Workspace] = None, stream=None, flags: int = 0) -> torch.Tensor:
+    """Nine quantities per window of the SoA packet stream (src[i], dst[i]) (device int32/uint32).
+
+    Returns a device int64 tensor [n_windows, 9], valid when `stream` (default: current) completes.
+    """
+    _check(src, "src", _U32_TYPES)
+    _check(dst, "dst", _U32_TYPES)
+    if src.numel() != dst.numel() or src.device != dst.device:
+        raise ValueError("src and dst must have the same length and device")
+    return _launch(src, dst, None, src.numel(), window, out, workspace, stream, flags, src.device)
+
+
+def window_stats_packed(keys: torch.Tensor, window: int = DEFAULT_WINDOW, *, out=None,
+                        workspace: Optional[Workspace] = None, stream=None, flags: int = 0) -> torch.Tensor:
+    """Nine quantities per window of packed keys[i] = src<<32 | dst (device int64/uint64)."""
+    _check(keys, "keys", _U64_TYPES)
+    return _launch(None, None, keys, keys.numel(), window, out, workspace, stream, flags, keys.device)
+
+
+def window_stats_from_host(keys_host: torch.Tensor, window: int = DEFAULT_WINDOW, *, device=None,
+                           keys_dev: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
+                           out_host: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None,
+                           stream=None) -> torch.Tensor:
+    """End-to-end call on HOST packed keys: H2D copy, the device computation, D2H copy of the result.
+
+    `keys_host` should be pinned for an asynchronous copy.  Returns the CPU int64 [n_windows, 9] result
+    (synchronised).
+    """
+    if keys_host.is_cuda or keys_host.dtype not in _U64_TYPES or keys_host.dim() != 1:
+        raise ValueError("keys_host must be a 1-D host int64/uint64 tensor")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    n = keys_host.numel()
+    if keys_dev is None:
+        keys_dev = torch.empty(n, dtype=keys_host.dtype, device=dev)
+    with torch.cuda.stream(s):
+        keys_dev[:n].copy_(keys_host, non_blocking=True)
+        res = window_stats_packed(keys_dev[:n], window, out=out, workspace=workspace, stream=s)
+        if out_host is None:
+            out_host = torch.empty(res.shape, dtype=torch.int64, pin_memory=True)
+        out_host.copy_(res, non_blocking=True)
+    s.synchronize()
+    return out_host

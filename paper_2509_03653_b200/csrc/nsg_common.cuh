@@ -1,0 +1,56 @@
+// nsg_common.cuh — shared device helpers of libnsg (the CUDA path).  Nothing here is shared
+// with oracle/ or gen/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nsg {
+
+typedef unsigned long long u64;
+typedef uint32_t u32;
+
+// Empty-slot sentinels.  Every 64-bit key and every 32-bit address is a legal value (DESIGN.md
+// reading R6), so the one key equal to a sentinel is never stored in a table: it is counted in a
+// per-table "escape" accumulator instead and folded back in when the table is scanned.
+constexpr u64 EMPTY64 = ~0ull;
+constexpr u32 EMPTY32 = ~0u;
+
+// Bijective mixers (murmur3 finalizers) used to spread keys over buckets and slots.  Bucket index
+// = top bits, slot index = low bits, so the two are independent.
+__host__ __device__ __forceinline__ u64 hash64(u64 h) {
+  h ^= h >> 33; h *= 0xff51afd7ed558ccdull;
+  h ^= h >> 33; h *= 0xc4ceb9fe1a85ec53ull;
+  h ^= h >> 33;
+  return h;
+}
+__host__ __device__ __forceinline__ u32 hash32(u32 x) {
+  x ^= x >> 16; x *= 0x85ebca6bu;
+  x ^= x >> 13; x *= 0xc2b2ae35u;
+  x ^= x >> 16;
+  return x;
+}
+
+__device__ __forceinline__ u64 ldcg64(const u64* p) { return __ldcg(reinterpret_cast<const unsigned long long*>(p)); }
+__device__ __forceinline__ u32 ldcg32(const u32* p) { return __ldcg(reinterpret_cast<const unsigned int*>(p)); }
+
+__device__ __forceinline__ u32 ld_acquire32(const u32* p) {
+  u32 v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release32(u32* p, u32 v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ u32 warp_sum(u32 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ u32 warp_max(u32 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+}  // namespace nsg

@@ -17,6 +17,10 @@ def pytest_configure(config):
 
 def pytest_sessionstart(session):
     # Build the native artefacts in-tree (idempotent; nvcc cross-compiles without a GPU).
+    import __graft_entry__
+
+    lib = __graft_entry__._load_file("_nsg_build_lib", os.path.join(ROOT, "paper_2509_03653_b200", "_lib.py"))
+    lib.build_libnsg()
     import gen
     import oracle
 

@@ -1,0 +1,109 @@
+"""The C-ABI library loads and exports every symbol include/nsg.h declares; host-side argument
+handling (no compute call needs a GPU here)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from nsg_testutil import ROOT
+
+HEADER = os.path.join(ROOT, "include", "nsg.h")
+LIB = os.path.join(ROOT, "paper_2509_03653_b200", "libnsg.so")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(nsg_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_expected_entry_points():
+    names = declared_functions()
+    for required in ("nsg_window_stats", "nsg_window_stats_packed", "nsg_workspace_bytes", "nsg_num_windows"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(LIB)
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_binding_export_list_matches_header():
+    from paper_2509_03653_b200 import _lib
+
+    assert sorted(_lib.EXPORTS) == declared_functions()
+
+
+def test_no_oracle_or_gen_symbols_in_libnsg():
+    lib = ctypes.CDLL(LIB)
+    for name in ("nsg_oracle_window_stats_map", "nsg_oracle_window_stats_sort", "nsg_gen_host", "nsg_gen_device"):
+        assert not hasattr(lib, name)
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2509_03653_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
+                assert "oracle.cpp" not in text and "nsggen" not in text, f
+
+
+def test_num_windows_and_workspace():
+    import paper_2509_03653_b200 as nsg
+
+    assert nsg.num_windows(0, 5) == 0
+    assert nsg.num_windows(10, 5) == 2
+    assert nsg.num_windows(11, 5) == 3
+    assert nsg.num_windows(1 << 23, 1 << 17) == 64
+    assert nsg.workspace_bytes(0, 1 << 17) == 0
+    a = nsg.workspace_bytes(1 << 17, 1 << 17)
+    b = nsg.workspace_bytes(1 << 23, 1 << 17)
+    assert 0 < a <= b
+    assert nsg.workspace_bytes(1 << 22, 1 << 21) > 0       # L2-path-only window
+    assert nsg.workspace_bytes(10, 0) == 0
+
+
+def test_argument_validation_without_gpu():
+    lib = ctypes.CDLL(LIB)
+    lib.nsg_window_stats_packed.restype = ctypes.c_int
+    lib.nsg_window_stats_packed.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    lib.nsg_window_stats.restype = ctypes.c_int
+    lib.nsg_window_stats.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                                     ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+    # n == 0: OK, nothing launched
+    assert lib.nsg_window_stats_packed(None, 0, 1 << 17, None, None, 0, None) == 0
+    # NULL data with n > 0
+    assert lib.nsg_window_stats_packed(None, 10, 1 << 17, 8, 256, 1 << 20, None) == 1
+    assert lib.nsg_window_stats(None, None, 10, 4, 8, 256, 1 << 20, None) == 1
+    # window 0 / too large
+    assert lib.nsg_window_stats_packed(8, 10, 0, 8, 256, 1 << 20, None) == 1
+    assert lib.nsg_window_stats_packed(8, 10, (1 << 31) + 1, 8, 256, 1 << 20, None) == 1
+    # misaligned workspace / out / keys
+    assert lib.nsg_window_stats_packed(8, 10, 4, 8, 255, 1 << 20, None) == 1
+    assert lib.nsg_window_stats_packed(8, 10, 4, 9, 256, 1 << 20, None) == 1
+    assert lib.nsg_window_stats_packed(12, 10, 4, 8, 256, 1 << 20, None) == 1
+
+
+def test_status_strings():
+    lib = ctypes.CDLL(LIB)
+    lib.nsg_status_string.restype = ctypes.c_char_p
+    assert lib.nsg_status_string(0) == b"NSG_OK"
+    assert lib.nsg_status_string(3) == b"NSG_ERR_WORKSPACE_TOO_SMALL"
+    lib.nsg_version.restype = ctypes.c_char_p
+    assert b"sm_100a" in lib.nsg_version()
+
+
+def test_sass_is_sm100a():
+    """The shipped library holds sm_100a SASS (cuobjdump), not PTX-only or another arch."""
+    import shutil
+    import subprocess
+
+    if shutil.which("cuobjdump") is None:
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run(["cuobjdump", "--list-elf", LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
