@@ -79,8 +79,11 @@ enum {
   NSG_FLAG_FORCE_GLOBAL = 1u << 0,     /* run every window on the L2 (global-table) path */
   NSG_FLAG_INJECT_OVERFLOW = 1u << 1,  /* mark every odd window as overflowed on the fast path, so the
                                           overflow hand-off to the L2 path is exercised */
-  NSG_FLAG_NO_FALLBACK_CHECK = 1u << 2 /* internal/benchmark: skip the fallback launch; results of an
+  NSG_FLAG_NO_FALLBACK_CHECK = 1u << 2, /* internal/benchmark: skip the fallback launch; results of an
                                           overflowed window are then undefined (never use for results) */
+  NSG_FLAG_PROFILE = 1u << 3           /* accumulate per-work-item-type SM cycles into the workspace:
+                                          u64[64] at nsg_diag_offset()+64: [0..12) per type (partition, link,
+                                          side) {items, cycles, wait cycles, 0}; [16+16*type+phase] cycles per phase */
 };
 
 /* Number of windows: ceil(n_packets / window); 0 if n_packets == 0 or window == 0. */

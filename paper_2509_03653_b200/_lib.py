@@ -12,7 +12,7 @@ import subprocess
 _PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.path.join(_PKG, "libnsg.so")
-SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("nsg.cu", "nsg_common.cuh")]
+SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("nsg.cu", "nsg_common.cuh", "nsg_fast.cuh", "nsg_global.cuh")]
 HEADER = os.path.join(ROOT, "include", "nsg.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]

@@ -41,6 +41,12 @@ __device__ __forceinline__ u32 ld_acquire32(const u32* p) {
 __device__ __forceinline__ void st_release32(u32* p, u32 v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Semaphore signal without a return value: after a __syncthreads(), one thread's release-RMW
+// publishes every write the CTA made before the barrier (PTX causality order is cumulative through
+// bar.sync; the same pattern as CUTLASS's GenericBarrier).
+__device__ __forceinline__ void red_release_add32(u32* p, u32 v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ u32 warp_sum(u32 v) {
 #pragma unroll

@@ -1,0 +1,766 @@
+// nsg_fast.cuh — the fast path of libnsg: one persistent kernel, three kinds of work item per window.
+//
+// Window w (packets [w*W, min((w+1)*W, n))) is processed as
+//   P(w,c)      c < cp   : a CH-key chunk is read from HBM once (128-bit streaming loads), counting-
+//                          sorted in SMEM by link bucket b = top logB bits of hash64(key) and written
+//                          to the window's L2-resident scratch slot, with its bucket offsets.
+//   L(w,b)      b < B    : the keys of link bucket b (about W/B of them) are gathered from every chunk
+//                          and aggregated in an SMEM hash table key -> count: this is A_t restricted to
+//                          the bucket ("Link packets from i to j").  One scan gives the
+//                          bucket's unique links (:181), max link packets (:183) and sum of counts
+//                          (:180), and emits one record per link and side, node<<32 | count, into
+//                          side buckets sb = top logB bits of hash32(node).
+//   S(w,side,sb)         : all records of side bucket sb (from every link bucket) are merged in an SMEM
+//                          table node -> (sum of counts, number of records): the row sums A_t 1 (:185)
+//                          and row nnz |A_t|_0 1 (:187) of those sources (or the column mirrors, :173).
+//                          A scan gives unique nodes (:184), max packets (:186), max fan (:188).
+//   F(w)                 : reduces the per-bucket partials of window w to the nine outputs.
+// Items are handed out by one global ticket counter in steps of IPS = 1 + 2B + B + cp tickets:
+// step k = F(k-LAG_F), S(k-LAG_S), L(k-LAG_L), P(k) (out-of-range windows are no-ops).  Every item
+// waits only on items with smaller tickets, so the schedule cannot deadlock; a scratch slot is reused
+// once its previous window is final (RSLOTS windows in flight).  Dependencies are counted
+// semaphores: __syncthreads() + red.release.gpu by one thread to signal, ld.acquire.gpu spin by one
+// thread + __syncthreads() to wait.
+#pragma once
+#include "nsg.h"
+#include "nsg_common.cuh"
+
+namespace nsg {
+
+constexpr int FT = 512;                      // threads per CTA; 2 CTAs per SM
+constexpr int NWARP = FT / 32;
+constexpr int KPT = 8;                       // elements per thread per round
+constexpr int CH = FT * KPT;                 // 4096 keys per chunk / per gather round
+constexpr int TCAP = 6144;                   // SMEM hash-table slots (slot = (h * TCAP) >> 32)
+constexpr int BUCKET_KEYS = 2048;            // target keys per link bucket (load factor ~1/3)
+constexpr int PCAP = 512;                    // pending-list capacity (entries) per insertion wave
+constexpr int MAX_LOGB = 9;
+constexpr int MAXB = 1 << MAX_LOGB;
+constexpr u64 FAST_MAX_WINDOW = (u64)BUCKET_KEYS << MAX_LOGB;  // 2^20
+constexpr int MAXCP = (int)(FAST_MAX_WINDOW / CH);
+constexpr int LAG_L = 4, LAG_S = 8, LAG_F = 11;  // pipeline lags (steps) of L, S, F items behind P
+constexpr int LOG_RSLOTS = 4;
+constexpr int RSLOTS = 1 << LOG_RSLOTS;      // scratch slots (windows in flight), > LAG_S
+constexpr u32 RCAP = 2 * (TCAP + 1) + 6;     // records per link bucket (both sides), 8-aligned
+
+// An entry waiting for its next probe: a = key (link table) or node | f<<32 (node table),
+// b = count (link) or p (node), probe = probe distance to try next.
+struct Pend { u64 a; u32 b; u32 probe; };
+
+static_assert(RSLOTS > LAG_F && LAG_F > LAG_S && LAG_S > LAG_L && LAG_L >= 1, "schedule lags");
+
+struct Geo {
+  u64 n, W, nw;
+  u32 logB, B, cp, cp_last, R;
+  u64 ips;          // tickets per step
+  u64 total_items;  // (nw + LAG_F) * ips
+  u32 flags;
+  u64* ticket;
+  u32* diag;
+  u64* prof;  // [3 item types][4] = {count, cycles, wait cycles, -} when NSG_FLAG_PROFILE
+  u32 *pdone, *ldone, *sdone, *fin, *ovf;
+  u64* kscr;  // [R][cp*CH]      keys, chunk-major, each chunk sorted by link bucket
+  u32* koff;  // [R][cp][B+1]    bucket offsets inside each chunk
+  u64* rscr;  // [R][B][RCAP]    link records of each link bucket, sorted by (side, side bucket)
+  u32* roff;  // [R][B][2B+1]    offsets of (side, side bucket) inside each link bucket's records
+  u32* lres;  // [R][B][4]       per link bucket: unique links, max count, sum of counts
+  u32* sres;  // [R][2][B][4]    per side bucket: unique nodes, max packets, max fan
+};
+
+struct SmemP { u64 stage[CH]; u32 hist[MAXB + 1]; };
+struct SmemL {
+  u64 lkey[TCAP]; u32 lcnt[TCAP]; Pend pend[2][PCAP]; u32 seg[MAXCP + 1]; u32 seglo[MAXCP]; u32 hist[2 * MAXB + 1];
+};
+struct SmemS { u32 key[TCAP]; u32 P[TCAP]; u32 F[TCAP]; Pend pend[2][PCAP]; u32 seg[MAXB + 1]; u32 seglo[MAXB]; };
+struct SmemMisc {
+  u32 wtmp[10 * NWARP];
+  u32 esc[4];  // [0] link-table escape count (key ~0); [1],[2] node-table escape P, F (node ~0)
+  u32 flag, dep;
+  u32 type, idx;
+  u32 pcnt[2];  // pending-list fill counters
+  u64 w;
+};
+constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+constexpr size_t MISC_BYTES = (sizeof(SmemMisc) + 15) & ~size_t(15);
+constexpr size_t FAST_SMEM = MISC_BYTES + cmax(sizeof(SmemP), cmax(sizeof(SmemL), sizeof(SmemS)));
+
+// ------------------------------------------------------------------------------------------
+// Block helpers
+// ------------------------------------------------------------------------------------------
+// In-place exclusive scan of a[0..n) by the whole CTA; afterwards a[n] = total.
+__device__ void block_exclusive_scan(u32* a, int n, u32* wtmp) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int per = (n + FT - 1) / FT;
+  const int b = min(t * per, n), e = min(b + per, n);
+  u32 s = 0;
+  for (int i = b; i < e; ++i) s += a[i];
+  u32 x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wtmp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    u32 v = lane < NWARP ? wtmp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane < NWARP) wtmp[lane] = v;
+  }
+  __syncthreads();
+  u32 run = x - s + (wid ? wtmp[wid - 1] : 0);
+  for (int i = b; i < e; ++i) {
+    const u32 v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  if (t == 0) a[n] = wtmp[NWARP - 1];
+  __syncthreads();
+}
+
+// Exclusive scan of a[0..n) in place by warp 0 (a[n] = total).  The caller brackets it with
+// __syncthreads(); n is small (chunks, buckets), so one warp beats a 3-barrier block scan.
+__device__ __forceinline__ void warp0_exclusive_scan(u32* a, int n) {
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const int per = (n + 31) >> 5;
+  const int b = min(lane * per, n), e = min(b + per, n);
+  u32 sum = 0;
+  for (int i = b; i < e; ++i) sum += a[i];
+  u32 x = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  u32 run = x - sum;
+  for (int i = b; i < e; ++i) {
+    const u32 v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  if (lane == 31) a[n] = x;
+}
+
+// Largest c in [0, n) with pre[c] <= i (pre is an exclusive prefix with pre[n] > i).
+__device__ __forceinline__ u32 find_seg(const u32* pre, u32 n, u32 i) {
+  u32 lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const u32 mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= i) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------------------------------------
+// SMEM hash tables, filled in dense "waves".  A claimed slot never changes key.  SMEM atomics
+// cost per warp-instruction, so a per-lane probe loop (whose later iterations run with a few lanes
+// active) is avoided: in wave 0 every entry tries its home slot with one full-warp CAS; entries
+// that find another key there are appended (warp-aggregated) to a compact pending list, and the
+// pending list is retried densely at the next probe position, wave after wave.
+// ------------------------------------------------------------------------------------------
+__device__ __forceinline__ u32 home_slot(u32 h) { return (u32)(((u64)h * (u64)TCAP) >> 32); }
+__device__ __forceinline__ u32 probe_slot(u32 home, u32 probe) {
+  const u32 x = home + probe;  // probe < TCAP
+  return x >= (u32)TCAP ? x - TCAP : x;
+}
+__device__ __forceinline__ u32 link_home(u64 key) { return home_slot((u32)hash64(key)); }
+// side buckets use the top bits of hash32(node), so the home slot uses an independent mix
+__device__ __forceinline__ u32 node_home(u32 node) { return home_slot(hash32(node ^ 0x9E3779B9u)); }
+
+// one attempt: true if the key now owns `slot` (inserted or already there) and was counted
+__device__ __forceinline__ bool link_try(u64* lkey, u32* lcnt, u64 key, u32 add, u32 slot) {
+  const u64 old = atomicCAS(reinterpret_cast<unsigned long long*>(&lkey[slot]), EMPTY64, key);
+  if (old == EMPTY64 || old == key) { atomicAdd(&lcnt[slot], add); return true; }
+  return false;
+}
+__device__ __forceinline__ bool node_try(u32* key, u32* P, u32* F, u32 node, u32 p, u32 f, u32 slot) {
+  const u32 old = atomicCAS(&key[slot], EMPTY32, node);
+  if (old == EMPTY32 || old == node) {
+    atomicAdd(&P[slot], p);
+    if (f) atomicAdd(&F[slot], f);
+    return true;
+  }
+  return false;
+}
+// rare path (pending list full): finish the probe sequence in this lane; false if the table is full
+__device__ __noinline__ bool link_finish(u64* lkey, u32* lcnt, u64 key, u32 add, u32 probe) {
+  const u32 home = link_home(key);
+  for (; probe < (u32)TCAP; ++probe)
+    if (link_try(lkey, lcnt, key, add, probe_slot(home, probe))) return true;
+  return false;
+}
+__device__ __noinline__ bool node_finish(u32* key, u32* P, u32* F, u32 node, u32 p, u32 f, u32 probe) {
+  const u32 home = node_home(node);
+  for (; probe < (u32)TCAP; ++probe)
+    if (node_try(key, P, F, node, p, f, probe_slot(home, probe))) return true;
+  return false;
+}
+
+// Warp-aggregated append of the lanes with `want` to pending list `list`; must be called by all
+// lanes of the warp.  Returns false for a lane whose entry did not fit (the caller finishes it).
+__device__ __forceinline__ bool pend_push(Pend* list, u32* cnt, bool want, const Pend& e) {
+  const u32 mask = __ballot_sync(0xffffffffu, want);
+  if (mask == 0) return true;
+  const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
+  u32 base = 0;
+  if (lane == leader) base = atomicAdd(cnt, (u32)__popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (!want) return true;
+  const u32 pos = base + __popc(mask & ((1u << lane) - 1u));
+  if (pos >= (u32)PCAP) return false;
+  list[pos] = e;
+  return true;
+}
+
+__device__ __forceinline__ u32 side_bucket(u32 node, u32 logB) { return logB ? hash32(node) >> (32 - logB) : 0u; }
+__device__ __forceinline__ u32 link_bucket(u64 key, u32 logB) { return logB ? (u32)(hash64(key) >> (64 - logB)) : 0u; }
+
+__device__ __forceinline__ void mark_overflow(const Geo& g, u64 w) {
+  if (atomicExch(&g.ovf[w], 1u) == 0u) atomicAdd(&g.diag[0], 1u);
+}
+
+__device__ __forceinline__ u32 chunks_of(const Geo& g, u64 w) { return w + 1 == g.nw ? g.cp_last : g.cp; }
+__device__ __forceinline__ u64 window_len(const Geo& g, u64 w) { return min(g.W, g.n - w * g.W); }
+__device__ __forceinline__ u32 slot_of(const Geo& g, u64 w) { return (u32)w & (g.R - 1); }
+
+// Spin (acquire) until *p >= v, starting from a first value `first` loaded earlier with
+// ld_acquire32 so that its latency overlapped other work.
+__device__ __forceinline__ long long wait_geq(const u32* p, u32 v, u32 first) {
+  if (first >= v) return 0;
+  const long long t0 = clock64();
+  while (ld_acquire32(p) < v) __nanosleep(32);
+  return clock64() - t0;
+}
+
+// Phase timer (NSG_FLAG_PROFILE): thread 0 adds the cycles since the previous mark to
+// prof[16 + type*16 + phase].  Marks are placed right after a __syncthreads().
+struct PhaseTimer {
+  long long last;
+  __device__ __forceinline__ PhaseTimer() { last = clock64(); }
+  __device__ __forceinline__ void mark(const Geo& g, int type, int phase) {
+    if ((g.flags & NSG_FLAG_PROFILE) && threadIdx.x == 0) {
+      const long long now = clock64();
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[16 + type * 16 + phase]), (unsigned long long)(now - last));
+      last = now;
+    }
+  }
+};
+
+__device__ __forceinline__ void prof_add(const Geo& g, int type, long long cyc, long long wait) {
+  if (g.flags & NSG_FLAG_PROFILE) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[type * 4 + 0]), 1ull);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[type * 4 + 1]), (unsigned long long)cyc);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[type * 4 + 2]), (unsigned long long)wait);
+    atomicMax(reinterpret_cast<unsigned long long*>(&g.prof[type * 4 + 3]), (unsigned long long)(cyc - wait));
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// P item: partition one chunk of window w by link bucket
+// ------------------------------------------------------------------------------------------
+__device__ void item_partition(const Geo& g, const u32* __restrict__ src, const u32* __restrict__ dst,
+                               const u64* __restrict__ keys, u64 w, u32 c, SmemP& s, SmemMisc& m) {
+  const int t = threadIdx.x;
+  PhaseTimer pt;
+  const long long tstart = clock64();
+  long long waited = 0;
+  u32 dep = 1;
+  if (t == 0 && w >= g.R) dep = ld_acquire32(&g.fin[w - g.R]);  // the slot's previous window is final
+  for (int i = t; i <= (int)g.B; i += FT) s.hist[i] = 0;
+  const u64 wbase = w * g.W;
+  const u64 wlen = min(g.W, g.n - wbase);
+  const u64 base = wbase + (u64)c * CH;
+  const u32 len = (u32)min((u64)CH, wlen - (u64)c * CH);
+  const u32 slot = slot_of(g, w);
+
+  // Full chunks with 16 B aligned bases use 128-bit loads (key order inside the chunk is irrelevant);
+  // otherwise element j of thread t is t + j*FT.
+  const bool full = len == CH;
+  u64 k[KPT];
+  if (keys) {
+    const u64* p = keys + base;
+    if (full && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+      const ulonglong2* p2 = reinterpret_cast<const ulonglong2*>(p);
+#pragma unroll
+      for (int j = 0; j < KPT / 2; ++j) {
+        const ulonglong2 v = __ldcs(p2 + t + j * FT);
+        k[2 * j] = v.x; k[2 * j + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) k[j] = (t + j * FT < (int)len) ? __ldcs(p + t + j * FT) : 0ull;
+    }
+  } else {
+    const u32* ps = src + base;
+    const u32* pd = dst + base;
+    if (full && ((reinterpret_cast<uintptr_t>(ps) & 15) == 0) && ((reinterpret_cast<uintptr_t>(pd) & 15) == 0)) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(ps);
+      const uint4* d4 = reinterpret_cast<const uint4*>(pd);
+#pragma unroll
+      for (int j = 0; j < KPT / 4; ++j) {
+        const uint4 a = __ldcs(s4 + t + j * FT);
+        const uint4 b = __ldcs(d4 + t + j * FT);
+        k[4 * j + 0] = ((u64)a.x << 32) | b.x;
+        k[4 * j + 1] = ((u64)a.y << 32) | b.y;
+        k[4 * j + 2] = ((u64)a.z << 32) | b.z;
+        k[4 * j + 3] = ((u64)a.w << 32) | b.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < KPT; ++j)
+        k[j] = (t + j * FT < (int)len) ? (((u64)__ldcs(ps + t + j * FT) << 32) | __ldcs(pd + t + j * FT)) : 0ull;
+    }
+  }
+  if (t == 0 && w >= g.R) waited = wait_geq(&g.fin[w - g.R], 1u, dep);
+  __syncthreads();  // hist cleared; thread 0's wait for the slot is published
+  pt.mark(g, 0, 0);
+#pragma unroll
+  for (int j = 0; j < KPT; ++j)
+    if (full || t + j * FT < (int)len) atomicAdd(&s.hist[link_bucket(k[j], g.logB)], 1u);
+  __syncthreads();
+  pt.mark(g, 0, 1);
+  block_exclusive_scan(s.hist, (int)g.B, m.wtmp);
+  u32* off = g.koff + ((u64)slot * g.cp + c) * (g.B + 1);
+  for (int i = t; i <= (int)g.B; i += FT) off[i] = s.hist[i];
+  __syncthreads();
+  pt.mark(g, 0, 2);
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    if (full || t + j * FT < (int)len) {
+      const u32 pos = atomicAdd(&s.hist[link_bucket(k[j], g.logB)], 1u);
+      s.stage[pos] = k[j];
+    }
+  }
+  __syncthreads();
+  pt.mark(g, 0, 3);
+  u64* out = g.kscr + (u64)slot * g.cp * CH + (u64)c * CH;
+  if (len == CH) {
+    ulonglong2* o2 = reinterpret_cast<ulonglong2*>(out);
+    const ulonglong2* s2 = reinterpret_cast<const ulonglong2*>(s.stage);
+#pragma unroll
+    for (int i = t; i < CH / 2; i += FT) o2[i] = s2[i];
+  } else {
+    for (u32 i = t; i < len; i += FT) out[i] = s.stage[i];
+  }
+  __syncthreads();
+  pt.mark(g, 0, 4);
+  if (t == 0) { red_release_add32(&g.pdone[w], 1u); prof_add(g, 0, clock64() - tstart, waited); }
+}
+
+// ------------------------------------------------------------------------------------------
+// L item: aggregate link bucket b of window w
+// ------------------------------------------------------------------------------------------
+// one attempt at `slot`; a new claim also counts the link's two records into the per-(side, side
+// bucket) histogram used to lay out the bucket's record region
+__device__ __forceinline__ bool link_try_h(u64* lkey, u32* lcnt, u32* hist, u32 B, u32 logB, u64 key, u32 add,
+                                           u32 slot) {
+  const u64 old = atomicCAS(reinterpret_cast<unsigned long long*>(&lkey[slot]), EMPTY64, key);
+  if (old == EMPTY64) {
+    atomicAdd(&hist[side_bucket((u32)(key >> 32), logB)], 1u);
+    atomicAdd(&hist[B + side_bucket((u32)key, logB)], 1u);
+  }
+  if (old == EMPTY64 || old == key) { atomicAdd(&lcnt[slot], add); return true; }
+  return false;
+}
+__device__ __noinline__ bool link_finish_h(u64* lkey, u32* lcnt, u32* hist, u32 B, u32 logB, u64 key, u32 add,
+                                           u32 probe) {
+  const u32 home = link_home(key);
+  for (; probe < (u32)TCAP; ++probe)
+    if (link_try_h(lkey, lcnt, hist, B, logB, key, add, probe_slot(home, probe))) return true;
+  return false;
+}
+
+constexpr u32 WAVE_TAIL = 64;  // pending entries below this finish per lane (no more CTA waves)
+
+__device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  PhaseTimer pt;
+  const u32 ncp = chunks_of(g, w);
+  const u32 B = g.B, logB = g.logB;
+  const long long tstart = clock64();
+  long long waited = 0;
+  u32 dep = 0;
+  if (t == 0) dep = ld_acquire32(&g.pdone[w]);  // latency overlaps the table init
+  {
+    ulonglong2* k2 = reinterpret_cast<ulonglong2*>(s.lkey);
+    uint4* c4 = reinterpret_cast<uint4*>(s.lcnt);
+    for (int i = t; i < TCAP / 2; i += FT) k2[i] = make_ulonglong2(EMPTY64, EMPTY64);
+    for (int i = t; i < TCAP / 4; i += FT) c4[i] = make_uint4(0, 0, 0, 0);
+  }
+  for (int i = t; i <= (int)(2 * B); i += FT) s.hist[i] = 0;
+  if (t < 4) m.esc[t] = 0;
+  if (t == 0) { m.flag = 0; waited = wait_geq(&g.pdone[w], g.cp, dep); }
+  __syncthreads();  // also publishes thread 0's acquire to the CTA
+  pt.mark(g, 1, 0);
+  const u32 slot = slot_of(g, w);
+  const u32* koff = g.koff + (u64)slot * g.cp * (B + 1);
+  for (u32 c = t; c < ncp; c += FT) {
+    const u32 lo = ldcg32(koff + (u64)c * (B + 1) + b), hi = ldcg32(koff + (u64)c * (B + 1) + b + 1);
+    s.seg[c] = hi - lo;
+    s.seglo[c] = c * CH + lo;
+  }
+  __syncthreads();
+  warp0_exclusive_scan(s.seg, (int)ncp);
+  __syncthreads();
+  pt.mark(g, 1, 1);
+  const u32 nb = s.seg[ncp];
+  const u64* ks = g.kscr + (u64)slot * g.cp * CH;
+  bool ok = true;
+  for (u32 base = 0; base < nb; base += CH) {  // CTA-uniform rounds of CH keys
+    u64 k[KPT];
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const u32 i = base + t + j * FT;
+      if (i < nb) {
+        const u32 c = find_seg(s.seg, ncp, i);
+        k[j] = ldcg64(ks + s.seglo[c] + (i - s.seg[c]));
+      }
+    }
+    if (t == 0) m.pcnt[0] = 0;
+    __syncthreads();
+    // wave 0: warp-leader aggregation (the lanes holding the first valid lane's key add once), then
+    // one full-warp CAS per entry at its home slot
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      if (base + j * FT >= nb) break;  // CTA-uniform
+      const bool valid = base + t + j * FT < nb;
+      const u32 vmask = __ballot_sync(0xffffffffu, valid);
+      const u64 lead = __shfl_sync(0xffffffffu, k[j], __ffs(vmask | 1u) - 1);
+      const u32 same = __ballot_sync(0xffffffffu, valid && k[j] == lead);
+      bool entry = valid;
+      u32 add = 1;
+      if (valid && k[j] == lead) { entry = lane == __ffs(same) - 1; add = (u32)__popc(same); }
+      if (entry && k[j] == EMPTY64) { atomicAdd(&m.esc[0], add); entry = false; }
+      bool placed = true;
+      if (entry) placed = link_try_h(s.lkey, s.lcnt, s.hist, B, logB, k[j], add, link_home(k[j]));
+      const Pend e{k[j], add, 1u};
+      if (!pend_push(s.pend[0], &m.pcnt[0], !placed, e))
+        ok = link_finish_h(s.lkey, s.lcnt, s.hist, B, logB, k[j], add, 1u) && ok;
+    }
+    __syncthreads();
+    // waves 1..: the pending list, densely, one probe further each wave; a short tail finishes per lane
+    int cur = 0;
+    u32 n = min(m.pcnt[0], (u32)PCAP);
+    while (n) {
+      if (n <= WAVE_TAIL) {
+        if ((u32)t < n) {
+          const Pend e = s.pend[cur][t];
+          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B, logB, e.a, e.b, e.probe) && ok;
+        }
+        break;
+      }
+      if (t == 0) m.pcnt[cur ^ 1] = 0;
+      __syncthreads();
+      for (u32 i0 = 0; i0 < n; i0 += FT) {
+        const u32 i = i0 + t;
+        const bool valid = i < n;
+        Pend e{0, 0, 0};
+        bool placed = true;
+        if (valid) {
+          e = s.pend[cur][i];
+          if (e.probe >= (u32)TCAP) ok = false;
+          else placed = link_try_h(s.lkey, s.lcnt, s.hist, B, logB, e.a, e.b, probe_slot(link_home(e.a), e.probe));
+        }
+        e.probe += 1;
+        if (!pend_push(s.pend[cur ^ 1], &m.pcnt[cur ^ 1], !placed, e))
+          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B, logB, e.a, e.b, e.probe) && ok;
+      }
+      __syncthreads();
+      cur ^= 1;
+      n = min(m.pcnt[cur], (u32)PCAP);
+    }
+  }
+  if (!ok) m.flag = 1;
+  if (t == 0 && m.esc[0]) {  // the key ~0 (255.255.255.255 -> 255.255.255.255) is one more link
+    atomicAdd(&s.hist[side_bucket(EMPTY32, logB)], 1u);
+    atomicAdd(&s.hist[B + side_bucket(EMPTY32, logB)], 1u);
+  }
+  __syncthreads();
+  pt.mark(g, 1, 2);
+  // record region layout: offsets of every (side, side bucket)
+  warp0_exclusive_scan(s.hist, (int)(2 * B));
+  __syncthreads();
+  u32* off = g.roff + ((u64)slot * B + b) * (2 * B + 1);
+  for (int i = t; i <= (int)(2 * B); i += FT) off[i] = s.hist[i];
+  pt.mark(g, 1, 3);
+  // One pass over the bucket's part of A_t: unique links (:181), max link packets (:183), sum of counts
+  // (:180); and one record per link and side, node<<32 | count.  (The barrier orders the offset copy
+  // above before the cursors move.)
+  __syncthreads();
+  u64* rec = g.rscr + ((u64)slot * B + b) * RCAP;
+  u32 nl = 0, mx = 0, sm = 0;
+  for (int i = t; i < TCAP; i += FT) {
+    const u64 key = s.lkey[i];
+    if (key != EMPTY64) {
+      const u32 c = s.lcnt[i];
+      nl += 1; mx = max(mx, c); sm += c;
+      const u32 sn = (u32)(key >> 32), dn = (u32)key;
+      rec[atomicAdd(&s.hist[side_bucket(sn, logB)], 1u)] = ((u64)sn << 32) | c;
+      rec[atomicAdd(&s.hist[B + side_bucket(dn, logB)], 1u)] = ((u64)dn << 32) | c;
+    }
+  }
+  if (t == 0 && m.esc[0]) {
+    const u32 c = m.esc[0];
+    nl += 1; mx = max(mx, c); sm += c;
+    const u64 r = ((u64)EMPTY32 << 32) | c;
+    rec[atomicAdd(&s.hist[side_bucket(EMPTY32, logB)], 1u)] = r;
+    rec[atomicAdd(&s.hist[B + side_bucket(EMPTY32, logB)], 1u)] = r;
+  }
+  nl = warp_sum(nl); mx = warp_max(mx); sm = warp_sum(sm);
+  if (lane == 0) { m.wtmp[4 * NWARP + wid] = nl; m.wtmp[5 * NWARP + wid] = mx; m.wtmp[6 * NWARP + wid] = sm; }
+  __syncthreads();
+  pt.mark(g, 1, 4);
+  if (t == 0) {
+    u32 a = 0, bm = 0, cs = 0;
+    for (int i = 0; i < NWARP; ++i) { a += m.wtmp[4 * NWARP + i]; bm = max(bm, m.wtmp[5 * NWARP + i]); cs += m.wtmp[6 * NWARP + i]; }
+    u32* r = g.lres + ((u64)slot * B + b) * 4;
+    r[0] = a; r[1] = bm; r[2] = cs;
+    if (m.flag) mark_overflow(g, w);
+    red_release_add32(&g.ldone[w], 1u);  // thread 0's own lres writes precede it in program order
+    prof_add(g, 1, clock64() - tstart, waited);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Window finalisation (run by the CTA that completes the window's last S item)
+// ------------------------------------------------------------------------------------------
+__device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict__ out) {
+  const int t = threadIdx.x;
+  const u32 slot = slot_of(g, w);
+  if (t == 0) wait_geq(&g.sdone[w], 2 * g.B, ld_acquire32(&g.sdone[w]));
+  __syncthreads();
+  // sums: 0 links, 1 sum of counts, 2 unique sources, 3 unique destinations;
+  // maxes: 4 max link, 5 max source packets, 6 max fan-out, 7 max destination packets, 8 max fan-in
+  u32 v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  for (u32 i = t; i < g.B; i += FT) {
+    const u32* r = g.lres + ((u64)slot * g.B + i) * 4;
+    v[0] += ldcg32(r); v[4] = max(v[4], ldcg32(r + 1)); v[1] += ldcg32(r + 2);
+    const u32* s0 = g.sres + (((u64)slot * 2 + 0) * g.B + i) * 4;
+    const u32* s1 = g.sres + (((u64)slot * 2 + 1) * g.B + i) * 4;
+    v[2] += ldcg32(s0); v[5] = max(v[5], ldcg32(s0 + 1)); v[6] = max(v[6], ldcg32(s0 + 2));
+    v[3] += ldcg32(s1); v[7] = max(v[7], ldcg32(s1 + 1)); v[8] = max(v[8], ldcg32(s1 + 2));
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v[j] = warp_sum(v[j]);
+#pragma unroll
+  for (int j = 4; j < 9; ++j) v[j] = warp_max(v[j]);
+  const int lane = t & 31, wid = t >> 5;
+  __syncthreads();
+  if (lane == 0)
+    for (int j = 0; j < 9; ++j) m.wtmp[j * NWARP + wid] = v[j];
+  __syncthreads();
+  if (t == 0) {
+    u32 r[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < NWARP; ++i) {
+      for (int j = 0; j < 4; ++j) r[j] += m.wtmp[j * NWARP + i];
+      for (int j = 4; j < 9; ++j) r[j] = max(r[j], m.wtmp[j * NWARP + i]);
+    }
+    const u64 wlen = min(g.W, g.n - w * g.W);
+    u64* o = out + w * NSG_NUM_STATS;
+    o[NSG_VALID_PACKETS] = r[1];
+    o[NSG_UNIQUE_LINKS] = r[0];
+    o[NSG_MAX_LINK_PACKETS] = r[4];
+    o[NSG_UNIQUE_SOURCES] = r[2];
+    o[NSG_MAX_SOURCE_PACKETS] = r[5];
+    o[NSG_MAX_SOURCE_FANOUT] = r[6];
+    o[NSG_UNIQUE_DESTINATIONS] = r[3];
+    o[NSG_MAX_DESTINATION_PACKETS] = r[7];
+    o[NSG_MAX_DESTINATION_FANIN] = r[8];
+    if ((u64)r[1] != wlen && ld_acquire32(&g.ovf[w]) == 0) atomicAdd(&g.diag[1], 1u);
+    if ((g.flags & NSG_FLAG_INJECT_OVERFLOW) && (w & 1)) mark_overflow(g, w);
+    st_release32(&g.fin[w], 1u);  // the slot may be reused: every reader of it has signalled sdone
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// S item: merge side bucket sb of one side of window w
+// ------------------------------------------------------------------------------------------
+__device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemMisc& m) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  PhaseTimer pt;
+  const u32 B = g.B;
+  const long long tstart = clock64();
+  long long waited = 0;
+  u32 dep = 0;
+  if (t == 0) dep = ld_acquire32(&g.ldone[w]);
+  {
+    uint4* k4 = reinterpret_cast<uint4*>(s.key);
+    uint4* p4 = reinterpret_cast<uint4*>(s.P);
+    uint4* f4 = reinterpret_cast<uint4*>(s.F);
+    for (int i = t; i < TCAP / 4; i += FT) {
+      k4[i] = make_uint4(EMPTY32, EMPTY32, EMPTY32, EMPTY32);
+      p4[i] = make_uint4(0, 0, 0, 0);
+      f4[i] = make_uint4(0, 0, 0, 0);
+    }
+  }
+  if (t < 4) m.esc[t] = 0;
+  if (t == 0) { m.flag = 0; waited = wait_geq(&g.ldone[w], B, dep); }
+  __syncthreads();
+  pt.mark(g, 2, 0);
+  const u32 slot = slot_of(g, w);
+  for (u32 b = t; b < B; b += FT) {
+    const u32* off = g.roff + ((u64)slot * B + b) * (2 * B + 1) + side * B;
+    const u32 lo = ldcg32(off + sb), hi = ldcg32(off + sb + 1);
+    s.seg[b] = hi - lo;
+    s.seglo[b] = b * RCAP + lo;
+  }
+  __syncthreads();
+  warp0_exclusive_scan(s.seg, (int)B);
+  __syncthreads();
+  pt.mark(g, 2, 1);
+  const u32 nr = s.seg[B];
+  const u64* rs = g.rscr + (u64)slot * B * RCAP;
+  bool ok = true;
+  for (u32 base = 0; base < nr; base += CH) {
+    u64 r[KPT];
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const u32 i = base + t + j * FT;
+      if (i < nr) {
+        const u32 bb = find_seg(s.seg, B, i);
+        r[j] = ldcg64(rs + s.seglo[bb] + (i - s.seg[bb]));
+      }
+    }
+    if (t == 0) m.pcnt[0] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      if (base + j * FT >= nr) break;  // CTA-uniform
+      const bool valid = base + t + j * FT < nr;
+      const u32 vmask = __ballot_sync(0xffffffffu, valid);
+      const u32 node = (u32)(r[j] >> 32);
+      u32 p = (u32)r[j], f = 1;
+      // warp-leader aggregation: a hot node (e.g. the heavy source) is merged once per warp
+      const u32 lead = __shfl_sync(0xffffffffu, node, __ffs(vmask | 1u) - 1);
+      const u32 same = __ballot_sync(0xffffffffu, valid && node == lead);
+      bool entry = valid;
+      if (valid && node == lead) {
+        const u32 sum = __reduce_add_sync(same, p);
+        entry = lane == __ffs(same) - 1;
+        p = sum; f = (u32)__popc(same);
+      }
+      if (entry && node == EMPTY32) { atomicAdd(&m.esc[1], p); atomicAdd(&m.esc[2], f); entry = false; }
+      bool placed = true;
+      if (entry) placed = node_try(s.key, s.P, s.F, node, p, f, node_home(node));
+      const Pend e{(u64)node | ((u64)f << 32), p, 1u};
+      if (!pend_push(s.pend[0], &m.pcnt[0], !placed, e)) ok = node_finish(s.key, s.P, s.F, node, p, f, 1u) && ok;
+    }
+    __syncthreads();
+    int cur = 0;
+    u32 n = min(m.pcnt[0], (u32)PCAP);
+    while (n) {
+      if (n <= WAVE_TAIL) {
+        if ((u32)t < n) {
+          const Pend e = s.pend[cur][t];
+          ok = node_finish(s.key, s.P, s.F, (u32)e.a, e.b, (u32)(e.a >> 32), e.probe) && ok;
+        }
+        break;
+      }
+      if (t == 0) m.pcnt[cur ^ 1] = 0;
+      __syncthreads();
+      for (u32 i0 = 0; i0 < n; i0 += FT) {
+        const u32 i = i0 + t;
+        const bool valid = i < n;
+        Pend e{0, 0, 0};
+        bool placed = true;
+        if (valid) {
+          e = s.pend[cur][i];
+          if (e.probe >= (u32)TCAP) ok = false;
+          else placed = node_try(s.key, s.P, s.F, (u32)e.a, e.b, (u32)(e.a >> 32), probe_slot(node_home((u32)e.a), e.probe));
+        }
+        e.probe += 1;
+        if (!pend_push(s.pend[cur ^ 1], &m.pcnt[cur ^ 1], !placed, e))
+          ok = node_finish(s.key, s.P, s.F, (u32)e.a, e.b, (u32)(e.a >> 32), e.probe) && ok;
+      }
+      __syncthreads();
+      cur ^= 1;
+      n = min(m.pcnt[cur], (u32)PCAP);
+    }
+  }
+  if (!ok) m.flag = 1;
+  __syncthreads();
+  pt.mark(g, 2, 2);
+  // unique nodes (1^T|A_t 1|_0 or its mirror), max packets (max A_t 1), max fan (max |A_t|_0 1)
+  u32 d = 0, mp = 0, mf = 0;
+  for (int i = t; i < TCAP; i += FT) {
+    if (s.key[i] != EMPTY32) { d += 1; mp = max(mp, s.P[i]); mf = max(mf, s.F[i]); }
+  }
+  if (t == 0 && m.esc[1]) { d += 1; mp = max(mp, m.esc[1]); mf = max(mf, m.esc[2]); }
+  d = warp_sum(d); mp = warp_max(mp); mf = warp_max(mf);
+  if (lane == 0) { m.wtmp[4 * NWARP + wid] = d; m.wtmp[5 * NWARP + wid] = mp; m.wtmp[6 * NWARP + wid] = mf; }
+  __syncthreads();
+  pt.mark(g, 2, 3);
+  if (t == 0) {
+    u32 a = 0, bp = 0, cf = 0;
+    for (int i = 0; i < NWARP; ++i) { a += m.wtmp[4 * NWARP + i]; bp = max(bp, m.wtmp[5 * NWARP + i]); cf = max(cf, m.wtmp[6 * NWARP + i]); }
+    u32* res = g.sres + (((u64)slot * 2 + side) * B + sb) * 4;
+    res[0] = a; res[1] = bp; res[2] = cf;
+    if (m.flag) mark_overflow(g, w);
+    red_release_add32(&g.sdone[w], 1u);  // thread 0 wrote res itself: program order + release
+    prof_add(g, 2, clock64() - tstart, waited);
+  }
+}
+// ------------------------------------------------------------------------------------------
+// Ticket decoding: step k = tk / ips holds F(k-LAG_F), S(k-LAG_S) [2B], L(k-LAG_L) [B], P(k) [cp].
+// ------------------------------------------------------------------------------------------
+enum : u32 { ITEM_P = 0, ITEM_L = 1, ITEM_S0 = 2, ITEM_S1 = 3, ITEM_F = 4, ITEM_NOP = 5, ITEM_DONE = 6 };
+
+__device__ __forceinline__ void decode_ticket(const Geo& g, u64 tk, SmemMisc& m) {
+  if (tk >= g.total_items) { m.type = ITEM_DONE; return; }
+  const u64 k = tk / g.ips;
+  u64 idx = tk - k * g.ips;
+  u64 w;
+  u32 type;
+  if (idx == 0) { type = ITEM_F; w = k - LAG_F; }
+  else if ((idx -= 1) < 2ull * g.B) { type = idx < g.B ? ITEM_S0 : ITEM_S1; idx &= g.B - 1; w = k - LAG_S; }
+  else if ((idx -= 2ull * g.B) < g.B) { type = ITEM_L; w = k - LAG_L; }
+  else { idx -= g.B; type = ITEM_P; w = k; }
+  // windows before the first step of a class (w wrapped below 0) or past the end are no-ops, except
+  // that P items beyond the last window's chunks still signal so L items can wait for a full count
+  if (w >= g.nw) type = ITEM_NOP;
+  m.type = type; m.w = w; m.idx = (u32)idx;
+}
+
+__global__ void __launch_bounds__(FT, 2)
+fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, const u64* __restrict__ keys,
+            u64* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SmemMisc& m = *reinterpret_cast<SmemMisc*>(smem_raw);
+  unsigned char* u = smem_raw + MISC_BYTES;
+  u64 next = 0;  // thread 0: the next ticket, fetched one item ahead so its latency is hidden
+  if (threadIdx.x == 0) next = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
+  for (;;) {
+    if (threadIdx.x == 0) {
+      decode_ticket(g, next, m);
+      if (m.type != ITEM_DONE) next = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
+    }
+    __syncthreads();
+    const u32 type = m.type, idx = m.idx;
+    const u64 w = m.w;
+    if (type == ITEM_DONE) break;
+    // every item function passes a __syncthreads() before thread 0 can overwrite m.type/m.w/m.idx
+    if (type == ITEM_P) {
+      if (idx < chunks_of(g, w)) {
+        item_partition(g, src, dst, keys, w, idx, *reinterpret_cast<SmemP*>(u), m);
+      } else {  // a chunk past the end of the last (short) window: count it done
+        if (threadIdx.x == 0) red_release_add32(&g.pdone[w], 1u);
+        __syncthreads();
+      }
+    } else if (type == ITEM_L) {
+      item_link(g, w, idx, *reinterpret_cast<SmemL*>(u), m);
+    } else if (type == ITEM_S0 || type == ITEM_S1) {
+      item_side(g, w, (int)(type - ITEM_S0), idx, *reinterpret_cast<SmemS*>(u), m);
+    } else if (type == ITEM_F) {
+      item_finalize(g, w, m, out);
+    } else {
+      __syncthreads();  // no-op ticket
+    }
+  }
+}
+
+}  // namespace nsg

@@ -1,0 +1,142 @@
+// nsg_global.cuh — the L2 path of libnsg: one CTA per window with global-memory hash tables.
+// Used for windows larger than the fast path supports and as the fast path's overflow hand-off.
+// Same definitions as the fast path (Table 2; mirrors line 173).
+#pragma once
+#include "nsg.h"
+#include "nsg_common.cuh"
+
+namespace nsg {
+
+constexpr int GT = 512;
+
+struct GGeo {
+  u64 n, W, nw;
+  u64 LC;       // slots per table (power of two >= 2*W)
+  u32 G;        // table sets
+  int only_overflowed;
+  u64* lkey;    // [G][LC]
+  u32* lcnt;    // [G][LC]
+  u32* nkey;    // [G][2][LC]
+  u32* nP;      // [G][2][LC]
+  u32* nF;      // [G][2][LC]
+  const u32* ovf;
+  u32* diag;
+};
+
+__device__ __forceinline__ void glob_link_insert(u64* lkey, u32* lcnt, u64 LC, u64 key) {
+  u64 slot = hash64(key) & (LC - 1);
+  for (;;) {
+    u64 k = ldcg64(&lkey[slot]);
+    if (k == EMPTY64) {
+      const u64 old = atomicCAS(reinterpret_cast<unsigned long long*>(&lkey[slot]), EMPTY64, key);
+      k = (old == EMPTY64) ? key : old;
+    }
+    if (k == key) { atomicAdd(&lcnt[slot], 1u); return; }
+    slot = (slot + 1) & (LC - 1);  // the table has >= 2x the window's slots: never full
+  }
+}
+
+__device__ __forceinline__ void glob_node_upsert(u32* key, u32* P, u32* F, u64 LC, u32* escP, u32* escF, u32 node,
+                                                 u32 p, u32 f) {
+  if (node == EMPTY32) { atomicAdd(escP, p); atomicAdd(escF, f); return; }
+  u64 slot = ((u64)hash32(node) * 0x9E3779B97F4A7C15ull >> 11) & (LC - 1);
+  for (;;) {
+    u32 k = ldcg32(&key[slot]);
+    if (k == EMPTY32) {
+      const u32 old = atomicCAS(&key[slot], EMPTY32, node);
+      k = (old == EMPTY32) ? node : old;
+    }
+    if (k == node) { atomicAdd(&P[slot], p); atomicAdd(&F[slot], f); return; }
+    slot = (slot + 1) & (LC - 1);
+  }
+}
+
+__global__ void __launch_bounds__(GT)
+global_kernel(GGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, const u64* __restrict__ keys,
+              u64* __restrict__ out) {
+  __shared__ u32 esc[5];
+  __shared__ u32 red[9 * (GT / 32)];
+  if (g.only_overflowed && ldcg32(&g.diag[0]) == 0) return;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const u64 LC = g.LC;
+  u64* lkey = g.lkey + (u64)blockIdx.x * LC;
+  u32* lcnt = g.lcnt + (u64)blockIdx.x * LC;
+  for (u64 w = blockIdx.x; w < g.nw; w += g.G) {
+    if (g.only_overflowed && ldcg32(&g.ovf[w]) == 0) continue;
+    const u64 base = w * g.W;
+    const u64 len = min(g.W, g.n - base);
+    for (u64 i = t; i < LC; i += GT) {
+      lkey[i] = EMPTY64; lcnt[i] = 0;
+      for (int sd = 0; sd < 2; ++sd) {
+        const u64 o = ((u64)blockIdx.x * 2 + sd) * LC + i;
+        g.nkey[o] = EMPTY32; g.nP[o] = 0; g.nF[o] = 0;
+      }
+    }
+    if (t < 5) esc[t] = 0;
+    __syncthreads();
+    for (u64 i = t; i < len; i += GT) {
+      const u64 key = keys ? keys[base + i] : (((u64)src[base + i] << 32) | dst[base + i]);
+      if (key == EMPTY64) atomicAdd(&esc[0], 1u);
+      else glob_link_insert(lkey, lcnt, LC, key);
+    }
+    __syncthreads();
+    u32* k0 = g.nkey + ((u64)blockIdx.x * 2 + 0) * LC;
+    u32* k1 = g.nkey + ((u64)blockIdx.x * 2 + 1) * LC;
+    u32* P0 = g.nP + ((u64)blockIdx.x * 2 + 0) * LC;
+    u32* P1 = g.nP + ((u64)blockIdx.x * 2 + 1) * LC;
+    u32* F0 = g.nF + ((u64)blockIdx.x * 2 + 0) * LC;
+    u32* F1 = g.nF + ((u64)blockIdx.x * 2 + 1) * LC;
+    u32 nl = 0, mx = 0, sm = 0;
+    for (u64 i = t; i < LC; i += GT) {
+      const u64 key = ldcg64(&lkey[i]);
+      if (key != EMPTY64) {
+        const u32 c = ldcg32(&lcnt[i]);
+        nl += 1; mx = max(mx, c); sm += c;
+        glob_node_upsert(k0, P0, F0, LC, &esc[1], &esc[2], (u32)(key >> 32), c, 1);
+        glob_node_upsert(k1, P1, F1, LC, &esc[3], &esc[4], (u32)key, c, 1);
+      }
+    }
+    if (t == 0 && esc[0]) {
+      const u32 c = esc[0];
+      nl += 1; mx = max(mx, c); sm += c;
+      atomicAdd(&esc[1], c); atomicAdd(&esc[2], 1u); atomicAdd(&esc[3], c); atomicAdd(&esc[4], 1u);
+    }
+    __syncthreads();
+    u32 d0 = 0, p0 = 0, f0 = 0, d1 = 0, p1 = 0, f1 = 0;
+    for (u64 i = t; i < LC; i += GT) {
+      if (ldcg32(&k0[i]) != EMPTY32) { d0 += 1; p0 = max(p0, ldcg32(&P0[i])); f0 = max(f0, ldcg32(&F0[i])); }
+      if (ldcg32(&k1[i]) != EMPTY32) { d1 += 1; p1 = max(p1, ldcg32(&P1[i])); f1 = max(f1, ldcg32(&F1[i])); }
+    }
+    if (t == 0 && esc[1]) { d0 += 1; p0 = max(p0, esc[1]); f0 = max(f0, esc[2]); }
+    if (t == 0 && esc[3]) { d1 += 1; p1 = max(p1, esc[3]); f1 = max(f1, esc[4]); }
+    u32 v[9] = {nl, sm, d0, d1, mx, p0, f0, p1, f1};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = warp_sum(v[j]);
+#pragma unroll
+    for (int j = 4; j < 9; ++j) v[j] = warp_max(v[j]);
+    if (lane == 0)
+      for (int j = 0; j < 9; ++j) red[j * (GT / 32) + wid] = v[j];
+    __syncthreads();
+    if (t == 0) {
+      u32 r[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+      for (int i = 0; i < GT / 32; ++i) {
+        for (int j = 0; j < 4; ++j) r[j] += red[j * (GT / 32) + i];
+        for (int j = 4; j < 9; ++j) r[j] = max(r[j], red[j * (GT / 32) + i]);
+      }
+      u64* o = out + w * NSG_NUM_STATS;
+      o[NSG_VALID_PACKETS] = r[1];
+      o[NSG_UNIQUE_LINKS] = r[0];
+      o[NSG_MAX_LINK_PACKETS] = r[4];
+      o[NSG_UNIQUE_SOURCES] = r[2];
+      o[NSG_MAX_SOURCE_PACKETS] = r[5];
+      o[NSG_MAX_SOURCE_FANOUT] = r[6];
+      o[NSG_UNIQUE_DESTINATIONS] = r[3];
+      o[NSG_MAX_DESTINATION_PACKETS] = r[7];
+      o[NSG_MAX_DESTINATION_FANIN] = r[8];
+      if ((u64)r[1] != len) atomicAdd(&g.diag[1], 1u);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace nsg
