@@ -1,0 +1,331 @@
+#!/usr/bin/env python3
+"""Benchmark of the per-window Network Sensing Graph Challenge path (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C2|C3|C1]
+
+One step = one pass of the whole hot path (partition -> link buckets -> side buckets -> the nine
+statistics of every window) over one C2-sized batch: 64 windows x 2^17 packets per GPU (weak
+scaling), Zipf(s=1.1, K=2^20) IPv4 pairs from the seeded counter-based generator, generated on the
+device.  Steps cycle through a 1 GiB ring of 16 such batches per GPU, so every step reads inputs
+that are not L2-resident (126 MB L2).  For N > 1 (torchrun, one rank per GPU, NCCL) each rank owns
+its own window blocks and the 72 B/window results are all-gathered every step.
+
+The JSON line carries: value (device-timed aggregate packets/s, max over ranks), e2e (the same
+metric through the public API from pinned HOST buffers, H2D + D2H inside the timed region),
+roofline (HBM: 8 B/packet + 72 B/window algorithmic bytes over the persistent kernel's CUDA-event
+time), cpu_baseline (the CPU oracle on a bounded sample, rank 0 at N=1), clocks and gpu_launches.
+`--impl reference` times the CPU oracle itself (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "packets/sec (device-timed, max over ranks) at 1/2/4/8 B200; HBM GB/s vs peak"
+UNIT = "packets/s"
+WINDOW = 1 << 17
+WINDOWS_PER_STEP = 64
+RING = 16
+BYTES_PER_PACKET = 8          # algorithmic: one packed u64 key (src<<32|dst) read once
+BYTES_PER_WINDOW_OUT = 72     # nine u64 per window written
+
+
+def workload(name: str):
+    import gen
+
+    if name == "C2":
+        return gen.Dist("zipf", 1.1, 1 << 20), 2, "C2: Zipf(s=1.1, K=2^20) IPv4 pairs, seed 2"
+    if name == "C3":
+        return gen.Dist("heavy"), 3, "C3: heavy skew (Bernoulli(1/2) source 10.0.0.1, uniform dst), seed 3"
+    if name == "C1":
+        return gen.Dist("uniform"), 1, "C1-shaped: uniform 32-bit src/dst, seed 1"
+    raise SystemExit(f"unknown workload {name}")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy, burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_per_launch(workload_name: str):
+    """dram__bytes_read+write per launch of the persistent kernel from a committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        e = t.get(workload_name)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.gpu)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            if len(r) >= 9:
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(dist, seed, budget_s: float = 10.0):
+    """The CPU oracle (O2, all host threads) on a bounded sample of the same workload."""
+    import gen
+    import oracle
+
+    threads = oracle.hardware_threads()
+    done_pkts, t_total, w = 0, 0.0, 0
+    batch = WINDOWS_PER_STEP
+    while t_total < budget_s and w < 16 * batch:
+        keys = gen.generate_host(dist, seed, w * WINDOW, batch * WINDOW, packed=True)
+        t0 = time.perf_counter()
+        oracle.window_stats_sort(keys=keys, window=WINDOW, threads=threads)
+        t_total += time.perf_counter() - t0
+        done_pkts += batch * WINDOW
+        w += batch
+    return {"value": done_pkts / t_total, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"{w} windows x 2^17 packets of the same stream (O2 std::sort oracle, {threads} threads, "
+                      f"{t_total:.1f} s)"}
+
+
+def run_reference(args):
+    """Reference arm of this tier: the CPU oracle as it stands, timed on the host cores."""
+    import gen
+    import oracle
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    dist_, seed, desc = workload(args.workload)
+    threads = oracle.hardware_threads()
+    per_step = 8  # windows per reference step: a bounded sample of the workload
+    samples = [gen.generate_host(dist_, seed, i * per_step * WINDOW, per_step * WINDOW, packed=True)
+               for i in range(min(4, args.steps + args.warmup))]
+    for i in range(args.warmup):
+        oracle.window_stats_sort(keys=samples[i % len(samples)], window=WINDOW, threads=threads)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        oracle.window_stats_sort(keys=samples[i % len(samples)], window=WINDOW, threads=threads)
+    dt = time.perf_counter() - t0
+    pkts = args.steps * per_step * WINDOW
+    value = pkts / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": desc + f" ({per_step} windows of 2^17 packets per step: bounded CPU sample)",
+                   "window": WINDOW},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": f"{per_step} windows per step x {args.steps} steps, O2 oracle, {threads} threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--once", action="store_true", help="a single untimed call (for ncu)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as tdist
+
+    import gen
+    import paper_2509_03653_b200 as nsg
+    from paper_2509_03653_b200.distributed import gather_window_stats
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N>1 must be launched with torchrun (one rank per GPU)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        tdist.init_process_group("nccl", device_id=dev)
+    dist_, seed, desc = workload(args.workload)
+
+    n = WINDOWS_PER_STEP * WINDOW
+    # this rank's ring: batch i of rank r covers packets [((i * world) + r) * n, ...) of the stream
+    ring = torch.empty((RING, n), dtype=torch.int64, device=dev)
+    for i in range(RING):
+        gen.generate_device(dist_, seed, ((i * world) + rank) * n, n, keys=ring[i])
+    torch.cuda.synchronize(dev)
+    ws = nsg.Workspace(n, WINDOW, dev)
+    outs = [torch.empty((WINDOWS_PER_STEP, 9), dtype=torch.int64, device=dev) for _ in range(RING)]
+    if args.once:
+        nsg.window_stats_packed(ring[0], WINDOW, out=outs[0], workspace=ws)
+        torch.cuda.synchronize(dev)
+        return 0
+
+    def step(i, evs=None):
+        r = nsg.window_stats_packed(ring[i % RING], WINDOW, out=outs[i % RING], workspace=ws, kernel_events=evs)
+        if world > 1:
+            gather_window_stats(r, WINDOWS_PER_STEP * world)
+        return r
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+    launches = nsg.last_launches()
+    diag = ws.diag()
+
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize(dev)
+    wall0 = time.perf_counter()
+    start.record()
+    for i in range(args.steps):
+        step(i, kev[i])
+    end.record()
+    torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - wall0
+    if world > 1:
+        tdist.barrier()
+    clocks = sampler.stop() if sampler else None
+    t_ms = start.elapsed_time(end)
+    k_ms = [a.elapsed_time(b) for a, b in kev]
+    k_avg = sum(k_ms) / len(k_ms)
+    if world > 1:
+        tt = torch.tensor([t_ms, k_avg], dtype=torch.float64, device=dev)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        t_ms, k_avg = float(tt[0]), float(tt[1])
+    total_pkts = n * world * args.steps
+    value = total_pkts / (t_ms / 1e3)
+
+    # ---- e2e: the public API from pinned host buffers (H2D of the keys + D2H of the result inside)
+    host = ring[0].cpu().pin_memory()
+    keys_dev = torch.empty(n, dtype=torch.int64, device=dev)
+    out_host = torch.empty((WINDOWS_PER_STEP, 9), dtype=torch.int64, pin_memory=True)
+    e2e_steps = max(3, min(args.steps, 50))
+    for _ in range(2):
+        nsg.window_stats_from_host(host, WINDOW, device=dev, keys_dev=keys_dev, out=outs[0], out_host=out_host,
+                                   workspace=ws)
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_steps):
+        nsg.window_stats_from_host(host, WINDOW, device=dev, keys_dev=keys_dev, out=outs[0], out_host=out_host,
+                                   workspace=ws)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        e2e_ms = float(tt[0])
+    e2e_value = n * world * e2e_steps / (e2e_ms / 1e3)
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        alg_bytes = n * BYTES_PER_PACKET + WINDOWS_PER_STEP * BYTES_PER_WINDOW_OUT
+        achieved = alg_bytes / (k_avg / 1e3) / 1e9
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(dist_, seed)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": desc + f"; {WINDOWS_PER_STEP} windows x 2^17 packets per GPU per step (C2 batch)",
+                       "window": WINDOW, "packets_per_gpu_per_step": n, "parallelism": f"windows sharded dp{world}",
+                       "l2": f"inputs larger than L2: ring of {RING} x {n * 8 >> 20} MiB batches per GPU, no flush",
+                       "input": "device-resident packed u64 keys (src<<32|dst)"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 8,
+                    "d2h_bytes_per_step": WINDOWS_PER_STEP * 9 * 8, "steps": e2e_steps},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic_per_launch(args.workload), "peak_source": peak_src,
+                         "kernel": "nsg::fast_kernel", "kernel_ms_avg": k_avg,
+                         "algorithmic_bytes_per_launch": alg_bytes},
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+            "gpu_launches": launches * args.steps,
+            "wall_s_timed_region": wall,
+            "diag": diag,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -106,6 +106,14 @@ nsg_status nsg_window_stats_ex(const uint32_t* src, const uint32_t* dst, const u
                                uint64_t window, uint64_t* out, void* workspace, size_t workspace_bytes,
                                void* stream, uint32_t flags);
 
+/* nsg_window_stats_ex plus measurement hooks: ev_before / ev_after (cudaEvent_t as void*, may be NULL)
+ * are recorded on `stream` immediately before and after the main kernel (the persistent fast-path
+ * kernel, or the L2-path kernel), excluding the workspace reset and the overflow-check launch, so a
+ * caller can time the dominant kernel with CUDA events without changing the work. */
+nsg_status nsg_window_stats_timed(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
+                                  uint64_t window, uint64_t* out, void* workspace, size_t workspace_bytes,
+                                  void* stream, uint32_t flags, void* ev_before, void* ev_after);
+
 /* Diagnostics of the last call that used `workspace` (device memory; read it after the stream has
  * completed the call): byte offset inside the workspace of a u32[4] =
  *   {windows the fast path handed to the L2 path because an SMEM table would overflow,

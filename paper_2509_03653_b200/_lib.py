@@ -24,6 +24,7 @@ EXPORTS = (
     "nsg_window_stats",
     "nsg_window_stats_packed",
     "nsg_window_stats_ex",
+    "nsg_window_stats_timed",
     "nsg_diag_offset",
     "nsg_last_launches",
     "nsg_status_string",
@@ -75,6 +76,8 @@ def load() -> ctypes.CDLL:
     lib.nsg_window_stats_packed.argtypes = [vp, u64, u64, vp, vp, sz, vp]
     lib.nsg_window_stats_ex.restype = ctypes.c_int
     lib.nsg_window_stats_ex.argtypes = [vp, vp, vp, u64, u64, vp, vp, sz, vp, u32]
+    lib.nsg_window_stats_timed.restype = ctypes.c_int
+    lib.nsg_window_stats_timed.argtypes = [vp, vp, vp, u64, u64, vp, vp, sz, vp, u32, vp, vp]
     lib.nsg_diag_offset.restype = sz
     lib.nsg_diag_offset.argtypes = []
     lib.nsg_last_launches.restype = ctypes.c_uint

@@ -109,7 +109,7 @@ def _check(t: torch.Tensor, name: str, dtypes) -> None:
         raise ValueError(f"{name} must be a contiguous 1-D tensor")
 
 
-def _launch(src, dst, keys, n, window, out, workspace, stream, flags, device):
+def _launch(src, dst, keys, n, window, out, workspace, stream, flags, device, events=None):
     window = int(window)
     if window < 1 or window > MAX_WINDOW:
         raise ValueError(f"window must be in [1, 2^31], got {window}")
@@ -123,13 +123,19 @@ def _launch(src, dst, keys, n, window, out, workspace, stream, flags, device):
         return out
     ws = _workspace(n, window, device, workspace)
     s = stream if stream is not None else torch.cuda.current_stream(device)
-    rc = _lib.nsg_window_stats_ex(
+    ev0 = ev1 = None
+    if events is not None:
+        for e in events:
+            if not e.cuda_event:  # torch creates the cudaEvent_t lazily, on first record
+                e.record(s)
+        ev0, ev1 = (ctypes.c_void_p(e.cuda_event) for e in events)
+    rc = _lib.nsg_window_stats_timed(
         None if src is None else src.data_ptr(),
         None if dst is None else dst.data_ptr(),
         None if keys is None else keys.data_ptr(),
-        n, window, out.data_ptr(), ws.ptr, ws.nbytes, ctypes.c_void_p(s.cuda_stream), int(flags))
+        n, window, out.data_ptr(), ws.ptr, ws.nbytes, ctypes.c_void_p(s.cuda_stream), int(flags), ev0, ev1)
     if rc != 0:
-        raise NsgError(rc, "nsg_window_stats_ex")
+        raise NsgError(rc, "nsg_window_stats_timed")
     return out
 
 
@@ -147,10 +153,16 @@ def window_stats(src: torch.Tensor, dst: torch.Tensor, window: int = DEFAULT_WIN
 
 
 def window_stats_packed(keys: torch.Tensor, window: int = DEFAULT_WINDOW, *, out=None,
-                        workspace: Optional[Workspace] = None, stream=None, flags: int = 0) -> torch.Tensor:
-    """Nine quantities per window of packed keys[i] = src<<32 | dst (device int64/uint64)."""
+                        workspace: Optional[Workspace] = None, stream=None, flags: int = 0,
+                        kernel_events=None) -> torch.Tensor:
+    """Nine quantities per window of packed keys[i] = src<<32 | dst (device int64/uint64).
+
+    kernel_events: optional (start, end) torch.cuda.Event pair (created with enable_timing=True),
+    recorded on the stream right around the main kernel (for measurement).
+    """
     _check(keys, "keys", _U64_TYPES)
-    return _launch(None, None, keys, keys.numel(), window, out, workspace, stream, flags, keys.device)
+    return _launch(None, None, keys, keys.numel(), window, out, workspace, stream, flags, keys.device,
+                   events=kernel_events)
 
 
 def window_stats_from_host(keys_host: torch.Tensor, window: int = DEFAULT_WINDOW, *, device=None,

@@ -137,7 +137,7 @@ static int sms_for_layout() {
 }
 
 static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u64 W, u64* out, void* ws,
-                      size_t ws_bytes, void* stream, u32 flags) {
+                      size_t ws_bytes, void* stream, u32 flags, void* ev_before = nullptr, void* ev_after = nullptr) {
   g_last_launches = 0;
   if (W == 0 || W > NSG_MAX_WINDOW) return NSG_ERR_INVALID_ARGUMENT;
   if (n == 0) return NSG_OK;
@@ -188,9 +188,11 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
     g.total_items = (L.nw + LAG_F) * g.ips;
     u64 grid = (u64)d.fast_blocks;
     if (grid > g.total_items) grid = g.total_items;
+    if (ev_before && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_before), s) != cudaSuccess) return NSG_ERR_CUDA;
     fast_kernel<<<(unsigned)grid, FT, FAST_SMEM, s>>>(g, src, dst, keys, out);
     g_last_launches++;
     if (cudaGetLastError() != cudaSuccess) return NSG_ERR_CUDA;
+    if (ev_after && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_after), s) != cudaSuccess) return NSG_ERR_CUDA;
     if (!(flags & NSG_FLAG_NO_FALLBACK_CHECK)) {
       gg.only_overflowed = 1;
       global_kernel<<<L.G, GT, 0, s>>>(gg, src, dst, keys, out);
@@ -199,9 +201,11 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
     }
   } else {
     gg.only_overflowed = 0;
+    if (ev_before && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_before), s) != cudaSuccess) return NSG_ERR_CUDA;
     global_kernel<<<L.G, GT, 0, s>>>(gg, src, dst, keys, out);
     g_last_launches++;
     if (cudaGetLastError() != cudaSuccess) return NSG_ERR_CUDA;
+    if (ev_after && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_after), s) != cudaSuccess) return NSG_ERR_CUDA;
   }
   return NSG_OK;
 }
@@ -242,6 +246,13 @@ nsg_status nsg_window_stats_ex(const uint32_t* src, const uint32_t* dst, const u
                                void* stream, uint32_t flags) {
   return nsg::run(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_packets, window,
                   reinterpret_cast<nsg::u64*>(out), workspace, workspace_bytes, stream, flags);
+}
+
+nsg_status nsg_window_stats_timed(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
+                                  uint64_t window, uint64_t* out, void* workspace, size_t workspace_bytes, void* stream,
+                                  uint32_t flags, void* ev_before, void* ev_after) {
+  return nsg::run(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_packets, window,
+                  reinterpret_cast<nsg::u64*>(out), workspace, workspace_bytes, stream, flags, ev_before, ev_after);
 }
 
 size_t nsg_diag_offset(void) { return nsg::DIAG_OFFSET; }
