@@ -82,8 +82,8 @@ enum {
   NSG_FLAG_NO_FALLBACK_CHECK = 1u << 2, /* internal/benchmark: skip the fallback launch; results of an
                                           overflowed window are then undefined (never use for results) */
   NSG_FLAG_PROFILE = 1u << 3           /* accumulate per-work-item-type SM cycles into the workspace:
-                                          u64[64] at nsg_diag_offset()+64: [0..12) per type (partition, link,
-                                          side) {items, cycles, wait cycles, 0}; [16+16*type+phase] cycles per phase */
+                                          u64[112] at nsg_diag_offset()+64: [0..12) per type (partition, link,
+                                          side) {items, cycles, wait cycles, max work}; [16+16*type+phase] cycles per phase, [64+...] max */
 };
 
 /* Number of windows: ceil(n_packets / window); 0 if n_packets == 0 or window == 0. */

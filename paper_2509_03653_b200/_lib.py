@@ -61,10 +61,11 @@ class NsgError(RuntimeError):
 
 
 def load() -> ctypes.CDLL:
-    if not os.path.exists(LIB_PATH):
+    path = os.environ.get("NSG_LIB_PATH_DEV", LIB_PATH)  # development override: a variant build of libnsg
+    if not os.path.exists(path):
         raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                           "(there is no CPU fallback)")
-    lib = ctypes.CDLL(LIB_PATH)
+    lib = ctypes.CDLL(path)
     u64, sz, vp, u32 = ctypes.c_uint64, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_uint32
     lib.nsg_num_windows.restype = u64
     lib.nsg_num_windows.argtypes = [u64, u64]

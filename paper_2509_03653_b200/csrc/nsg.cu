@@ -41,7 +41,7 @@ struct Layout {
   u64 nw;
   // fast
   u32 logB, B, cp, cp_last, R;
-  size_t o_pw, o_kscr, o_koff, o_rscr, o_roff, o_lres, o_sres;
+  size_t o_pw, o_kscr, o_koff, o_rscr, o_roff, o_rend, o_lres, o_sres;
   size_t memset_bytes;
   // global
   u64 LC;
@@ -71,6 +71,7 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     L.o_koff = o; o = align256(o + (size_t)L.R * L.cp * (L.B + 1) * sizeof(u32));
     L.o_rscr = o; o = align256(o + (size_t)L.R * L.B * RCAP * sizeof(u64));
     L.o_roff = o; o = align256(o + (size_t)L.R * L.B * (2 * L.B + 1) * sizeof(u32));
+    L.o_rend = o; o = align256(o + (size_t)L.R * L.B * (2 * L.B) * sizeof(u32));
     L.o_lres = o; o = align256(o + (size_t)L.R * L.B * 4 * sizeof(u32));
     L.o_sres = o; o = align256(o + (size_t)L.R * 2 * L.B * 4 * sizeof(u32));
   }
@@ -182,6 +183,7 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
     g.koff = reinterpret_cast<u32*>(base + L.o_koff);
     g.rscr = reinterpret_cast<u64*>(base + L.o_rscr);
     g.roff = reinterpret_cast<u32*>(base + L.o_roff);
+    g.rend = reinterpret_cast<u32*>(base + L.o_rend);
     g.lres = reinterpret_cast<u32*>(base + L.o_lres);
     g.sres = reinterpret_cast<u32*>(base + L.o_sres);
     g.ips = 1ull + 3ull * g.B + g.cp;

@@ -27,17 +27,36 @@
 
 namespace nsg {
 
-constexpr int FT = 512;                      // threads per CTA; 2 CTAs per SM
+#ifndef NSG_FT
+#define NSG_FT 512
+#endif
+#ifndef NSG_TCAP
+#define NSG_TCAP 6144
+#endif
+#ifndef NSG_BUCKET_KEYS
+#define NSG_BUCKET_KEYS 2048
+#endif
+#ifndef NSG_PCAP
+#define NSG_PCAP 512
+#endif
+constexpr int FT = NSG_FT;                   // threads per CTA (default 512: 2 CTAs per SM)
 constexpr int NWARP = FT / 32;
 constexpr int KPT = 8;                       // elements per thread per round
 constexpr int CH = FT * KPT;                 // 4096 keys per chunk / per gather round
-constexpr int TCAP = 6144;                   // SMEM hash-table slots (slot = (h * TCAP) >> 32)
-constexpr int BUCKET_KEYS = 2048;            // target keys per link bucket (load factor ~1/3)
-constexpr int PCAP = 512;                    // pending-list capacity (entries) per insertion wave
-constexpr int MAX_LOGB = 9;
+constexpr int TCAP = NSG_TCAP;               // SMEM hash-table slots (slot = (h * TCAP) >> 32)
+constexpr int BUCKET_KEYS = NSG_BUCKET_KEYS; // target keys per link bucket (load factor ~1/3)
+constexpr int PCAP = NSG_PCAP;               // pending-list capacity (entries) per insertion wave
+constexpr int MAX_LOGB = 20 - (BUCKET_KEYS == 1024 ? 10 : BUCKET_KEYS == 2048 ? 11 : 12);  // B * BUCKET_KEYS <= 2^20
 constexpr int MAXB = 1 << MAX_LOGB;
-constexpr u64 FAST_MAX_WINDOW = (u64)BUCKET_KEYS << MAX_LOGB;  // 2^20
-constexpr int MAXCP = (int)(FAST_MAX_WINDOW / CH);
+constexpr u64 FAST_MAX_WINDOW = ((u64)BUCKET_KEYS << MAX_LOGB) - 1;  // 2^20 - 1: P fits a record's 20 bits
+constexpr int MAXCP = (int)((FAST_MAX_WINDOW + CH) / CH);
+// A link record: node << 32 | F << 20 | P (F = links merged into it, P = their packets; a window on
+// the fast path has < 2^20 packets so P always fits, and F is split over several records if > 4095).
+constexpr u32 REC_PBITS = 20, REC_FMAX = 4095;
+__host__ __device__ __forceinline__ u64 make_rec(u32 node, u32 f, u32 p) {
+  return ((u64)node << 32) | ((u64)f << REC_PBITS) | p;
+}
+static_assert(TCAP % FT == 0, "emission loop is warp-uniform");
 constexpr int LAG_L = 4, LAG_S = 8, LAG_F = 11;  // pipeline lags (steps) of L, S, F items behind P
 constexpr int LOG_RSLOTS = 4;
 constexpr int RSLOTS = 1 << LOG_RSLOTS;      // scratch slots (windows in flight), > LAG_S
@@ -62,16 +81,24 @@ struct Geo {
   u64* kscr;  // [R][cp*CH]      keys, chunk-major, each chunk sorted by link bucket
   u32* koff;  // [R][cp][B+1]    bucket offsets inside each chunk
   u64* rscr;  // [R][B][RCAP]    link records of each link bucket, sorted by (side, side bucket)
-  u32* roff;  // [R][B][2B+1]    offsets of (side, side bucket) inside each link bucket's records
+  u32* roff;  // [R][B][2B+1]    start offsets of (side, side bucket) inside each link bucket's records
+  u32* rend;  // [R][B][2B]      end offsets (records are aggregated per node, so segments may be short)
   u32* lres;  // [R][B][4]       per link bucket: unique links, max count, sum of counts
   u32* sres;  // [R][2][B][4]    per side bucket: unique nodes, max packets, max fan
 };
 
 struct SmemP { u64 stage[CH]; u32 hist[MAXB + 1]; };
+// Per-warp gather tables: warp w gathers segments w, w + NWARP, ... (chunks for L, link buckets for S).
+constexpr int WSEG_L = (MAXCP + NWARP - 1) / NWARP;
+constexpr int WSEG_S = (MAXB + NWARP - 1) / NWARP;
+static_assert(WSEG_L <= 32 && WSEG_S <= 32, "one segment per lane");
 struct SmemL {
-  u64 lkey[TCAP]; u32 lcnt[TCAP]; Pend pend[2][PCAP]; u32 seg[MAXCP + 1]; u32 seglo[MAXCP]; u32 hist[2 * MAXB + 1];
+  u64 lkey[TCAP]; u32 lcnt[TCAP]; Pend pend[2][PCAP]; u32 wlo[NWARP][WSEG_L]; u32 wpre[NWARP][WSEG_L + 1];
+  u32 hist[2 * MAXB + 1];
 };
-struct SmemS { u32 key[TCAP]; u32 P[TCAP]; u32 F[TCAP]; Pend pend[2][PCAP]; u32 seg[MAXB + 1]; u32 seglo[MAXB]; };
+struct SmemS {
+  u32 key[TCAP]; u32 P[TCAP]; u32 F[TCAP]; Pend pend[2][PCAP]; u32 wlo[NWARP][WSEG_S]; u32 wpre[NWARP][WSEG_S + 1];
+};
 struct SmemMisc {
   u32 wtmp[10 * NWARP];
   u32 esc[4];  // [0] link-table escape count (key ~0); [1],[2] node-table escape P, F (node ~0)
@@ -201,6 +228,13 @@ __device__ __noinline__ bool node_finish(u32* key, u32* P, u32* F, u32 node, u32
   return false;
 }
 
+// merge a cached (node, P, F) aggregate into the node table (one lane); nothing if it saw no record
+__device__ __noinline__ bool node_flush(u32* key, u32* P, u32* F, u32* esc, u32 node, u32 p, u32 f) {
+  if (f == 0) return true;
+  if (node == EMPTY32) { atomicAdd(&esc[1], p); atomicAdd(&esc[2], f); return true; }
+  return node_finish(key, P, F, node, p, f, 0u);
+}
+
 // Warp-aggregated append of the lanes with `want` to pending list `list`; must be called by all
 // lanes of the warp.  Returns false for a lane whose entry did not fit (the caller finishes it).
 __device__ __forceinline__ bool pend_push(Pend* list, u32* cnt, bool want, const Pend& e) {
@@ -246,6 +280,7 @@ struct PhaseTimer {
     if ((g.flags & NSG_FLAG_PROFILE) && threadIdx.x == 0) {
       const long long now = clock64();
       atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[16 + type * 16 + phase]), (unsigned long long)(now - last));
+      atomicMax(reinterpret_cast<unsigned long long*>(&g.prof[64 + type * 16 + phase]), (unsigned long long)(now - last));
       last = now;
     }
   }
@@ -324,9 +359,12 @@ __device__ void item_partition(const Geo& g, const u32* __restrict__ src, const 
     if (full || t + j * FT < (int)len) atomicAdd(&s.hist[link_bucket(k[j], g.logB)], 1u);
   __syncthreads();
   pt.mark(g, 0, 1);
-  block_exclusive_scan(s.hist, (int)g.B, m.wtmp);
-  u32* off = g.koff + ((u64)slot * g.cp + c) * (g.B + 1);
-  for (int i = t; i <= (int)g.B; i += FT) off[i] = s.hist[i];
+  warp0_exclusive_scan(s.hist, (int)g.B);  // warp 0 scans and publishes the chunk's bucket offsets
+  if (t < 32) {
+    __syncwarp();
+    u32* off = g.koff + ((u64)slot * g.cp + c) * (g.B + 1);
+    for (int i = t; i <= (int)g.B; i += 32) off[i] = s.hist[i];
+  }
   __syncthreads();
   pt.mark(g, 0, 2);
 #pragma unroll
@@ -377,6 +415,25 @@ __device__ __noinline__ bool link_finish_h(u64* lkey, u32* lcnt, u32* hist, u32 
 
 constexpr u32 WAVE_TAIL = 64;  // pending entries below this finish per lane (no more CTA waves)
 
+// Warp-level gather setup: lane q < nseg describes segment q of this warp (global element offset `lo`,
+// length `len`); the warp publishes segment starts and exclusive prefixes into its SMEM rows and
+// returns the warp's element total.  No CTA barrier is involved.
+__device__ __forceinline__ u32 warp_segments(u32* wlo, u32* wpre, u32 nseg, u32 lo, u32 len) {
+  const int lane = threadIdx.x & 31;
+  if ((u32)lane >= nseg) len = 0;
+  u32 x = len;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  const u32 total = __shfl_sync(0xffffffffu, x, 31);
+  if ((u32)lane < nseg) { wlo[lane] = lo; wpre[lane] = x - len; }
+  if (lane == 0) wpre[nseg] = total;
+  __syncwarp();
+  return total;
+}
+
 __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   PhaseTimer pt;
@@ -394,55 +451,56 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
   }
   for (int i = t; i <= (int)(2 * B); i += FT) s.hist[i] = 0;
   if (t < 4) m.esc[t] = 0;
-  if (t == 0) { m.flag = 0; waited = wait_geq(&g.pdone[w], g.cp, dep); }
+  if (t == 0) { m.flag = 0; m.pcnt[0] = 0; waited = wait_geq(&g.pdone[w], g.cp, dep); }
   __syncthreads();  // also publishes thread 0's acquire to the CTA
   pt.mark(g, 1, 0);
   const u32 slot = slot_of(g, w);
   const u32* koff = g.koff + (u64)slot * g.cp * (B + 1);
-  for (u32 c = t; c < ncp; c += FT) {
-    const u32 lo = ldcg32(koff + (u64)c * (B + 1) + b), hi = ldcg32(koff + (u64)c * (B + 1) + b + 1);
-    s.seg[c] = hi - lo;
-    s.seglo[c] = c * CH + lo;
-  }
-  __syncthreads();
-  warp0_exclusive_scan(s.seg, (int)ncp);
-  __syncthreads();
-  pt.mark(g, 1, 1);
-  const u32 nb = s.seg[ncp];
   const u64* ks = g.kscr + (u64)slot * g.cp * CH;
   bool ok = true;
-  for (u32 base = 0; base < nb; base += CH) {  // CTA-uniform rounds of CH keys
-    u64 k[KPT];
+  {
+    // warp wid gathers bucket b's segment of chunks wid, wid + NWARP, ...; wave 0 runs per warp
+    const u32 nseg = (u32)wid < ncp ? (ncp - 1 - wid) / NWARP + 1 : 0;
+    u32 lo = 0, len = 0;
+    if ((u32)lane < nseg) {
+      const u32 c = wid + lane * NWARP;
+      const u32* o = koff + (u64)c * (B + 1) + b;
+      lo = ldcg32(o);
+      len = ldcg32(o + 1) - lo;
+      lo += c * CH;
+    }
+    u32* wlo = s.wlo[wid];
+    u32* wpre = s.wpre[wid];
+    const u32 total = warp_segments(wlo, wpre, nseg, lo, len);
+    for (u32 base = 0; base < total; base += 32 * KPT) {  // warp-uniform rounds
+      u64 k[KPT];
 #pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      const u32 i = base + t + j * FT;
-      if (i < nb) {
-        const u32 c = find_seg(s.seg, ncp, i);
-        k[j] = ldcg64(ks + s.seglo[c] + (i - s.seg[c]));
+      for (int j = 0; j < KPT; ++j) {
+        const u32 e = base + lane + 32 * j;
+        if (e < total) {
+          const u32 q = find_seg(wpre, nseg, e);
+          k[j] = ldcg64(ks + wlo[q] + (e - wpre[q]));
+        }
+      }
+      // wave 0: one full-warp CAS per key at its home slot, then one at the next slot for the losers
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        if (base + 32 * j >= total) break;  // warp-uniform
+        bool entry = base + lane + 32 * j < total;
+        if (entry && k[j] == EMPTY64) { atomicAdd(&m.esc[0], 1u); entry = false; }
+        bool placed = true;
+        u32 home = 0;
+        if (entry) { home = link_home(k[j]); placed = link_try_h(s.lkey, s.lcnt, s.hist, B, logB, k[j], 1u, home); }
+        if (!placed) placed = link_try_h(s.lkey, s.lcnt, s.hist, B, logB, k[j], 1u, probe_slot(home, 1u));
+        const Pend e{k[j], 1u, 2u};
+        if (!pend_push(s.pend[0], &m.pcnt[0], !placed, e))
+          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B, logB, k[j], 1u, 2u) && ok;
       }
     }
-    if (t == 0) m.pcnt[0] = 0;
-    __syncthreads();
-    // wave 0: warp-leader aggregation (the lanes holding the first valid lane's key add once), then
-    // one full-warp CAS per entry at its home slot
-#pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      if (base + j * FT >= nb) break;  // CTA-uniform
-      const bool valid = base + t + j * FT < nb;
-      const u32 vmask = __ballot_sync(0xffffffffu, valid);
-      const u64 lead = __shfl_sync(0xffffffffu, k[j], __ffs(vmask | 1u) - 1);
-      const u32 same = __ballot_sync(0xffffffffu, valid && k[j] == lead);
-      bool entry = valid;
-      u32 add = 1;
-      if (valid && k[j] == lead) { entry = lane == __ffs(same) - 1; add = (u32)__popc(same); }
-      if (entry && k[j] == EMPTY64) { atomicAdd(&m.esc[0], add); entry = false; }
-      bool placed = true;
-      if (entry) placed = link_try_h(s.lkey, s.lcnt, s.hist, B, logB, k[j], add, link_home(k[j]));
-      const Pend e{k[j], add, 1u};
-      if (!pend_push(s.pend[0], &m.pcnt[0], !placed, e))
-        ok = link_finish_h(s.lkey, s.lcnt, s.hist, B, logB, k[j], add, 1u) && ok;
-    }
-    __syncthreads();
+  }
+  __syncthreads();
+  pt.mark(g, 1, 1);
+  {
     // waves 1..: the pending list, densely, one probe further each wave; a short tail finishes per lane
     int cur = 0;
     u32 n = min(m.pcnt[0], (u32)PCAP);
@@ -458,10 +516,9 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
       __syncthreads();
       for (u32 i0 = 0; i0 < n; i0 += FT) {
         const u32 i = i0 + t;
-        const bool valid = i < n;
         Pend e{0, 0, 0};
         bool placed = true;
-        if (valid) {
+        if (i < n) {
           e = s.pend[cur][i];
           if (e.probe >= (u32)TCAP) ok = false;
           else placed = link_try_h(s.lkey, s.lcnt, s.hist, B, logB, e.a, e.b, probe_slot(link_home(e.a), e.probe));
@@ -482,16 +539,17 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
   }
   __syncthreads();
   pt.mark(g, 1, 2);
-  // record region layout: offsets of every (side, side bucket)
+  // record region layout: offsets of every (side, side bucket), scanned and published by warp 0
   warp0_exclusive_scan(s.hist, (int)(2 * B));
+  if (t < 32) {
+    __syncwarp();
+    u32* off = g.roff + ((u64)slot * B + b) * (2 * B + 1);
+    for (int i = t; i <= (int)(2 * B); i += 32) off[i] = s.hist[i];
+  }
   __syncthreads();
-  u32* off = g.roff + ((u64)slot * B + b) * (2 * B + 1);
-  for (int i = t; i <= (int)(2 * B); i += FT) off[i] = s.hist[i];
   pt.mark(g, 1, 3);
   // One pass over the bucket's part of A_t: unique links (:181), max link packets (:183), sum of counts
-  // (:180); and one record per link and side, node<<32 | count.  (The barrier orders the offset copy
-  // above before the cursors move.)
-  __syncthreads();
+  // (:180); and one record per link and side, node<<32 | 1<<20 | count.
   u64* rec = g.rscr + ((u64)slot * B + b) * RCAP;
   u32 nl = 0, mx = 0, sm = 0;
   for (int i = t; i < TCAP; i += FT) {
@@ -500,14 +558,14 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
       const u32 c = s.lcnt[i];
       nl += 1; mx = max(mx, c); sm += c;
       const u32 sn = (u32)(key >> 32), dn = (u32)key;
-      rec[atomicAdd(&s.hist[side_bucket(sn, logB)], 1u)] = ((u64)sn << 32) | c;
-      rec[atomicAdd(&s.hist[B + side_bucket(dn, logB)], 1u)] = ((u64)dn << 32) | c;
+      rec[atomicAdd(&s.hist[side_bucket(sn, logB)], 1u)] = make_rec(sn, 1u, c);
+      rec[atomicAdd(&s.hist[B + side_bucket(dn, logB)], 1u)] = make_rec(dn, 1u, c);
     }
   }
   if (t == 0 && m.esc[0]) {
     const u32 c = m.esc[0];
     nl += 1; mx = max(mx, c); sm += c;
-    const u64 r = ((u64)EMPTY32 << 32) | c;
+    const u64 r = make_rec(EMPTY32, 1u, c);
     rec[atomicAdd(&s.hist[side_bucket(EMPTY32, logB)], 1u)] = r;
     rec[atomicAdd(&s.hist[B + side_bucket(EMPTY32, logB)], 1u)] = r;
   }
@@ -515,14 +573,22 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
   if (lane == 0) { m.wtmp[4 * NWARP + wid] = nl; m.wtmp[5 * NWARP + wid] = mx; m.wtmp[6 * NWARP + wid] = sm; }
   __syncthreads();
   pt.mark(g, 1, 4);
-  if (t == 0) {
-    u32 a = 0, bm = 0, cs = 0;
-    for (int i = 0; i < NWARP; ++i) { a += m.wtmp[4 * NWARP + i]; bm = max(bm, m.wtmp[5 * NWARP + i]); cs += m.wtmp[6 * NWARP + i]; }
-    u32* r = g.lres + ((u64)slot * B + b) * 4;
-    r[0] = a; r[1] = bm; r[2] = cs;
-    if (m.flag) mark_overflow(g, w);
-    red_release_add32(&g.ldone[w], 1u);  // thread 0's own lres writes precede it in program order
-    prof_add(g, 1, clock64() - tstart, waited);
+  if (wid == 0) {
+    u32 a = lane < NWARP ? m.wtmp[4 * NWARP + lane] : 0u;
+    u32 bm = lane < NWARP ? m.wtmp[5 * NWARP + lane] : 0u;
+    u32 cs = lane < NWARP ? m.wtmp[6 * NWARP + lane] : 0u;
+    a = warp_sum(a); bm = warp_max(bm); cs = warp_sum(cs);
+    u32* rend = g.rend + ((u64)slot * B + b) * (2 * B);
+    for (int i = lane; i < (int)(2 * B); i += 32) rend[i] = s.hist[i];  // cursors = segment ends
+    __syncwarp();
+    if (lane == 0) {
+      u32* r = g.lres + ((u64)slot * B + b) * 4;
+      r[0] = a; r[1] = bm; r[2] = cs;
+      if (m.flag) mark_overflow(g, w);
+      __threadfence_block();
+      red_release_add32(&g.ldone[w], 1u);  // after the CTA barrier; warp 0's writes precede it
+      prof_add(g, 1, clock64() - tstart, waited);
+    }
   }
 }
 
@@ -599,58 +665,76 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
     }
   }
   if (t < 4) m.esc[t] = 0;
-  if (t == 0) { m.flag = 0; waited = wait_geq(&g.ldone[w], B, dep); }
+  if (t == 0) { m.flag = 0; m.pcnt[0] = 0; waited = wait_geq(&g.ldone[w], B, dep); }
   __syncthreads();
   pt.mark(g, 2, 0);
   const u32 slot = slot_of(g, w);
-  for (u32 b = t; b < B; b += FT) {
-    const u32* off = g.roff + ((u64)slot * B + b) * (2 * B + 1) + side * B;
-    const u32 lo = ldcg32(off + sb), hi = ldcg32(off + sb + 1);
-    s.seg[b] = hi - lo;
-    s.seglo[b] = b * RCAP + lo;
-  }
-  __syncthreads();
-  warp0_exclusive_scan(s.seg, (int)B);
-  __syncthreads();
-  pt.mark(g, 2, 1);
-  const u32 nr = s.seg[B];
   const u64* rs = g.rscr + (u64)slot * B * RCAP;
   bool ok = true;
-  for (u32 base = 0; base < nr; base += CH) {
-    u64 r[KPT];
+  {
+    // warp wid gathers side bucket sb's records from link buckets wid, wid + NWARP, ...
+    const u32 nseg = (u32)wid < B ? (B - 1 - wid) / NWARP + 1 : 0;
+    u32 lo = 0, len = 0;
+    if ((u32)lane < nseg) {
+      const u32 lb = wid + lane * NWARP;
+      lo = ldcg32(g.roff + ((u64)slot * B + lb) * (2 * B + 1) + side * B + sb);
+      len = ldcg32(g.rend + ((u64)slot * B + lb) * (2 * B) + side * B + sb) - lo;
+      lo += lb * RCAP;
+    }
+    u32* wlo = s.wlo[wid];
+    u32* wpre = s.wpre[wid];
+    const u32 total = warp_segments(wlo, wpre, nseg, lo, len);
+    // Warp-uniform register cache of one hot node (e.g. the heavy source): records of the cached node
+    // are summed in registers across rounds and merged into the table once, when the entry is evicted.
+    // An entry is replaced only after a round in which it had fewer than 8 hits.
+    bool c_has = false;
+    u32 c_node = 0, c_p = 0, c_f = 0, c_hits = 0;
+    for (u32 base = 0; base < total; base += 32 * KPT) {  // warp-uniform rounds
+      u64 r[KPT];
 #pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      const u32 i = base + t + j * FT;
-      if (i < nr) {
-        const u32 bb = find_seg(s.seg, B, i);
-        r[j] = ldcg64(rs + s.seglo[bb] + (i - s.seg[bb]));
+      for (int j = 0; j < KPT; ++j) {
+        const u32 e = base + lane + 32 * j;
+        if (e < total) {
+          const u32 q = find_seg(wpre, nseg, e);
+          r[j] = ldcg64(rs + wlo[q] + (e - wpre[q]));
+        }
+      }
+      if (!c_has || c_hits < 8) {  // (re)seed the cache with the first record of the round
+        const u32 cand = __shfl_sync(0xffffffffu, (u32)(r[0] >> 32), 0);
+        if (c_has && cand != c_node && lane == 0)  // evict: merge the old entry into the table
+          ok = node_flush(s.key, s.P, s.F, m.esc, c_node, c_p, c_f) && ok;
+        if (!c_has || cand != c_node) { c_node = cand; c_p = 0; c_f = 0; c_has = true; }
+      }
+      c_hits = 0;
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        if (base + 32 * j >= total) break;  // warp-uniform
+        const bool valid = base + lane + 32 * j < total;
+        const u32 node = (u32)(r[j] >> 32);
+        const u32 p = (u32)r[j] & ((1u << REC_PBITS) - 1u);
+        const u32 f = (u32)(r[j] >> REC_PBITS) & REC_FMAX;
+        const bool hit = valid && node == c_node;
+        const u32 hm = __ballot_sync(0xffffffffu, hit);
+        if (hm) {
+          c_p += __reduce_add_sync(0xffffffffu, hit ? p : 0u);
+          c_f += __reduce_add_sync(0xffffffffu, hit ? f : 0u);
+          c_hits += (u32)__popc(hm);
+        }
+        bool entry = valid && !hit;
+        if (entry && node == EMPTY32) { atomicAdd(&m.esc[1], p); atomicAdd(&m.esc[2], f); entry = false; }
+        bool placed = true;
+        u32 home = 0;
+        if (entry) { home = node_home(node); placed = node_try(s.key, s.P, s.F, node, p, f, home); }
+        if (!placed) placed = node_try(s.key, s.P, s.F, node, p, f, probe_slot(home, 1u));
+        const Pend e{(u64)node | ((u64)f << 32), p, 2u};
+        if (!pend_push(s.pend[0], &m.pcnt[0], !placed, e)) ok = node_finish(s.key, s.P, s.F, node, p, f, 2u) && ok;
       }
     }
-    if (t == 0) m.pcnt[0] = 0;
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      if (base + j * FT >= nr) break;  // CTA-uniform
-      const bool valid = base + t + j * FT < nr;
-      const u32 vmask = __ballot_sync(0xffffffffu, valid);
-      const u32 node = (u32)(r[j] >> 32);
-      u32 p = (u32)r[j], f = 1;
-      // warp-leader aggregation: a hot node (e.g. the heavy source) is merged once per warp
-      const u32 lead = __shfl_sync(0xffffffffu, node, __ffs(vmask | 1u) - 1);
-      const u32 same = __ballot_sync(0xffffffffu, valid && node == lead);
-      bool entry = valid;
-      if (valid && node == lead) {
-        const u32 sum = __reduce_add_sync(same, p);
-        entry = lane == __ffs(same) - 1;
-        p = sum; f = (u32)__popc(same);
-      }
-      if (entry && node == EMPTY32) { atomicAdd(&m.esc[1], p); atomicAdd(&m.esc[2], f); entry = false; }
-      bool placed = true;
-      if (entry) placed = node_try(s.key, s.P, s.F, node, p, f, node_home(node));
-      const Pend e{(u64)node | ((u64)f << 32), p, 1u};
-      if (!pend_push(s.pend[0], &m.pcnt[0], !placed, e)) ok = node_finish(s.key, s.P, s.F, node, p, f, 1u) && ok;
-    }
-    __syncthreads();
+    if (c_has && lane == 0) ok = node_flush(s.key, s.P, s.F, m.esc, c_node, c_p, c_f) && ok;  // flush the cache
+  }
+  __syncthreads();
+  pt.mark(g, 2, 1);
+  {
     int cur = 0;
     u32 n = min(m.pcnt[0], (u32)PCAP);
     while (n) {
@@ -665,10 +749,9 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
       __syncthreads();
       for (u32 i0 = 0; i0 < n; i0 += FT) {
         const u32 i = i0 + t;
-        const bool valid = i < n;
         Pend e{0, 0, 0};
         bool placed = true;
-        if (valid) {
+        if (i < n) {
           e = s.pend[cur][i];
           if (e.probe >= (u32)TCAP) ok = false;
           else placed = node_try(s.key, s.P, s.F, (u32)e.a, e.b, (u32)(e.a >> 32), probe_slot(node_home((u32)e.a), e.probe));
@@ -695,54 +778,77 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
   if (lane == 0) { m.wtmp[4 * NWARP + wid] = d; m.wtmp[5 * NWARP + wid] = mp; m.wtmp[6 * NWARP + wid] = mf; }
   __syncthreads();
   pt.mark(g, 2, 3);
-  if (t == 0) {
-    u32 a = 0, bp = 0, cf = 0;
-    for (int i = 0; i < NWARP; ++i) { a += m.wtmp[4 * NWARP + i]; bp = max(bp, m.wtmp[5 * NWARP + i]); cf = max(cf, m.wtmp[6 * NWARP + i]); }
-    u32* res = g.sres + (((u64)slot * 2 + side) * B + sb) * 4;
-    res[0] = a; res[1] = bp; res[2] = cf;
-    if (m.flag) mark_overflow(g, w);
-    red_release_add32(&g.sdone[w], 1u);  // thread 0 wrote res itself: program order + release
-    prof_add(g, 2, clock64() - tstart, waited);
+  if (wid == 0) {
+    u32 a = lane < NWARP ? m.wtmp[4 * NWARP + lane] : 0u;
+    u32 bp = lane < NWARP ? m.wtmp[5 * NWARP + lane] : 0u;
+    u32 cf = lane < NWARP ? m.wtmp[6 * NWARP + lane] : 0u;
+    a = warp_sum(a); bp = warp_max(bp); cf = warp_max(cf);
+    if (lane == 0) {
+      u32* res = g.sres + (((u64)slot * 2 + side) * B + sb) * 4;
+      res[0] = a; res[1] = bp; res[2] = cf;
+      if (m.flag) mark_overflow(g, w);
+      red_release_add32(&g.sdone[w], 1u);  // thread 0 wrote res itself: program order + release
+      prof_add(g, 2, clock64() - tstart, waited);
+    }
   }
 }
+
 // ------------------------------------------------------------------------------------------
 // Ticket decoding: step k = tk / ips holds F(k-LAG_F), S(k-LAG_S) [2B], L(k-LAG_L) [B], P(k) [cp].
 // ------------------------------------------------------------------------------------------
 enum : u32 { ITEM_P = 0, ITEM_L = 1, ITEM_S0 = 2, ITEM_S1 = 3, ITEM_F = 4, ITEM_NOP = 5, ITEM_DONE = 6 };
 
-__device__ __forceinline__ void decode_ticket(const Geo& g, u64 tk, SmemMisc& m) {
-  if (tk >= g.total_items) { m.type = ITEM_DONE; return; }
-  const u64 k = tk / g.ips;
-  u64 idx = tk - k * g.ips;
+struct Item { u32 type, idx; u64 w; };
+
+__device__ __forceinline__ Item decode_ticket(const Geo& g, u64 tk) {
+  Item it{ITEM_DONE, 0, 0};
+  if (tk >= g.total_items) return it;
+  u64 k, idx;
+  if (g.total_items <= 0xFFFFFFFFull) {  // 32-bit division when it fits (the usual case)
+    const u32 k32 = (u32)tk / (u32)g.ips;
+    k = k32;
+    idx = (u32)tk - k32 * (u32)g.ips;
+  } else {
+    k = tk / g.ips;
+    idx = tk - k * g.ips;
+  }
   u64 w;
   u32 type;
   if (idx == 0) { type = ITEM_F; w = k - LAG_F; }
   else if ((idx -= 1) < 2ull * g.B) { type = idx < g.B ? ITEM_S0 : ITEM_S1; idx &= g.B - 1; w = k - LAG_S; }
   else if ((idx -= 2ull * g.B) < g.B) { type = ITEM_L; w = k - LAG_L; }
   else { idx -= g.B; type = ITEM_P; w = k; }
-  // windows before the first step of a class (w wrapped below 0) or past the end are no-ops, except
-  // that P items beyond the last window's chunks still signal so L items can wait for a full count
+  // windows before the first step of a class (w wrapped below 0) or past the end are no-ops
   if (w >= g.nw) type = ITEM_NOP;
-  m.type = type; m.w = w; m.idx = (u32)idx;
+  it.type = type; it.w = w; it.idx = (u32)idx;
+  return it;
 }
 
-__global__ void __launch_bounds__(FT, 2)
+__global__ void __launch_bounds__(FT, 1024 / FT)
 fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, const u64* __restrict__ keys,
             u64* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmemMisc& m = *reinterpret_cast<SmemMisc*>(smem_raw);
   unsigned char* u = smem_raw + MISC_BYTES;
-  u64 next = 0;  // thread 0: the next ticket, fetched one item ahead so its latency is hidden
-  if (threadIdx.x == 0) next = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
+  // Thread 0 keeps the ticket pipeline: the item after the current one is fetched (atomicAdd) one
+  // item ahead and decoded at the start of the current item, so the boundary barrier only publishes
+  // an already-decoded descriptor.
+  u64 tk_next = 0;
+  Item nxt{ITEM_DONE, 0, 0};
+  if (threadIdx.x == 0) {
+    const Item first = decode_ticket(g, atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull));
+    m.type = first.type; m.idx = first.idx; m.w = first.w;
+    if (first.type != ITEM_DONE) tk_next = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
+  }
   for (;;) {
-    if (threadIdx.x == 0) {
-      decode_ticket(g, next, m);
-      if (m.type != ITEM_DONE) next = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
-    }
     __syncthreads();
     const u32 type = m.type, idx = m.idx;
     const u64 w = m.w;
     if (type == ITEM_DONE) break;
+    if (threadIdx.x == 0) {
+      nxt = decode_ticket(g, tk_next);
+      if (nxt.type != ITEM_DONE) tk_next = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
+    }
     // every item function passes a __syncthreads() before thread 0 can overwrite m.type/m.w/m.idx
     if (type == ITEM_P) {
       if (idx < chunks_of(g, w)) {
@@ -760,6 +866,8 @@ fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, con
     } else {
       __syncthreads();  // no-op ticket
     }
+    // every item function passed a __syncthreads() after all threads read m.type/m.w/m.idx
+    if (threadIdx.x == 0) { m.type = nxt.type; m.idx = nxt.idx; m.w = nxt.w; }
   }
 }
 

@@ -50,7 +50,7 @@ t = timed(0)
 print(f"{cfg.name}: {t*1e3:.1f} us  {cfg.n_packets / t / 1e6:.1f} Gpkt/s")
 tp = timed(FLAG_PROFILE, reps=1)
 off = ws.offset + 128
-prof = ws.buffer[off:off + 512].view(torch.int64).cpu().numpy()
+prof = ws.buffer[off:off + 896].view(torch.int64).cpu().numpy()
 clk = 1.9e9
 print(f"profiled run: {tp*1e3:.1f} us")
 for i, name in enumerate(["partition", "link", "side"]):
@@ -60,4 +60,6 @@ for i, name in enumerate(["partition", "link", "side"]):
               f" total {cyc / clk * 1e3:8.2f} CTA-ms")
         ph = prof[16 + 16 * i:16 + 16 * i + 8]
         print("     phases (avg cyc/item):", " ".join(f"{x / n:8.0f}" for x in ph if x))
+        pm = prof[64 + 16 * i:64 + 16 * i + 8]
+        print("     phases (max cyc/item):", " ".join(f"{x:8d}" for x in pm if x))
 print("diag", ws.diag())
