@@ -57,8 +57,8 @@ __host__ __device__ __forceinline__ u64 make_rec(u32 node, u32 f, u32 p) {
   return ((u64)node << 32) | ((u64)f << REC_PBITS) | p;
 }
 static_assert(TCAP % FT == 0, "emission loop is warp-uniform");
-constexpr int LAG_L = 4, LAG_S = 8, LAG_F = 11;  // pipeline lags (steps) of L, S, F items behind P
-constexpr int LOG_RSLOTS = 4;
+constexpr int LAG_L = 8, LAG_S = 20, LAG_F = 26;  // pipeline lags (steps) of L, S, F items behind P (measured plateau)
+constexpr int LOG_RSLOTS = 5;
 constexpr int RSLOTS = 1 << LOG_RSLOTS;      // scratch slots (windows in flight), > LAG_S
 constexpr u32 RCAP = 2 * (TCAP + 1) + 6;     // records per link bucket (both sides), 8-aligned
 

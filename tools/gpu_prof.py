@@ -14,6 +14,8 @@ from gen.configs import CONFIGS
 FLAG_PROFILE = 8
 from gen.configs import Config
 EXTRA = {"U2": Config("U2", 1 << 23, gen.Dist("uniform"), 2), "Z08": Config("Z08", 1 << 23, gen.Dist("zipf", 0.8, 1 << 20), 2),
+         "C2x4": Config("C2x4", 1 << 25, gen.Dist("zipf", 1.1, 1 << 20), 2), "C2x16": Config("C2x16", 1 << 27, gen.Dist("zipf", 1.1, 1 << 20), 2),
+         "C2h": Config("C2h", 1 << 22, gen.Dist("zipf", 1.1, 1 << 20), 2),
          "Z13": Config("Z13", 1 << 23, gen.Dist("zipf", 1.3, 1 << 20), 2)}
 name = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("-") else "C2"
 cfg = CONFIGS.get(name) or EXTRA[name]
