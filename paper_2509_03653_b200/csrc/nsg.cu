@@ -40,7 +40,7 @@ struct Layout {
   bool fast;
   u64 nw;
   // fast
-  u32 logB, B, cp, cp_last, R;
+  u32 logB, B, logB2, B2, cp, cp_last, R;
   size_t o_pw, o_kscr, o_koff, o_rscr, o_roff, o_rend, o_lres, o_sres;
   size_t memset_bytes;
   // global
@@ -63,6 +63,8 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     const u64 want = (W + BUCKET_KEYS - 1) / BUCKET_KEYS;
     L.B = (u32)next_pow2(want < 1 ? 1 : want);
     L.logB = ilog2(L.B);
+    L.B2 = L.B > 1 ? L.B / 2 : 1;
+    L.logB2 = ilog2(L.B2);
     L.cp = (u32)((W + CH - 1) / CH);
     const u64 last = n - (L.nw - 1) * W;
     L.cp_last = (u32)((last + CH - 1) / CH);
@@ -70,10 +72,10 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     L.o_kscr = o; o = align256(o + (size_t)L.R * L.cp * CH * sizeof(u64));
     L.o_koff = o; o = align256(o + (size_t)L.R * L.cp * (L.B + 1) * sizeof(u32));
     L.o_rscr = o; o = align256(o + (size_t)L.R * L.B * RCAP * sizeof(u64));
-    L.o_roff = o; o = align256(o + (size_t)L.R * L.B * (2 * L.B + 1) * sizeof(u32));
-    L.o_rend = o; o = align256(o + (size_t)L.R * L.B * (2 * L.B) * sizeof(u32));
+    L.o_roff = o; o = align256(o + (size_t)L.R * L.B * (2 * L.B2 + 1) * sizeof(u32));
+    L.o_rend = o; o = align256(o + (size_t)L.R * L.B * (2 * L.B2) * sizeof(u32));
     L.o_lres = o; o = align256(o + (size_t)L.R * L.B * 4 * sizeof(u32));
-    L.o_sres = o; o = align256(o + (size_t)L.R * 2 * L.B * 4 * sizeof(u32));
+    L.o_sres = o; o = align256(o + (size_t)L.R * 2 * L.B2 * 4 * sizeof(u32));
   }
   // L2-path table sets: the full path for large windows, the overflow hand-off otherwise.
   L.LC = next_pow2(2 * W);
@@ -173,7 +175,7 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
   if (use_fast) {
     Geo g;
     g.n = n; g.W = W; g.nw = L.nw;
-    g.logB = L.logB; g.B = L.B; g.cp = L.cp; g.cp_last = L.cp_last; g.R = L.R;
+    g.logB = L.logB; g.B = L.B; g.logB2 = L.logB2; g.B2 = L.B2; g.cp = L.cp; g.cp_last = L.cp_last; g.R = L.R;
     g.flags = flags;
     g.ticket = reinterpret_cast<u64*>(base);
     g.diag = reinterpret_cast<u32*>(base + DIAG_OFFSET);
@@ -186,7 +188,7 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
     g.rend = reinterpret_cast<u32*>(base + L.o_rend);
     g.lres = reinterpret_cast<u32*>(base + L.o_lres);
     g.sres = reinterpret_cast<u32*>(base + L.o_sres);
-    g.ips = 1ull + 3ull * g.B + g.cp;
+    g.ips = 1ull + 2ull * g.B2 + g.B + g.cp;
     g.total_items = (L.nw + LAG_F) * g.ips;
     u64 grid = (u64)d.fast_blocks;
     if (grid > g.total_items) grid = g.total_items;

@@ -43,7 +43,9 @@ constexpr int FT = NSG_FT;                   // threads per CTA (default 512: 2 
 constexpr int NWARP = FT / 32;
 constexpr int KPT = 8;                       // elements per thread per round
 constexpr int CH = FT * KPT;                 // 4096 keys per chunk / per gather round
-constexpr int TCAP = NSG_TCAP;               // SMEM hash-table slots (slot = (h * TCAP) >> 32)
+constexpr int TCAP = NSG_TCAP;               // link-table slots (slot = (h * TCAP) >> 32)
+constexpr int TCAP_S = 8192;                 // node-table slots of a side item
+constexpr int PCAP_S = 256;                  // side items' pending-list capacity
 constexpr int BUCKET_KEYS = NSG_BUCKET_KEYS; // target keys per link bucket (load factor ~1/3)
 constexpr int PCAP = NSG_PCAP;               // pending-list capacity (entries) per insertion wave
 constexpr int MAX_LOGB = 20 - (BUCKET_KEYS == 1024 ? 10 : BUCKET_KEYS == 2048 ? 11 : 12);  // B * BUCKET_KEYS <= 2^20
@@ -71,6 +73,7 @@ static_assert(RSLOTS > LAG_F && LAG_F > LAG_S && LAG_S > LAG_L && LAG_L >= 1, "s
 struct Geo {
   u64 n, W, nw;
   u32 logB, B, cp, cp_last, R;
+  u32 logB2, B2;    // side buckets per side (B2 = B/2: side items merge twice as many records)
   u64 ips;          // tickets per step
   u64 total_items;  // (nw + LAG_F) * ips
   u32 flags;
@@ -97,7 +100,7 @@ struct SmemL {
   u32 hist[2 * MAXB + 1];
 };
 struct SmemS {
-  u32 key[TCAP]; u32 P[TCAP]; u32 F[TCAP]; Pend pend[2][PCAP]; u32 wlo[NWARP][WSEG_S]; u32 wpre[NWARP][WSEG_S + 1];
+  u32 key[TCAP_S]; u32 P[TCAP_S]; u32 F[TCAP_S]; Pend pend[2][PCAP_S]; u32 wlo[NWARP][WSEG_S]; u32 wpre[NWARP][WSEG_S + 1];
 };
 struct SmemMisc {
   u32 wtmp[10 * NWARP];
@@ -195,9 +198,13 @@ __device__ __forceinline__ u32 probe_slot(u32 home, u32 probe) {
   const u32 x = home + probe;  // probe < TCAP
   return x >= (u32)TCAP ? x - TCAP : x;
 }
+__device__ __forceinline__ u32 probe_slot_s(u32 home, u32 probe) {
+  const u32 x = home + probe;  // probe < TCAP_S (a power of two)
+  return x & (TCAP_S - 1);
+}
 __device__ __forceinline__ u32 link_home(u64 key) { return home_slot((u32)hash64(key)); }
 // side buckets use the top bits of hash32(node), so the home slot uses an independent mix
-__device__ __forceinline__ u32 node_home(u32 node) { return home_slot(hash32(node ^ 0x9E3779B9u)); }
+__device__ __forceinline__ u32 node_home(u32 node) { return (u32)(((u64)hash32(node ^ 0x9E3779B9u) * (u64)TCAP_S) >> 32); }
 
 // one attempt: true if the key now owns `slot` (inserted or already there) and was counted
 __device__ __forceinline__ bool link_try(u64* lkey, u32* lcnt, u64 key, u32 add, u32 slot) {
@@ -223,8 +230,8 @@ __device__ __noinline__ bool link_finish(u64* lkey, u32* lcnt, u64 key, u32 add,
 }
 __device__ __noinline__ bool node_finish(u32* key, u32* P, u32* F, u32 node, u32 p, u32 f, u32 probe) {
   const u32 home = node_home(node);
-  for (; probe < (u32)TCAP; ++probe)
-    if (node_try(key, P, F, node, p, f, probe_slot(home, probe))) return true;
+  for (; probe < (u32)TCAP_S; ++probe)
+    if (node_try(key, P, F, node, p, f, probe_slot_s(home, probe))) return true;
   return false;
 }
 
@@ -237,7 +244,7 @@ __device__ __noinline__ bool node_flush(u32* key, u32* P, u32* F, u32* esc, u32 
 
 // Warp-aggregated append of the lanes with `want` to pending list `list`; must be called by all
 // lanes of the warp.  Returns false for a lane whose entry did not fit (the caller finishes it).
-__device__ __forceinline__ bool pend_push(Pend* list, u32* cnt, bool want, const Pend& e) {
+__device__ __forceinline__ bool pend_push(Pend* list, u32* cnt, bool want, const Pend& e, u32 cap = PCAP) {
   const u32 mask = __ballot_sync(0xffffffffu, want);
   if (mask == 0) return true;
   const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
@@ -246,7 +253,7 @@ __device__ __forceinline__ bool pend_push(Pend* list, u32* cnt, bool want, const
   base = __shfl_sync(0xffffffffu, base, leader);
   if (!want) return true;
   const u32 pos = base + __popc(mask & ((1u << lane) - 1u));
-  if (pos >= (u32)PCAP) return false;
+  if (pos >= cap) return false;
   list[pos] = e;
   return true;
 }
@@ -438,7 +445,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   PhaseTimer pt;
   const u32 ncp = chunks_of(g, w);
-  const u32 B = g.B, logB = g.logB;
+  const u32 B = g.B, B2 = g.B2, logB2 = g.logB2;
   const long long tstart = clock64();
   long long waited = 0;
   u32 dep = 0;
@@ -449,7 +456,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
     for (int i = t; i < TCAP / 2; i += FT) k2[i] = make_ulonglong2(EMPTY64, EMPTY64);
     for (int i = t; i < TCAP / 4; i += FT) c4[i] = make_uint4(0, 0, 0, 0);
   }
-  for (int i = t; i <= (int)(2 * B); i += FT) s.hist[i] = 0;
+  for (int i = t; i <= (int)(2 * B2); i += FT) s.hist[i] = 0;
   if (t < 4) m.esc[t] = 0;
   if (t == 0) { m.flag = 0; m.pcnt[0] = 0; waited = wait_geq(&g.pdone[w], g.cp, dep); }
   __syncthreads();  // also publishes thread 0's acquire to the CTA
@@ -490,11 +497,11 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
         if (entry && k[j] == EMPTY64) { atomicAdd(&m.esc[0], 1u); entry = false; }
         bool placed = true;
         u32 home = 0;
-        if (entry) { home = link_home(k[j]); placed = link_try_h(s.lkey, s.lcnt, s.hist, B, logB, k[j], 1u, home); }
-        if (!placed) placed = link_try_h(s.lkey, s.lcnt, s.hist, B, logB, k[j], 1u, probe_slot(home, 1u));
+        if (entry) { home = link_home(k[j]); placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, home); }
+        if (!placed) placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, probe_slot(home, 1u));
         const Pend e{k[j], 1u, 2u};
         if (!pend_push(s.pend[0], &m.pcnt[0], !placed, e))
-          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B, logB, k[j], 1u, 2u) && ok;
+          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, 2u) && ok;
       }
     }
   }
@@ -508,7 +515,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
       if (n <= WAVE_TAIL) {
         if ((u32)t < n) {
           const Pend e = s.pend[cur][t];
-          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B, logB, e.a, e.b, e.probe) && ok;
+          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, e.a, e.b, e.probe) && ok;
         }
         break;
       }
@@ -521,11 +528,11 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
         if (i < n) {
           e = s.pend[cur][i];
           if (e.probe >= (u32)TCAP) ok = false;
-          else placed = link_try_h(s.lkey, s.lcnt, s.hist, B, logB, e.a, e.b, probe_slot(link_home(e.a), e.probe));
+          else placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, e.a, e.b, probe_slot(link_home(e.a), e.probe));
         }
         e.probe += 1;
         if (!pend_push(s.pend[cur ^ 1], &m.pcnt[cur ^ 1], !placed, e))
-          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B, logB, e.a, e.b, e.probe) && ok;
+          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, e.a, e.b, e.probe) && ok;
       }
       __syncthreads();
       cur ^= 1;
@@ -534,17 +541,17 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
   }
   if (!ok) m.flag = 1;
   if (t == 0 && m.esc[0]) {  // the key ~0 (255.255.255.255 -> 255.255.255.255) is one more link
-    atomicAdd(&s.hist[side_bucket(EMPTY32, logB)], 1u);
-    atomicAdd(&s.hist[B + side_bucket(EMPTY32, logB)], 1u);
+    atomicAdd(&s.hist[side_bucket(EMPTY32, logB2)], 1u);
+    atomicAdd(&s.hist[B2 + side_bucket(EMPTY32, logB2)], 1u);
   }
   __syncthreads();
   pt.mark(g, 1, 2);
   // record region layout: offsets of every (side, side bucket), scanned and published by warp 0
-  warp0_exclusive_scan(s.hist, (int)(2 * B));
+  warp0_exclusive_scan(s.hist, (int)(2 * B2));
   if (t < 32) {
     __syncwarp();
-    u32* off = g.roff + ((u64)slot * B + b) * (2 * B + 1);
-    for (int i = t; i <= (int)(2 * B); i += 32) off[i] = s.hist[i];
+    u32* off = g.roff + ((u64)slot * B + b) * (2 * B2 + 1);
+    for (int i = t; i <= (int)(2 * B2); i += 32) off[i] = s.hist[i];
   }
   __syncthreads();
   pt.mark(g, 1, 3);
@@ -558,16 +565,16 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
       const u32 c = s.lcnt[i];
       nl += 1; mx = max(mx, c); sm += c;
       const u32 sn = (u32)(key >> 32), dn = (u32)key;
-      rec[atomicAdd(&s.hist[side_bucket(sn, logB)], 1u)] = make_rec(sn, 1u, c);
-      rec[atomicAdd(&s.hist[B + side_bucket(dn, logB)], 1u)] = make_rec(dn, 1u, c);
+      rec[atomicAdd(&s.hist[side_bucket(sn, logB2)], 1u)] = make_rec(sn, 1u, c);
+      rec[atomicAdd(&s.hist[B2 + side_bucket(dn, logB2)], 1u)] = make_rec(dn, 1u, c);
     }
   }
   if (t == 0 && m.esc[0]) {
     const u32 c = m.esc[0];
     nl += 1; mx = max(mx, c); sm += c;
     const u64 r = make_rec(EMPTY32, 1u, c);
-    rec[atomicAdd(&s.hist[side_bucket(EMPTY32, logB)], 1u)] = r;
-    rec[atomicAdd(&s.hist[B + side_bucket(EMPTY32, logB)], 1u)] = r;
+    rec[atomicAdd(&s.hist[side_bucket(EMPTY32, logB2)], 1u)] = r;
+    rec[atomicAdd(&s.hist[B2 + side_bucket(EMPTY32, logB2)], 1u)] = r;
   }
   nl = warp_sum(nl); mx = warp_max(mx); sm = warp_sum(sm);
   if (lane == 0) { m.wtmp[4 * NWARP + wid] = nl; m.wtmp[5 * NWARP + wid] = mx; m.wtmp[6 * NWARP + wid] = sm; }
@@ -578,8 +585,8 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
     u32 bm = lane < NWARP ? m.wtmp[5 * NWARP + lane] : 0u;
     u32 cs = lane < NWARP ? m.wtmp[6 * NWARP + lane] : 0u;
     a = warp_sum(a); bm = warp_max(bm); cs = warp_sum(cs);
-    u32* rend = g.rend + ((u64)slot * B + b) * (2 * B);
-    for (int i = lane; i < (int)(2 * B); i += 32) rend[i] = s.hist[i];  // cursors = segment ends
+    u32* rend = g.rend + ((u64)slot * B + b) * (2 * B2);
+    for (int i = lane; i < (int)(2 * B2); i += 32) rend[i] = s.hist[i];  // cursors = segment ends
     __syncwarp();
     if (lane == 0) {
       u32* r = g.lres + ((u64)slot * B + b) * 4;
@@ -598,7 +605,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
 __device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict__ out) {
   const int t = threadIdx.x;
   const u32 slot = slot_of(g, w);
-  if (t == 0) wait_geq(&g.sdone[w], 2 * g.B, ld_acquire32(&g.sdone[w]));
+  if (t == 0) wait_geq(&g.sdone[w], 2 * g.B2, ld_acquire32(&g.sdone[w]));
   __syncthreads();
   // sums: 0 links, 1 sum of counts, 2 unique sources, 3 unique destinations;
   // maxes: 4 max link, 5 max source packets, 6 max fan-out, 7 max destination packets, 8 max fan-in
@@ -606,8 +613,10 @@ __device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict_
   for (u32 i = t; i < g.B; i += FT) {
     const u32* r = g.lres + ((u64)slot * g.B + i) * 4;
     v[0] += ldcg32(r); v[4] = max(v[4], ldcg32(r + 1)); v[1] += ldcg32(r + 2);
-    const u32* s0 = g.sres + (((u64)slot * 2 + 0) * g.B + i) * 4;
-    const u32* s1 = g.sres + (((u64)slot * 2 + 1) * g.B + i) * 4;
+  }
+  for (u32 i = t; i < g.B2; i += FT) {
+    const u32* s0 = g.sres + (((u64)slot * 2 + 0) * g.B2 + i) * 4;
+    const u32* s1 = g.sres + (((u64)slot * 2 + 1) * g.B2 + i) * 4;
     v[2] += ldcg32(s0); v[5] = max(v[5], ldcg32(s0 + 1)); v[6] = max(v[6], ldcg32(s0 + 2));
     v[3] += ldcg32(s1); v[7] = max(v[7], ldcg32(s1 + 1)); v[8] = max(v[8], ldcg32(s1 + 2));
   }
@@ -649,7 +658,7 @@ __device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict_
 __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemMisc& m) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   PhaseTimer pt;
-  const u32 B = g.B;
+  const u32 B = g.B, B2 = g.B2;
   const long long tstart = clock64();
   long long waited = 0;
   u32 dep = 0;
@@ -658,7 +667,7 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
     uint4* k4 = reinterpret_cast<uint4*>(s.key);
     uint4* p4 = reinterpret_cast<uint4*>(s.P);
     uint4* f4 = reinterpret_cast<uint4*>(s.F);
-    for (int i = t; i < TCAP / 4; i += FT) {
+    for (int i = t; i < TCAP_S / 4; i += FT) {
       k4[i] = make_uint4(EMPTY32, EMPTY32, EMPTY32, EMPTY32);
       p4[i] = make_uint4(0, 0, 0, 0);
       f4[i] = make_uint4(0, 0, 0, 0);
@@ -677,8 +686,8 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
     u32 lo = 0, len = 0;
     if ((u32)lane < nseg) {
       const u32 lb = wid + lane * NWARP;
-      lo = ldcg32(g.roff + ((u64)slot * B + lb) * (2 * B + 1) + side * B + sb);
-      len = ldcg32(g.rend + ((u64)slot * B + lb) * (2 * B) + side * B + sb) - lo;
+      lo = ldcg32(g.roff + ((u64)slot * B + lb) * (2 * B2 + 1) + side * B2 + sb);
+      len = ldcg32(g.rend + ((u64)slot * B + lb) * (2 * B2) + side * B2 + sb) - lo;
       lo += lb * RCAP;
     }
     u32* wlo = s.wlo[wid];
@@ -725,9 +734,9 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
         bool placed = true;
         u32 home = 0;
         if (entry) { home = node_home(node); placed = node_try(s.key, s.P, s.F, node, p, f, home); }
-        if (!placed) placed = node_try(s.key, s.P, s.F, node, p, f, probe_slot(home, 1u));
+        if (!placed) placed = node_try(s.key, s.P, s.F, node, p, f, probe_slot_s(home, 1u));
         const Pend e{(u64)node | ((u64)f << 32), p, 2u};
-        if (!pend_push(s.pend[0], &m.pcnt[0], !placed, e)) ok = node_finish(s.key, s.P, s.F, node, p, f, 2u) && ok;
+        if (!pend_push(s.pend[0], &m.pcnt[0], !placed, e, PCAP_S)) ok = node_finish(s.key, s.P, s.F, node, p, f, 2u) && ok;
       }
     }
     if (c_has && lane == 0) ok = node_flush(s.key, s.P, s.F, m.esc, c_node, c_p, c_f) && ok;  // flush the cache
@@ -736,7 +745,7 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
   pt.mark(g, 2, 1);
   {
     int cur = 0;
-    u32 n = min(m.pcnt[0], (u32)PCAP);
+    u32 n = min(m.pcnt[0], (u32)PCAP_S);
     while (n) {
       if (n <= WAVE_TAIL) {
         if ((u32)t < n) {
@@ -753,16 +762,16 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
         bool placed = true;
         if (i < n) {
           e = s.pend[cur][i];
-          if (e.probe >= (u32)TCAP) ok = false;
-          else placed = node_try(s.key, s.P, s.F, (u32)e.a, e.b, (u32)(e.a >> 32), probe_slot(node_home((u32)e.a), e.probe));
+          if (e.probe >= (u32)TCAP_S) ok = false;
+          else placed = node_try(s.key, s.P, s.F, (u32)e.a, e.b, (u32)(e.a >> 32), probe_slot_s(node_home((u32)e.a), e.probe));
         }
         e.probe += 1;
-        if (!pend_push(s.pend[cur ^ 1], &m.pcnt[cur ^ 1], !placed, e))
+        if (!pend_push(s.pend[cur ^ 1], &m.pcnt[cur ^ 1], !placed, e, PCAP_S))
           ok = node_finish(s.key, s.P, s.F, (u32)e.a, e.b, (u32)(e.a >> 32), e.probe) && ok;
       }
       __syncthreads();
       cur ^= 1;
-      n = min(m.pcnt[cur], (u32)PCAP);
+      n = min(m.pcnt[cur], (u32)PCAP_S);
     }
   }
   if (!ok) m.flag = 1;
@@ -770,7 +779,7 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
   pt.mark(g, 2, 2);
   // unique nodes (1^T|A_t 1|_0 or its mirror), max packets (max A_t 1), max fan (max |A_t|_0 1)
   u32 d = 0, mp = 0, mf = 0;
-  for (int i = t; i < TCAP; i += FT) {
+  for (int i = t; i < TCAP_S; i += FT) {
     if (s.key[i] != EMPTY32) { d += 1; mp = max(mp, s.P[i]); mf = max(mf, s.F[i]); }
   }
   if (t == 0 && m.esc[1]) { d += 1; mp = max(mp, m.esc[1]); mf = max(mf, m.esc[2]); }
@@ -784,7 +793,7 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
     u32 cf = lane < NWARP ? m.wtmp[6 * NWARP + lane] : 0u;
     a = warp_sum(a); bp = warp_max(bp); cf = warp_max(cf);
     if (lane == 0) {
-      u32* res = g.sres + (((u64)slot * 2 + side) * B + sb) * 4;
+      u32* res = g.sres + (((u64)slot * 2 + side) * B2 + sb) * 4;
       res[0] = a; res[1] = bp; res[2] = cf;
       if (m.flag) mark_overflow(g, w);
       red_release_add32(&g.sdone[w], 1u);  // thread 0 wrote res itself: program order + release
@@ -794,7 +803,7 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
 }
 
 // ------------------------------------------------------------------------------------------
-// Ticket decoding: step k = tk / ips holds F(k-LAG_F), S(k-LAG_S) [2B], L(k-LAG_L) [B], P(k) [cp].
+// Ticket decoding: step k = tk / ips holds F(k-LAG_F), S(k-LAG_S) [2*B2], L(k-LAG_L) [B], P(k) [cp].
 // ------------------------------------------------------------------------------------------
 enum : u32 { ITEM_P = 0, ITEM_L = 1, ITEM_S0 = 2, ITEM_S1 = 3, ITEM_F = 4, ITEM_NOP = 5, ITEM_DONE = 6 };
 
@@ -815,8 +824,8 @@ __device__ __forceinline__ Item decode_ticket(const Geo& g, u64 tk) {
   u64 w;
   u32 type;
   if (idx == 0) { type = ITEM_F; w = k - LAG_F; }
-  else if ((idx -= 1) < 2ull * g.B) { type = idx < g.B ? ITEM_S0 : ITEM_S1; idx &= g.B - 1; w = k - LAG_S; }
-  else if ((idx -= 2ull * g.B) < g.B) { type = ITEM_L; w = k - LAG_L; }
+  else if ((idx -= 1) < 2ull * g.B2) { type = idx < g.B2 ? ITEM_S0 : ITEM_S1; idx &= g.B2 - 1; w = k - LAG_S; }
+  else if ((idx -= 2ull * g.B2) < g.B) { type = ITEM_L; w = k - LAG_L; }
   else { idx -= g.B; type = ITEM_P; w = k; }
   // windows before the first step of a class (w wrapped below 0) or past the end are no-ops
   if (w >= g.nw) type = ITEM_NOP;
