@@ -63,7 +63,8 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     const u64 want = (W + BUCKET_KEYS - 1) / BUCKET_KEYS;
     L.B = (u32)next_pow2(want < 1 ? 1 : want);
     L.logB = ilog2(L.B);
-    L.B2 = L.B > 1 ? L.B / 2 : 1;
+    const u64 want2 = (W + NODE_BUCKET - 1) / NODE_BUCKET;
+    L.B2 = (u32)next_pow2(want2 < 1 ? 1 : want2);
     L.logB2 = ilog2(L.B2);
     L.cp = (u32)((W + CH - 1) / CH);
     const u64 last = n - (L.nw - 1) * W;

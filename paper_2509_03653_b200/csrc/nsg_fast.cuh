@@ -31,13 +31,13 @@ namespace nsg {
 #define NSG_FT 512
 #endif
 #ifndef NSG_TCAP
-#define NSG_TCAP 6144
+#define NSG_TCAP 8192
 #endif
 #ifndef NSG_BUCKET_KEYS
-#define NSG_BUCKET_KEYS 2048
+#define NSG_BUCKET_KEYS 4096
 #endif
 #ifndef NSG_PCAP
-#define NSG_PCAP 512
+#define NSG_PCAP 256
 #endif
 constexpr int FT = NSG_FT;                   // threads per CTA (default 512: 2 CTAs per SM)
 constexpr int NWARP = FT / 32;
@@ -45,11 +45,13 @@ constexpr int KPT = 8;                       // elements per thread per round
 constexpr int CH = FT * KPT;                 // 4096 keys per chunk / per gather round
 constexpr int TCAP = NSG_TCAP;               // link-table slots (slot = (h * TCAP) >> 32)
 constexpr int TCAP_S = 8192;                 // node-table slots of a side item
+constexpr int NODE_BUCKET = TCAP_S / 2;      // side buckets are sized for <= 4096 nodes (load <= 1/2)
 constexpr int PCAP_S = 256;                  // side items' pending-list capacity
-constexpr int BUCKET_KEYS = NSG_BUCKET_KEYS; // target keys per link bucket (load factor ~1/3)
+constexpr int BUCKET_KEYS = NSG_BUCKET_KEYS; // target keys per link bucket (table load factor <= 1/2)
 constexpr int PCAP = NSG_PCAP;               // pending-list capacity (entries) per insertion wave
 constexpr int MAX_LOGB = 20 - (BUCKET_KEYS == 1024 ? 10 : BUCKET_KEYS == 2048 ? 11 : 12);  // B * BUCKET_KEYS <= 2^20
 constexpr int MAXB = 1 << MAX_LOGB;
+constexpr int MAXB2 = (1 << 20) / NODE_BUCKET;     // side buckets for the largest fast-path window
 constexpr u64 FAST_MAX_WINDOW = ((u64)BUCKET_KEYS << MAX_LOGB) - 1;  // 2^20 - 1: P fits a record's 20 bits
 constexpr int MAXCP = (int)((FAST_MAX_WINDOW + CH) / CH);
 // A link record: node << 32 | F << 20 | P (F = links merged into it, P = their packets; a window on
@@ -73,7 +75,7 @@ static_assert(RSLOTS > LAG_F && LAG_F > LAG_S && LAG_S > LAG_L && LAG_L >= 1, "s
 struct Geo {
   u64 n, W, nw;
   u32 logB, B, cp, cp_last, R;
-  u32 logB2, B2;    // side buckets per side (B2 = B/2: side items merge twice as many records)
+  u32 logB2, B2;    // side buckets per side: ceil(W / NODE_BUCKET) rounded up to a power of two
   u64 ips;          // tickets per step
   u64 total_items;  // (nw + LAG_F) * ips
   u32 flags;
@@ -97,7 +99,7 @@ constexpr int WSEG_S = (MAXB + NWARP - 1) / NWARP;
 static_assert(WSEG_L <= 32 && WSEG_S <= 32, "one segment per lane");
 struct SmemL {
   u64 lkey[TCAP]; u32 lcnt[TCAP]; Pend pend[2][PCAP]; u32 wlo[NWARP][WSEG_L]; u32 wpre[NWARP][WSEG_L + 1];
-  u32 hist[2 * MAXB + 1];
+  u32 hist[2 * MAXB2 + 1];
 };
 struct SmemS {
   u32 key[TCAP_S]; u32 P[TCAP_S]; u32 F[TCAP_S]; Pend pend[2][PCAP_S]; u32 wlo[NWARP][WSEG_S]; u32 wpre[NWARP][WSEG_S + 1];
