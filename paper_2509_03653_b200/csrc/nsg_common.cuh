@@ -8,6 +8,7 @@ namespace nsg {
 
 typedef unsigned long long u64;
 typedef uint32_t u32;
+typedef uint16_t u16;
 
 // Empty-slot sentinels.  Every 64-bit key and every 32-bit address is a legal value (DESIGN.md
 // reading R6), so the one key equal to a sentinel is never stored in a table: it is counted in a

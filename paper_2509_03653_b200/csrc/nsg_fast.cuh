@@ -37,7 +37,7 @@ namespace nsg {
 #define NSG_BUCKET_KEYS 4096
 #endif
 #ifndef NSG_PCAP
-#define NSG_PCAP 256
+#define NSG_PCAP 512
 #endif
 constexpr int FT = NSG_FT;                   // threads per CTA (default 512: 2 CTAs per SM)
 constexpr int NWARP = FT / 32;
@@ -46,7 +46,7 @@ constexpr int CH = FT * KPT;                 // 4096 keys per chunk / per gather
 constexpr int TCAP = NSG_TCAP;               // link-table slots (slot = (h * TCAP) >> 32)
 constexpr int TCAP_S = 8192;                 // node-table slots of a side item
 constexpr int NODE_BUCKET = TCAP_S / 2;      // side buckets are sized for <= 4096 nodes (load <= 1/2)
-constexpr int PCAP_S = 256;                  // side items' pending-list capacity
+constexpr int PCAP_S = 512;                  // side items' pending-list capacity
 constexpr int BUCKET_KEYS = NSG_BUCKET_KEYS; // target keys per link bucket (table load factor <= 1/2)
 constexpr int PCAP = NSG_PCAP;               // pending-list capacity (entries) per insertion wave
 constexpr int MAX_LOGB = 20 - (BUCKET_KEYS == 1024 ? 10 : BUCKET_KEYS == 2048 ? 11 : 12);  // B * BUCKET_KEYS <= 2^20
@@ -66,9 +66,7 @@ constexpr int LOG_RSLOTS = 5;
 constexpr int RSLOTS = 1 << LOG_RSLOTS;      // scratch slots (windows in flight), > LAG_S
 constexpr u32 RCAP = 2 * (TCAP + 1) + 6;     // records per link bucket (both sides), 8-aligned
 
-// An entry waiting for its next probe: a = key (link table) or node | f<<32 (node table),
-// b = count (link) or p (node), probe = probe distance to try next.
-struct Pend { u64 a; u32 b; u32 probe; };
+
 
 static_assert(RSLOTS > LAG_F && LAG_F > LAG_S && LAG_S > LAG_L && LAG_L >= 1, "schedule lags");
 
@@ -97,12 +95,14 @@ struct SmemP { u64 stage[CH]; u32 hist[MAXB + 1]; };
 constexpr int WSEG_L = (MAXCP + NWARP - 1) / NWARP;
 constexpr int WSEG_S = (MAXB + NWARP - 1) / NWARP;
 static_assert(WSEG_L <= 32 && WSEG_S <= 32, "one segment per lane");
+// Pending lists are SoA: a = the key (link item) or node<<32 | F<<20 | P (side item), p = next probe.
 struct SmemL {
-  u64 lkey[TCAP]; u32 lcnt[TCAP]; Pend pend[2][PCAP]; u32 wlo[NWARP][WSEG_L]; u32 wpre[NWARP][WSEG_L + 1];
+  u64 lkey[TCAP]; u32 lcnt[TCAP]; u64 pa[2][PCAP]; u16 pp[2][PCAP]; u32 wlo[NWARP][WSEG_L]; u32 wpre[NWARP][WSEG_L + 1];
   u32 hist[2 * MAXB2 + 1];
 };
 struct SmemS {
-  u32 key[TCAP_S]; u32 P[TCAP_S]; u32 F[TCAP_S]; Pend pend[2][PCAP_S]; u32 wlo[NWARP][WSEG_S]; u32 wpre[NWARP][WSEG_S + 1];
+  u32 key[TCAP_S]; u32 P[TCAP_S]; u32 F[TCAP_S]; u64 pa[2][PCAP_S]; u16 pp[2][PCAP_S]; u32 wlo[NWARP][WSEG_S];
+  u32 wpre[NWARP][WSEG_S + 1];
 };
 struct SmemMisc {
   u32 wtmp[10 * NWARP];
@@ -246,7 +246,7 @@ __device__ __noinline__ bool node_flush(u32* key, u32* P, u32* F, u32* esc, u32 
 
 // Warp-aggregated append of the lanes with `want` to pending list `list`; must be called by all
 // lanes of the warp.  Returns false for a lane whose entry did not fit (the caller finishes it).
-__device__ __forceinline__ bool pend_push(Pend* list, u32* cnt, bool want, const Pend& e, u32 cap = PCAP) {
+__device__ __forceinline__ bool pend_push(u64* la, u16* lp, u32* cnt, bool want, u64 a, u32 probe, u32 cap) {
   const u32 mask = __ballot_sync(0xffffffffu, want);
   if (mask == 0) return true;
   const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
@@ -256,7 +256,8 @@ __device__ __forceinline__ bool pend_push(Pend* list, u32* cnt, bool want, const
   if (!want) return true;
   const u32 pos = base + __popc(mask & ((1u << lane) - 1u));
   if (pos >= cap) return false;
-  list[pos] = e;
+  la[pos] = a;
+  lp[pos] = (u16)probe;
   return true;
 }
 
@@ -282,6 +283,15 @@ __device__ __forceinline__ long long wait_geq(const u32* p, u32 v, u32 first) {
 
 // Phase timer (NSG_FLAG_PROFILE): thread 0 adds the cycles since the previous mark to
 // prof[16 + type*16 + phase].  Marks are placed right after a __syncthreads().
+// profiling: after the first wave, add the number of entries that wanted the pending list to
+// prof[16 + 16*type + 12] and its max to prof[64 + 16*type + 12]
+__device__ __forceinline__ void prof_pending(const Geo& g, int type, u32 n) {
+  if ((g.flags & NSG_FLAG_PROFILE) && threadIdx.x == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[16 + type * 16 + 12]), (unsigned long long)n);
+    atomicMax(reinterpret_cast<unsigned long long*>(&g.prof[64 + type * 16 + 12]), (unsigned long long)n);
+  }
+}
+
 struct PhaseTimer {
   long long last;
   __device__ __forceinline__ PhaseTimer() { last = clock64(); }
@@ -501,40 +511,39 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
         u32 home = 0;
         if (entry) { home = link_home(k[j]); placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, home); }
         if (!placed) placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, probe_slot(home, 1u));
-        const Pend e{k[j], 1u, 2u};
-        if (!pend_push(s.pend[0], &m.pcnt[0], !placed, e))
+        if (!pend_push(s.pa[0], s.pp[0], &m.pcnt[0], !placed, k[j], 2u, PCAP))
           ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, 2u) && ok;
       }
     }
   }
   __syncthreads();
   pt.mark(g, 1, 1);
+  prof_pending(g, 1, m.pcnt[0]);
   {
     // waves 1..: the pending list, densely, one probe further each wave; a short tail finishes per lane
     int cur = 0;
     u32 n = min(m.pcnt[0], (u32)PCAP);
     while (n) {
       if (n <= WAVE_TAIL) {
-        if ((u32)t < n) {
-          const Pend e = s.pend[cur][t];
-          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, e.a, e.b, e.probe) && ok;
-        }
+        if ((u32)t < n) ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, s.pa[cur][t], 1u, s.pp[cur][t]) && ok;
         break;
       }
       if (t == 0) m.pcnt[cur ^ 1] = 0;
       __syncthreads();
       for (u32 i0 = 0; i0 < n; i0 += FT) {
         const u32 i = i0 + t;
-        Pend e{0, 0, 0};
+        u64 a = 0;
+        u32 probe = 0;
         bool placed = true;
         if (i < n) {
-          e = s.pend[cur][i];
-          if (e.probe >= (u32)TCAP) ok = false;
-          else placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, e.a, e.b, probe_slot(link_home(e.a), e.probe));
+          a = s.pa[cur][i];
+          probe = s.pp[cur][i];
+          if (probe >= (u32)TCAP) ok = false;
+          else placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, a, 1u, probe_slot(link_home(a), probe));
         }
-        e.probe += 1;
-        if (!pend_push(s.pend[cur ^ 1], &m.pcnt[cur ^ 1], !placed, e))
-          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, e.a, e.b, e.probe) && ok;
+        probe += 1;
+        if (!pend_push(s.pa[cur ^ 1], s.pp[cur ^ 1], &m.pcnt[cur ^ 1], !placed, a, probe, PCAP))
+          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, a, 1u, probe) && ok;
       }
       __syncthreads();
       cur ^= 1;
@@ -737,22 +746,24 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
         u32 home = 0;
         if (entry) { home = node_home(node); placed = node_try(s.key, s.P, s.F, node, p, f, home); }
         if (!placed) placed = node_try(s.key, s.P, s.F, node, p, f, probe_slot_s(home, 1u));
-        const Pend e{(u64)node | ((u64)f << 32), p, 2u};
-        if (!pend_push(s.pend[0], &m.pcnt[0], !placed, e, PCAP_S)) ok = node_finish(s.key, s.P, s.F, node, p, f, 2u) && ok;
+        if (!pend_push(s.pa[0], s.pp[0], &m.pcnt[0], !placed, make_rec(node, f, p), 2u, PCAP_S))
+          ok = node_finish(s.key, s.P, s.F, node, p, f, 2u) && ok;
       }
     }
     if (c_has && lane == 0) ok = node_flush(s.key, s.P, s.F, m.esc, c_node, c_p, c_f) && ok;  // flush the cache
   }
   __syncthreads();
   pt.mark(g, 2, 1);
+  prof_pending(g, 2, m.pcnt[0]);
   {
     int cur = 0;
     u32 n = min(m.pcnt[0], (u32)PCAP_S);
     while (n) {
       if (n <= WAVE_TAIL) {
         if ((u32)t < n) {
-          const Pend e = s.pend[cur][t];
-          ok = node_finish(s.key, s.P, s.F, (u32)e.a, e.b, (u32)(e.a >> 32), e.probe) && ok;
+          const u64 a = s.pa[cur][t];
+          ok = node_finish(s.key, s.P, s.F, (u32)(a >> 32), (u32)a & ((1u << REC_PBITS) - 1u),
+                           (u32)(a >> REC_PBITS) & REC_FMAX, s.pp[cur][t]) && ok;
         }
         break;
       }
@@ -760,16 +771,20 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
       __syncthreads();
       for (u32 i0 = 0; i0 < n; i0 += FT) {
         const u32 i = i0 + t;
-        Pend e{0, 0, 0};
+        u64 a = 0;
+        u32 probe = 0;
         bool placed = true;
+        const u32 nd = (u32)(s.pa[cur][min(i, n - 1)] >> 32);
         if (i < n) {
-          e = s.pend[cur][i];
-          if (e.probe >= (u32)TCAP_S) ok = false;
-          else placed = node_try(s.key, s.P, s.F, (u32)e.a, e.b, (u32)(e.a >> 32), probe_slot_s(node_home((u32)e.a), e.probe));
+          a = s.pa[cur][i];
+          probe = s.pp[cur][i];
+          if (probe >= (u32)TCAP_S) ok = false;
+          else placed = node_try(s.key, s.P, s.F, nd, (u32)a & ((1u << REC_PBITS) - 1u), (u32)(a >> REC_PBITS) & REC_FMAX,
+                                 probe_slot_s(node_home(nd), probe));
         }
-        e.probe += 1;
-        if (!pend_push(s.pend[cur ^ 1], &m.pcnt[cur ^ 1], !placed, e, PCAP_S))
-          ok = node_finish(s.key, s.P, s.F, (u32)e.a, e.b, (u32)(e.a >> 32), e.probe) && ok;
+        probe += 1;
+        if (!pend_push(s.pa[cur ^ 1], s.pp[cur ^ 1], &m.pcnt[cur ^ 1], !placed, a, probe, PCAP_S))
+          ok = node_finish(s.key, s.P, s.F, nd, (u32)a & ((1u << REC_PBITS) - 1u), (u32)(a >> REC_PBITS) & REC_FMAX, probe) && ok;
       }
       __syncthreads();
       cur ^= 1;

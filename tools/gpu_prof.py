@@ -64,4 +64,6 @@ for i, name in enumerate(["partition", "link", "side"]):
         print("     phases (avg cyc/item):", " ".join(f"{x / n:8.0f}" for x in ph if x))
         pm = prof[64 + 16 * i:64 + 16 * i + 8]
         print("     phases (max cyc/item):", " ".join(f"{x:8d}" for x in pm if x))
+        if prof[16 + 16 * i + 12]:
+            print(f"     first-wave pending entries: avg {prof[16 + 16 * i + 12] / n:.1f}, max {prof[64 + 16 * i + 12]}")
 print("diag", ws.diag())
