@@ -207,11 +207,16 @@ def main():
     if world != args.gpus:
         if world == 1 and args.gpus > 1:
             raise SystemExit("--gpus N>1 must be launched with torchrun (one rank per GPU)")
+    local = local % max(1, torch.cuda.device_count())  # NSG_BENCH_BACKEND=gloo may share one GPU
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        tdist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("NSG_BENCH_BACKEND", "nccl")  # "gloo": test the N>1 path on one GPU
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=dev)
+        else:
+            tdist.init_process_group(backend)
     dist_, seed, desc = workload(args.workload)
 
     n = WINDOWS_PER_STEP * WINDOW
@@ -261,8 +266,9 @@ def main():
     t_ms = start.elapsed_time(end)
     k_ms = [a.elapsed_time(b) for a, b in kev]
     k_avg = sum(k_ms) / len(k_ms)
+    coll_dev = dev if world > 1 and tdist.get_backend() == "nccl" else torch.device("cpu")
     if world > 1:
-        tt = torch.tensor([t_ms, k_avg], dtype=torch.float64, device=dev)
+        tt = torch.tensor([t_ms, k_avg], dtype=torch.float64, device=coll_dev)
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
         t_ms, k_avg = float(tt[0]), float(tt[1])
     total_pkts = n * world * args.steps
@@ -288,7 +294,7 @@ def main():
     torch.cuda.synchronize(dev)
     e2e_ms = e0.elapsed_time(e1)
     if world > 1:
-        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([e2e_ms], dtype=torch.float64, device=coll_dev)
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
         e2e_ms = float(tt[0])
     e2e_value = n * world * e2e_steps / (e2e_ms / 1e3)

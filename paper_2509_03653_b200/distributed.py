@@ -41,6 +41,9 @@ def gather_window_stats(local: torch.Tensor, n_windows: int, group=None) -> torc
     if local.shape != (w1 - w0, NUM_STATS) or local.dtype != torch.int64:
         raise ValueError(f"rank {rank}: expected int64 [{w1 - w0}, 9], got {tuple(local.shape)} {local.dtype}")
     rows = max(window_block(n_windows, r, world)[1] - window_block(n_windows, r, world)[0] for r in range(world))
+    home = local.device
+    if dist.get_backend(group) == "gloo" and local.is_cuda:  # gloo gathers host tensors
+        local = local.cpu()
     padded = torch.zeros((rows, NUM_STATS), dtype=torch.int64, device=local.device)
     padded[: w1 - w0].copy_(local)
     out = torch.empty((world * rows, NUM_STATS), dtype=torch.int64, device=local.device)
@@ -49,7 +52,7 @@ def gather_window_stats(local: torch.Tensor, n_windows: int, group=None) -> torc
     for r in range(world):
         a, b = window_block(n_windows, r, world)
         pieces.append(out[r * rows: r * rows + (b - a)])
-    return torch.cat(pieces, dim=0)
+    return torch.cat(pieces, dim=0).to(home)
 
 
 def distributed_window_stats(keys_local: torch.Tensor, n_windows: int, window: int, group=None,
