@@ -22,7 +22,7 @@ from gen.configs import sweep_config
 ap = argparse.ArgumentParser()
 ap.add_argument("--min-log2", type=int, default=28)
 ap.add_argument("--max-log2", type=int, default=32)
-ap.add_argument("--out", default=None)
+ap.add_argument("--out", default=None, help="JSON file (write it under gpurun_out/ to bring it back from the GPU box)")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
