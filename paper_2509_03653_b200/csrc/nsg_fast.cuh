@@ -432,7 +432,7 @@ __device__ __noinline__ bool link_finish_h(u64* lkey, u32* lcnt, u32* hist, u32 
   return false;
 }
 
-constexpr u32 WAVE_TAIL = 64;  // pending entries below this finish per lane (no more CTA waves)
+constexpr u32 WAVE_TAIL = 512; // pending entries (<= list capacity) finish per lane: measured faster than barrier-separated waves
 
 // Warp-level gather setup: lane q < nseg describes segment q of this warp (global element offset `lo`,
 // length `len`); the warp publishes segment starts and exclusive prefixes into its SMEM rows and
@@ -570,6 +570,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
   // (:180); and one record per link and side, node<<32 | 1<<20 | count.
   u64* rec = g.rscr + ((u64)slot * B + b) * RCAP;
   u32 nl = 0, mx = 0, sm = 0;
+#ifndef NSG_EXP_SKIP_EMIT  // timing experiment only: results are wrong when defined
   for (int i = t; i < TCAP; i += FT) {
     const u64 key = s.lkey[i];
     if (key != EMPTY64) {
@@ -580,6 +581,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
       rec[atomicAdd(&s.hist[B2 + side_bucket(dn, logB2)], 1u)] = make_rec(dn, 1u, c);
     }
   }
+#endif
   if (t == 0 && m.esc[0]) {
     const u32 c = m.esc[0];
     nl += 1; mx = max(mx, c); sm += c;
@@ -670,6 +672,11 @@ __device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict_
 // ------------------------------------------------------------------------------------------
 __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemMisc& m) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+#ifdef NSG_EXP_SKIP_S  // timing experiment only: results are wrong
+  if (t == 0) { wait_geq(&g.ldone[w], g.B, 0); red_release_add32(&g.sdone[w], 1u); }
+  __syncthreads();
+  return;
+#endif
   PhaseTimer pt;
   const u32 B = g.B, B2 = g.B2;
   const long long tstart = clock64();
