@@ -460,26 +460,18 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
   const u32 B = g.B, B2 = g.B2, logB2 = g.logB2;
   const long long tstart = clock64();
   long long waited = 0;
-  u32 dep = 0;
-  if (t == 0) dep = ld_acquire32(&g.pdone[w]);  // latency overlaps the table init
-  {
-    ulonglong2* k2 = reinterpret_cast<ulonglong2*>(s.lkey);
-    uint4* c4 = reinterpret_cast<uint4*>(s.lcnt);
-    for (int i = t; i < TCAP / 2; i += FT) k2[i] = make_ulonglong2(EMPTY64, EMPTY64);
-    for (int i = t; i < TCAP / 4; i += FT) c4[i] = make_uint4(0, 0, 0, 0);
-  }
-  for (int i = t; i <= (int)(2 * B2); i += FT) s.hist[i] = 0;
-  if (t < 4) m.esc[t] = 0;
-  if (t == 0) { m.flag = 0; m.pcnt[0] = 0; waited = wait_geq(&g.pdone[w], g.cp, dep); }
-  __syncthreads();  // also publishes thread 0's acquire to the CTA
-  pt.mark(g, 1, 0);
   const u32 slot = slot_of(g, w);
   const u32* koff = g.koff + (u64)slot * g.cp * (B + 1);
   const u64* ks = g.kscr + (u64)slot * g.cp * CH;
   bool ok = true;
+  // The partition items of window w are complete (thread 0 waited at the previous item boundary), so
+  // the gather starts at once: warp wid reads bucket b's segment of chunks wid, wid + NWARP, ... and
+  // issues its first round of key loads; their L2 latency overlaps the table initialisation below.
+  const u32 nseg = (u32)wid < ncp ? (ncp - 1 - wid) / NWARP + 1 : 0;
+  u32* wlo = s.wlo[wid];
+  u32* wpre = s.wpre[wid];
+  u32 total;
   {
-    // warp wid gathers bucket b's segment of chunks wid, wid + NWARP, ...; wave 0 runs per warp
-    const u32 nseg = (u32)wid < ncp ? (ncp - 1 - wid) / NWARP + 1 : 0;
     u32 lo = 0, len = 0;
     if ((u32)lane < nseg) {
       const u32 c = wid + lane * NWARP;
@@ -488,11 +480,30 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
       len = ldcg32(o + 1) - lo;
       lo += c * CH;
     }
-    u32* wlo = s.wlo[wid];
-    u32* wpre = s.wpre[wid];
-    const u32 total = warp_segments(wlo, wpre, nseg, lo, len);
-    for (u32 base = 0; base < total; base += 32 * KPT) {  // warp-uniform rounds
-      u64 k[KPT];
+    total = warp_segments(wlo, wpre, nseg, lo, len);
+  }
+  u64 k[KPT];
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    const u32 e = lane + 32 * j;
+    if (e < total) {
+      const u32 q = find_seg(wpre, nseg, e);
+      k[j] = ldcg64(ks + wlo[q] + (e - wpre[q]));
+    }
+  }
+  {
+    ulonglong2* k2 = reinterpret_cast<ulonglong2*>(s.lkey);
+    uint4* c4 = reinterpret_cast<uint4*>(s.lcnt);
+    for (int i = t; i < TCAP / 2; i += FT) k2[i] = make_ulonglong2(EMPTY64, EMPTY64);
+    for (int i = t; i < TCAP / 4; i += FT) c4[i] = make_uint4(0, 0, 0, 0);
+  }
+  for (int i = t; i <= (int)(2 * B2); i += FT) s.hist[i] = 0;
+  if (t < 4) m.esc[t] = 0;
+  if (t == 0) { m.flag = 0; m.pcnt[0] = 0; }
+  __syncthreads();
+  pt.mark(g, 1, 0);
+  for (u32 base = 0; base < total; base += 32 * KPT) {  // warp-uniform rounds
+    if (base) {
 #pragma unroll
       for (int j = 0; j < KPT; ++j) {
         const u32 e = base + lane + 32 * j;
@@ -501,19 +512,19 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
           k[j] = ldcg64(ks + wlo[q] + (e - wpre[q]));
         }
       }
-      // wave 0: one full-warp CAS per key at its home slot, then one at the next slot for the losers
+    }
+    // wave 0: one full-warp CAS per key at its home slot, then one at the next slot for the losers
 #pragma unroll
-      for (int j = 0; j < KPT; ++j) {
-        if (base + 32 * j >= total) break;  // warp-uniform
-        bool entry = base + lane + 32 * j < total;
-        if (entry && k[j] == EMPTY64) { atomicAdd(&m.esc[0], 1u); entry = false; }
-        bool placed = true;
-        u32 home = 0;
-        if (entry) { home = link_home(k[j]); placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, home); }
-        if (!placed) placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, probe_slot(home, 1u));
-        if (!pend_push(s.pa[0], s.pp[0], &m.pcnt[0], !placed, k[j], 2u, PCAP))
-          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, 2u) && ok;
-      }
+    for (int j = 0; j < KPT; ++j) {
+      if (base + 32 * j >= total) break;  // warp-uniform
+      bool entry = base + lane + 32 * j < total;
+      if (entry && k[j] == EMPTY64) { atomicAdd(&m.esc[0], 1u); entry = false; }
+      bool placed = true;
+      u32 home = 0;
+      if (entry) { home = link_home(k[j]); placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, home); }
+      if (!placed) placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, probe_slot(home, 1u));
+      if (!pend_push(s.pa[0], s.pp[0], &m.pcnt[0], !placed, k[j], 2u, PCAP))
+        ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, 2u) && ok;
     }
   }
   __syncthreads();
@@ -618,8 +629,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
 __device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict__ out) {
   const int t = threadIdx.x;
   const u32 slot = slot_of(g, w);
-  if (t == 0) wait_geq(&g.sdone[w], 2 * g.B2, ld_acquire32(&g.sdone[w]));
-  __syncthreads();
+  // all side items of window w are complete (waited for at the previous item boundary)
   // sums: 0 links, 1 sum of counts, 2 unique sources, 3 unique destinations;
   // maxes: 4 max link, 5 max source packets, 6 max fan-out, 7 max destination packets, 8 max fan-in
   u32 v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -681,27 +691,13 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
   const u32 B = g.B, B2 = g.B2;
   const long long tstart = clock64();
   long long waited = 0;
-  u32 dep = 0;
-  if (t == 0) dep = ld_acquire32(&g.ldone[w]);
-  {
-    uint4* k4 = reinterpret_cast<uint4*>(s.key);
-    uint4* p4 = reinterpret_cast<uint4*>(s.P);
-    uint4* f4 = reinterpret_cast<uint4*>(s.F);
-    for (int i = t; i < TCAP_S / 4; i += FT) {
-      k4[i] = make_uint4(EMPTY32, EMPTY32, EMPTY32, EMPTY32);
-      p4[i] = make_uint4(0, 0, 0, 0);
-      f4[i] = make_uint4(0, 0, 0, 0);
-    }
-  }
-  if (t < 4) m.esc[t] = 0;
-  if (t == 0) { m.flag = 0; m.pcnt[0] = 0; waited = wait_geq(&g.ldone[w], B, dep); }
-  __syncthreads();
-  pt.mark(g, 2, 0);
   const u32 slot = slot_of(g, w);
   const u64* rs = g.rscr + (u64)slot * B * RCAP;
   bool ok = true;
   {
-    // warp wid gathers side bucket sb's records from link buckets wid, wid + NWARP, ...
+    // All link items of window w are complete (waited for at the previous item boundary): warp wid
+    // gathers side bucket sb's records from link buckets wid, wid + NWARP, ... and issues its first
+    // round of loads before the table initialisation, which hides their L2 latency.
     const u32 nseg = (u32)wid < B ? (B - 1 - wid) / NWARP + 1 : 0;
     u32 lo = 0, len = 0;
     if ((u32)lane < nseg) {
@@ -713,25 +709,51 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
     u32* wlo = s.wlo[wid];
     u32* wpre = s.wpre[wid];
     const u32 total = warp_segments(wlo, wpre, nseg, lo, len);
+    u64 r[KPT];
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const u32 e = lane + 32 * j;
+      if (e < total) {
+        const u32 q = find_seg(wpre, nseg, e);
+        r[j] = ldcg64(rs + wlo[q] + (e - wpre[q]));
+      }
+    }
+    {
+      uint4* k4 = reinterpret_cast<uint4*>(s.key);
+      uint4* p4 = reinterpret_cast<uint4*>(s.P);
+      uint4* f4 = reinterpret_cast<uint4*>(s.F);
+      for (int i = t; i < TCAP_S / 4; i += FT) {
+        k4[i] = make_uint4(EMPTY32, EMPTY32, EMPTY32, EMPTY32);
+        p4[i] = make_uint4(0, 0, 0, 0);
+        f4[i] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    if (t < 4) m.esc[t] = 0;
+    if (t == 0) { m.flag = 0; m.pcnt[0] = 0; }
+    __syncthreads();
+    pt.mark(g, 2, 0);
     // Warp-uniform register cache of one hot node (e.g. the heavy source): records of the cached node
-    // are summed in registers across rounds and merged into the table once, when the entry is evicted.
-    // An entry is replaced only after a round in which it had fewer than 8 hits.
+    // are summed in lane registers across rounds and merged into the table once, when the entry is
+    // evicted.  An entry is replaced only after a round in which it had fewer than 8 hits.
     bool c_has = false;
     u32 c_node = 0, c_p = 0, c_f = 0, c_hits = 0;
     for (u32 base = 0; base < total; base += 32 * KPT) {  // warp-uniform rounds
-      u64 r[KPT];
+      if (base) {
 #pragma unroll
-      for (int j = 0; j < KPT; ++j) {
-        const u32 e = base + lane + 32 * j;
-        if (e < total) {
-          const u32 q = find_seg(wpre, nseg, e);
-          r[j] = ldcg64(rs + wlo[q] + (e - wpre[q]));
+        for (int j = 0; j < KPT; ++j) {
+          const u32 e = base + lane + 32 * j;
+          if (e < total) {
+            const u32 q = find_seg(wpre, nseg, e);
+            r[j] = ldcg64(rs + wlo[q] + (e - wpre[q]));
+          }
         }
       }
       if (!c_has || c_hits < 8) {  // (re)seed the cache with the first record of the round
         const u32 cand = __shfl_sync(0xffffffffu, (u32)(r[0] >> 32), 0);
-        if (c_has && cand != c_node && lane == 0)  // evict: merge the old entry into the table
-          ok = node_flush(s.key, s.P, s.F, m.esc, c_node, c_p, c_f) && ok;
+        if (c_has && cand != c_node) {  // evict: merge the old entry (lane partial sums) into the table
+          const u32 sp = warp_sum(c_p), sf = warp_sum(c_f);
+          if (lane == 0) ok = node_flush(s.key, s.P, s.F, m.esc, c_node, sp, sf) && ok;
+        }
         if (!c_has || cand != c_node) { c_node = cand; c_p = 0; c_f = 0; c_has = true; }
       }
       c_hits = 0;
@@ -743,12 +765,8 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
         const u32 p = (u32)r[j] & ((1u << REC_PBITS) - 1u);
         const u32 f = (u32)(r[j] >> REC_PBITS) & REC_FMAX;
         const bool hit = valid && node == c_node;
-        const u32 hm = __ballot_sync(0xffffffffu, hit);
-        if (hm) {
-          c_p += __reduce_add_sync(0xffffffffu, hit ? p : 0u);
-          c_f += __reduce_add_sync(0xffffffffu, hit ? f : 0u);
-          c_hits += (u32)__popc(hm);
-        }
+        c_hits += (u32)__popc(__ballot_sync(0xffffffffu, hit));
+        if (hit) { c_p += p; c_f += f; }  // lane partial sums; reduced once, when the entry is flushed
         bool entry = valid && !hit;
         if (entry && node == EMPTY32) { atomicAdd(&m.esc[1], p); atomicAdd(&m.esc[2], f); entry = false; }
         bool placed = true;
@@ -759,7 +777,10 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
           ok = node_finish(s.key, s.P, s.F, node, p, f, 2u) && ok;
       }
     }
-    if (c_has && lane == 0) ok = node_flush(s.key, s.P, s.F, m.esc, c_node, c_p, c_f) && ok;  // flush the cache
+    if (c_has) {  // flush the cache
+      const u32 sp = warp_sum(c_p), sf = warp_sum(c_f);
+      if (lane == 0) ok = node_flush(s.key, s.P, s.F, m.esc, c_node, sp, sf) && ok;
+    }
   }
   __syncthreads();
   pt.mark(g, 2, 1);
@@ -835,6 +856,27 @@ enum : u32 { ITEM_P = 0, ITEM_L = 1, ITEM_S0 = 2, ITEM_S1 = 3, ITEM_F = 4, ITEM_
 
 struct Item { u32 type, idx; u64 w; };
 
+// Thread 0: block until the dependencies of `it` are complete (acquire).  Called before the barrier
+// that starts the item, so the item's first loads can be issued at once.  An item only ever waits on
+// items with smaller tickets, so the schedule cannot deadlock.
+__device__ __forceinline__ long long wait_item_deps(const Geo& g, const Item& it) {
+  switch (it.type) {
+    case ITEM_P: return 0;  // waits inside, after issuing its HBM loads (slot reuse rarely blocks)
+    case ITEM_L: return wait_geq(&g.pdone[it.w], g.cp, 0u);                       // all chunks partitioned
+    case ITEM_S0:
+    case ITEM_S1: return wait_geq(&g.ldone[it.w], g.B, 0u);                       // all link buckets emitted
+    case ITEM_F: return wait_geq(&g.sdone[it.w], 2 * g.B2, 0u);                   // all side buckets merged
+    default: return 0;
+  }
+}
+__device__ __forceinline__ void prof_wait(const Geo& g, const Item& it, long long waited) {
+  if ((g.flags & NSG_FLAG_PROFILE) && waited) {
+    const int type = it.type == ITEM_P ? 0 : it.type == ITEM_L ? 1 : 2;
+    if (it.type <= ITEM_S1)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[type * 4 + 2]), (unsigned long long)waited);
+  }
+}
+
 __device__ __forceinline__ Item decode_ticket(const Geo& g, u64 tk) {
   Item it{ITEM_DONE, 0, 0};
   if (tk >= g.total_items) return it;
@@ -872,6 +914,7 @@ fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, con
   Item nxt{ITEM_DONE, 0, 0};
   if (threadIdx.x == 0) {
     const Item first = decode_ticket(g, atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull));
+    prof_wait(g, first, wait_item_deps(g, first));
     m.type = first.type; m.idx = first.idx; m.w = first.w;
     if (first.type != ITEM_DONE) tk_next = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
   }
@@ -902,7 +945,10 @@ fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, con
       __syncthreads();  // no-op ticket
     }
     // every item function passed a __syncthreads() after all threads read m.type/m.w/m.idx
-    if (threadIdx.x == 0) { m.type = nxt.type; m.idx = nxt.idx; m.w = nxt.w; }
+    if (threadIdx.x == 0) {
+      prof_wait(g, nxt, wait_item_deps(g, nxt));
+      m.type = nxt.type; m.idx = nxt.idx; m.w = nxt.w;
+    }
   }
 }
 
