@@ -29,7 +29,7 @@ namespace nsg {
 // ------------------------------------------------------------------------------------------
 constexpr size_t DIAG_OFFSET = 64;
 constexpr size_t PROF_OFFSET = 128;  // u64[16], NSG_FLAG_PROFILE
-constexpr size_t CTRL_BYTES = 1024;  // ticket, diag (64), prof u64[64] (128)
+constexpr size_t CTRL_BYTES = 4096;  // ticket, diag (64), prof u64[256] (128)
 constexpr u64 GLOBAL_BUDGET = 2ull << 30;  // cap on L2-path table memory
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }

@@ -110,6 +110,7 @@ struct SmemMisc {
   u32 flag, dep;
   u32 type, idx;
   u32 pcnt[2];  // pending-list fill counters
+  u32 hot[2];   // link item: per side, a side bucket holding >= 8x the average records (or ~0u)
   u64 w;
 };
 constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
@@ -568,6 +569,24 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
   }
   __syncthreads();
   pt.mark(g, 1, 2);
+  // A side bucket with >= 8x the average records (the heavy source's bucket) is "hot": its records
+  // are merged per node by a warp register cache during emission (below).
+  if (wid == 0) {
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      u32 mx = 0, mi = 0, tot = 0;
+      for (u32 i = lane; i < B2; i += 32) {
+        const u32 v = s.hist[side * B2 + i];
+        tot += v;
+        if (v > mx) { mx = v; mi = i; }
+      }
+      tot = warp_sum(tot);
+      const u32 gmx = warp_max(mx);
+      const u32 who = __ballot_sync(0xffffffffu, mx == gmx && gmx > 0);
+      const u32 gmi = __shfl_sync(0xffffffffu, mi, who ? __ffs(who) - 1 : 0);
+      if (lane == 0) m.hot[side] = (B2 > 1 && gmx >= 512 && gmx >= 8 * (tot / B2)) ? gmi : ~0u;
+    }
+  }
   // record region layout: offsets of every (side, side bucket), scanned and published by warp 0
   warp0_exclusive_scan(s.hist, (int)(2 * B2));
   if (t < 32) {
@@ -582,14 +601,57 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
   u64* rec = g.rscr + ((u64)slot * B + b) * RCAP;
   u32 nl = 0, mx = 0, sm = 0;
 #ifndef NSG_EXP_SKIP_EMIT  // timing experiment only: results are wrong when defined
-  for (int i = t; i < TCAP; i += FT) {
-    const u64 key = s.lkey[i];
-    if (key != EMPTY64) {
-      const u32 c = s.lcnt[i];
-      nl += 1; mx = max(mx, c); sm += c;
-      const u32 sn = (u32)(key >> 32), dn = (u32)key;
-      rec[atomicAdd(&s.hist[side_bucket(sn, logB2)], 1u)] = make_rec(sn, 1u, c);
-      rec[atomicAdd(&s.hist[B2 + side_bucket(dn, logB2)], 1u)] = make_rec(dn, 1u, c);
+  const u32 hot0 = m.hot[0], hot1 = m.hot[1];
+  if (hot0 == ~0u && hot1 == ~0u) {  // CTA-uniform: no skewed side bucket (the common case)
+    for (int i = t; i < TCAP; i += FT) {
+      const u64 key = s.lkey[i];
+      if (key != EMPTY64) {
+        const u32 c = s.lcnt[i];
+        nl += 1; mx = max(mx, c); sm += c;
+        const u32 sn = (u32)(key >> 32), dn = (u32)key;
+        rec[atomicAdd(&s.hist[side_bucket(sn, logB2)], 1u)] = make_rec(sn, 1u, c);
+        rec[atomicAdd(&s.hist[B2 + side_bucket(dn, logB2)], 1u)] = make_rec(dn, 1u, c);
+      }
+    }
+  } else {
+    // per side, a warp cache node (seeded from the hot bucket's first record of the warp while it has
+    // had no hit) whose links are summed in lane registers and emitted as one record per warp
+    u32 cn[2] = {0, 0}, ch[2] = {0, 0}, lp[2] = {0, 0}, lf[2] = {0, 0};
+    for (int i = t; i < TCAP; i += FT) {  // TCAP % FT == 0: every lane runs the same iterations
+      const u64 key = s.lkey[i];
+      const bool valid = key != EMPTY64;
+      const u32 c = valid ? s.lcnt[i] : 0u;
+      if (valid) { nl += 1; mx = max(mx, c); sm += c; }
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const u32 node = side ? (u32)key : (u32)(key >> 32);
+        const u32 sbk = side_bucket(node, logB2);
+        const u32 hot = side ? hot1 : hot0;
+        const bool inhot = valid && sbk == hot;
+        const u32 hm = __ballot_sync(0xffffffffu, inhot);
+        bool hit = false;
+        if (hm) {
+          if (ch[side] == 0) cn[side] = __shfl_sync(0xffffffffu, node, __ffs(hm) - 1);
+          hit = inhot && node == cn[side];
+          ch[side] += (u32)__popc(__ballot_sync(0xffffffffu, hit));
+          if (hit) { lp[side] += c; lf[side] += 1; }
+        }
+        if (valid && !hit) rec[atomicAdd(&s.hist[side * B2 + sbk], 1u)] = make_rec(node, 1u, c);
+      }
+    }
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const u32 p = warp_sum(lp[side]);
+      u32 f = warp_sum(lf[side]);
+      if (lane == 0 && f) {  // one merged record (split when F > REC_FMAX)
+        const u32 nrec = (f + REC_FMAX - 1) / REC_FMAX;
+        const u32 pos = atomicAdd(&s.hist[side * B2 + side_bucket(cn[side], logB2)], nrec);
+        for (u32 q = 0; q < nrec; ++q) {
+          const u32 fr = min(f, REC_FMAX);
+          rec[pos + q] = make_rec(cn[side], fr, q == 0 ? p : 0u);
+          f -= fr;
+        }
+      }
     }
   }
 #endif
@@ -709,6 +771,8 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
     u32* wlo = s.wlo[wid];
     u32* wpre = s.wpre[wid];
     const u32 total = warp_segments(wlo, wpre, nseg, lo, len);
+    if (lane == 0 && (g.flags & NSG_FLAG_PROFILE) && w == 0 && side * B2 + sb < 64)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[192 + side * B2 + sb]), (unsigned long long)total);
     u64 r[KPT];
 #pragma unroll
     for (int j = 0; j < KPT; ++j) {
@@ -839,6 +903,9 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
     u32 bp = lane < NWARP ? m.wtmp[5 * NWARP + lane] : 0u;
     u32 cf = lane < NWARP ? m.wtmp[6 * NWARP + lane] : 0u;
     a = warp_sum(a); bp = warp_max(bp); cf = warp_max(cf);
+    if (lane == 0 && (g.flags & NSG_FLAG_PROFILE) && w == 0 && side * B2 + sb < 64) {  // window-0 detail
+      g.prof[128 + side * B2 + sb] = (u64)(clock64() - tstart);
+    }
     if (lane == 0) {
       u32* res = g.sres + (((u64)slot * 2 + side) * B2 + sb) * 4;
       res[0] = a; res[1] = bp; res[2] = cf;
