@@ -44,14 +44,24 @@ constexpr int NWARP = FT / 32;
 constexpr int KPT = 8;                       // elements per thread per round
 constexpr int CH = FT * KPT;                 // 4096 keys per chunk / per gather round
 constexpr int TCAP = NSG_TCAP;               // link-table slots (slot = (h * TCAP) >> 32)
-constexpr int TCAP_S = 8192;                 // node-table slots of a side item
+#ifndef NSG_TCAP_S
+#define NSG_TCAP_S 8192
+#endif
+#ifndef NSG_PCAP_S
+#define NSG_PCAP_S 512
+#endif
+#ifndef NSG_LOG_FAST_WINDOW
+#define NSG_LOG_FAST_WINDOW 20
+#endif
+constexpr int TCAP_S = NSG_TCAP_S;           // node-table slots of a side item
 constexpr int NODE_BUCKET = TCAP_S / 2;      // side buckets are sized for <= 4096 nodes (load <= 1/2)
-constexpr int PCAP_S = 512;                  // side items' pending-list capacity
+constexpr int PCAP_S = NSG_PCAP_S;           // side items' pending-list capacity
 constexpr int BUCKET_KEYS = NSG_BUCKET_KEYS; // target keys per link bucket (table load factor <= 1/2)
 constexpr int PCAP = NSG_PCAP;               // pending-list capacity (entries) per insertion wave
-constexpr int MAX_LOGB = 20 - (BUCKET_KEYS == 1024 ? 10 : BUCKET_KEYS == 2048 ? 11 : 12);  // B * BUCKET_KEYS <= 2^20
+constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x >> 1); }
+constexpr int MAX_LOGB = NSG_LOG_FAST_WINDOW - ilog2c(BUCKET_KEYS);  // B * BUCKET_KEYS <= 2^LOG_FAST_WINDOW
 constexpr int MAXB = 1 << MAX_LOGB;
-constexpr int MAXB2 = (1 << 20) / NODE_BUCKET;     // side buckets for the largest fast-path window
+constexpr int MAXB2 = (1 << NSG_LOG_FAST_WINDOW) / NODE_BUCKET;  // side buckets for the largest fast window
 constexpr u64 FAST_MAX_WINDOW = ((u64)BUCKET_KEYS << MAX_LOGB) - 1;  // 2^20 - 1: P fits a record's 20 bits
 constexpr int MAXCP = (int)((FAST_MAX_WINDOW + CH) / CH);
 // A link record: node << 32 | F << 20 | P (F = links merged into it, P = their packets; a window on
@@ -974,27 +984,35 @@ fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, con
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmemMisc& m = *reinterpret_cast<SmemMisc*>(smem_raw);
   unsigned char* u = smem_raw + MISC_BYTES;
-  // Thread 0 keeps the ticket pipeline: the item after the current one is fetched (atomicAdd) one
-  // item ahead and decoded at the start of the current item, so the boundary barrier only publishes
-  // an already-decoded descriptor.
+  // The scheduler thread (lane 0 of warp 1) keeps the ticket pipeline: the item after the current one
+  // is fetched (atomicAdd) one item ahead and decoded at the start of the current item; at its end the
+  // scheduler waits for the next item's dependencies (acquire) while warp 0 is still doing the item's
+  // tail (result writes, release), so the two round trips overlap and the boundary barrier only
+  // publishes an already-decoded, ready descriptor.
+  const bool sched = threadIdx.x == 32;
   u64 tk_next = 0;
   Item nxt{ITEM_DONE, 0, 0};
-  if (threadIdx.x == 0) {
+  if (sched) {
     const Item first = decode_ticket(g, atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull));
     prof_wait(g, first, wait_item_deps(g, first));
     m.type = first.type; m.idx = first.idx; m.w = first.w;
     if (first.type != ITEM_DONE) tk_next = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
   }
+  long long t_end = 0;  // scheduler: clock at the end of the previous item (profiling)
   for (;;) {
     __syncthreads();
     const u32 type = m.type, idx = m.idx;
     const u64 w = m.w;
     if (type == ITEM_DONE) break;
-    if (threadIdx.x == 0) {
+    if (sched) {
+      if ((g.flags & NSG_FLAG_PROFILE) && t_end) {  // boundary: tail/wait overlap + barrier
+        atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[12]), (unsigned long long)(clock64() - t_end));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[13]), 1ull);
+      }
       nxt = decode_ticket(g, tk_next);
       if (nxt.type != ITEM_DONE) tk_next = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
     }
-    // every item function passes a __syncthreads() before thread 0 can overwrite m.type/m.w/m.idx
+    // every item function passes a __syncthreads() before the scheduler can overwrite m.type/m.w/m.idx
     if (type == ITEM_P) {
       if (idx < chunks_of(g, w)) {
         item_partition(g, src, dst, keys, w, idx, *reinterpret_cast<SmemP*>(u), m);
@@ -1012,7 +1030,8 @@ fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, con
       __syncthreads();  // no-op ticket
     }
     // every item function passed a __syncthreads() after all threads read m.type/m.w/m.idx
-    if (threadIdx.x == 0) {
+    if (sched) {
+      t_end = clock64();
       prof_wait(g, nxt, wait_item_deps(g, nxt));
       m.type = nxt.type; m.idx = nxt.idx; m.w = nxt.w;
     }

@@ -66,6 +66,8 @@ for i, name in enumerate(["partition", "link", "side"]):
         print("     phases (max cyc/item):", " ".join(f"{x:8d}" for x in pm if x))
         if prof[16 + 16 * i + 12]:
             print(f"     first-wave pending entries: avg {prof[16 + 16 * i + 12] / n:.1f}, max {prof[64 + 16 * i + 12]}")
+if prof[13]:
+    print(f"item boundary (thread 0: end of item -> start of next): avg {prof[12] / prof[13]:.0f} cyc over {prof[13]} boundaries")
 if "--items" in sys.argv:
     det = ws.buffer[ws.offset + 128:ws.offset + 128 + 8 * 256].view(torch.int64).cpu().numpy()
     print("window 0 side items (side*B2+sb: cycles / records):")
