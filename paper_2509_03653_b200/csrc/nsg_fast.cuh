@@ -2,14 +2,14 @@
 //
 // Window w (packets [w*W, min((w+1)*W, n))) is processed as
 //   P(w,c)      c < cp   : a CH-key chunk is read from HBM once (128-bit streaming loads), counting-
-//                          sorted in SMEM by link bucket b = top logB bits of hash64(key) and written
+//                          sorted in SMEM by link bucket b = top logB bits of kmix(key) and written
 //                          to the window's L2-resident scratch slot, with its bucket offsets.
 //   L(w,b)      b < B    : the keys of link bucket b (about W/B of them) are gathered from every chunk
 //                          and aggregated in an SMEM hash table key -> count: this is A_t restricted to
 //                          the bucket ("Link packets from i to j").  One scan gives the
 //                          bucket's unique links (:181), max link packets (:183) and sum of counts
 //                          (:180), and emits one record per link and side, node<<32 | count, into
-//                          side buckets sb = top logB bits of hash32(node).
+//                          side buckets sb = top logB bits of node*0x9E3779B1.
 //   S(w,side,sb)         : all records of side bucket sb (from every link bucket) are merged in an SMEM
 //                          table node -> (sum of counts, number of records): the row sums A_t 1 (:185)
 //                          and row nnz |A_t|_0 1 (:187) of those sources (or the column mirrors, :173).
@@ -215,9 +215,16 @@ __device__ __forceinline__ u32 probe_slot_s(u32 home, u32 probe) {
   const u32 x = home + probe;  // probe < TCAP_S (a power of two)
   return x & (TCAP_S - 1);
 }
-__device__ __forceinline__ u32 link_home(u64 key) { return home_slot((u32)hash64(key)); }
-// side buckets use the top bits of hash32(node), so the home slot uses an independent mix
-__device__ __forceinline__ u32 node_home(u32 node) { return (u32)(((u64)hash32(node ^ 0x9E3779B9u) * (u64)TCAP_S) >> 32); }
+// Cheap multiplicative mixes (one multiply each; hashes only steer performance, never results):
+// kmix's top bits pick the link bucket and its low 32 bits (which fold in the product's high half)
+// the home slot; side buckets take the top bits of node * 0x9E3779B1 and node homes the top bits of
+// an independent multiplier.
+__device__ __forceinline__ u64 kmix(u64 k) {
+  const u64 h = k * 0x9E3779B97F4A7C15ull;
+  return h ^ (h >> 29);
+}
+__device__ __forceinline__ u32 link_home(u64 key) { return home_slot((u32)kmix(key)); }
+__device__ __forceinline__ u32 node_home(u32 node) { return (u32)(((u64)(node * 0x85EBCA77u) * (u64)TCAP_S) >> 32); }
 
 // one attempt: true if the key now owns `slot` (inserted or already there) and was counted
 __device__ __forceinline__ bool link_try(u64* lkey, u32* lcnt, u64 key, u32 add, u32 slot) {
@@ -272,8 +279,8 @@ __device__ __forceinline__ bool pend_push(u64* la, u16* lp, u32* cnt, bool want,
   return true;
 }
 
-__device__ __forceinline__ u32 side_bucket(u32 node, u32 logB) { return logB ? hash32(node) >> (32 - logB) : 0u; }
-__device__ __forceinline__ u32 link_bucket(u64 key, u32 logB) { return logB ? (u32)(hash64(key) >> (64 - logB)) : 0u; }
+__device__ __forceinline__ u32 side_bucket(u32 node, u32 logB) { return logB ? (node * 0x9E3779B1u) >> (32 - logB) : 0u; }
+__device__ __forceinline__ u32 link_bucket(u64 key, u32 logB) { return logB ? (u32)(kmix(key) >> (64 - logB)) : 0u; }
 
 __device__ __forceinline__ void mark_overflow(const Geo& g, u64 w) {
   if (atomicExch(&g.ovf[w], 1u) == 0u) atomicAdd(&g.diag[0], 1u);
