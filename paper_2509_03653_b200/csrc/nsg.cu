@@ -12,6 +12,7 @@
 //   nsg_global.cuh — any window <= 2^31 and the fast path's overflow hand-off: one CTA per window
 //                    with global-memory hash tables.
 // This file holds the C ABI: argument checks, workspace layout, launches.
+#include <algorithm>
 #include "nsg.h"
 #include "nsg_common.cuh"
 #include "nsg_fast.cuh"
@@ -189,8 +190,27 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
     g.rend = reinterpret_cast<u32*>(base + L.o_rend);
     g.lres = reinterpret_cast<u32*>(base + L.o_lres);
     g.sres = reinterpret_cast<u32*>(base + L.o_sres);
-    g.ips = 1ull + 2ull * g.B2 + g.B + g.cp;
-    g.total_items = (L.nw + LAG_F) * g.ips;
+    {  // ticket regions (see Geo): breakpoints where an item class enters or leaves the schedule
+      u64 pts[8] = {0, (u64)LAG_L, (u64)LAG_S, (u64)LAG_F, L.nw, L.nw + LAG_L, L.nw + LAG_S, L.nw + LAG_F};
+      std::sort(pts, pts + 8);
+      u64 t = 0;
+      g.nreg = 0;
+      for (int i = 0; i + 1 < 8; ++i) {
+        const u64 a = pts[i], b = pts[i + 1];
+        if (a == b) continue;
+        u32 mask = 0, ips = 0;
+        if (a >= (u64)LAG_F && a < L.nw + LAG_F) { mask |= 1u; ips += 1; }
+        if (a >= (u64)LAG_S && a < L.nw + LAG_S) { mask |= 2u; ips += 2 * g.B2; }
+        if (a >= (u64)LAG_L && a < L.nw + LAG_L) { mask |= 4u; ips += g.B; }
+        if (a < L.nw) { mask |= 8u; ips += g.cp; }
+        if (!ips) continue;
+        g.reg_k0[g.nreg] = a; g.reg_t0[g.nreg] = t; g.reg_ips[g.nreg] = ips; g.reg_mask[g.nreg] = mask;
+        t += (b - a) * ips;
+        ++g.nreg;
+      }
+      g.reg_t0[g.nreg] = t;
+      g.total_items = t;
+    }
     u64 grid = (u64)d.fast_blocks;
     if (grid > g.total_items) grid = g.total_items;
     if (ev_before && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_before), s) != cudaSuccess) return NSG_ERR_CUDA;
@@ -263,6 +283,21 @@ nsg_status nsg_window_stats_timed(const uint32_t* src, const uint32_t* dst, cons
 size_t nsg_diag_offset(void) { return nsg::DIAG_OFFSET; }
 
 unsigned nsg_last_launches(void) { return nsg::g_last_launches; }
+
+#ifdef NSG_EXP_TRACE
+// timing experiment only: copy the item trace of the last launches to `host` (u64[cap][4]) and reset
+unsigned nsg_debug_trace(void* host, unsigned cap) {
+  unsigned n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, nsg::g_trace_n, sizeof(n));
+  n = n < cap ? n : cap;
+  if (n > nsg::TRACE_CAP) n = nsg::TRACE_CAP;
+  cudaMemcpyFromSymbol(host, nsg::g_trace, (size_t)n * 32);
+  const unsigned z = 0;
+  cudaMemcpyToSymbol(nsg::g_trace_n, &z, sizeof(z));
+  return n;
+}
+#endif
 
 const char* nsg_status_string(nsg_status s) {
   switch (s) {

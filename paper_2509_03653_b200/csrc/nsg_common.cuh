@@ -46,7 +46,11 @@ __device__ __forceinline__ void st_release32(u32* p, u32 v) {
 // publishes every write the CTA made before the barrier (PTX causality order is cumulative through
 // bar.sync; the same pattern as CUTLASS's GenericBarrier).
 __device__ __forceinline__ void red_release_add32(u32* p, u32 v) {
+#ifndef NSG_EXP_RELAXED_RELEASE
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#else  // timing experiment only: no ordering
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#endif
 }
 
 // Drop a 128-byte L2 line without writing it back (its contents become undefined).

@@ -15,8 +15,9 @@
 //                          and row nnz |A_t|_0 1 (:187) of those sources (or the column mirrors, :173).
 //                          A scan gives unique nodes (:184), max packets (:186), max fan (:188).
 //   F(w)                 : reduces the per-bucket partials of window w to the nine outputs.
-// Items are handed out by one global ticket counter in steps of IPS = 1 + 2B + B + cp tickets:
-// step k = F(k-LAG_F), S(k-LAG_S), L(k-LAG_L), P(k) (out-of-range windows are no-ops).  Every item
+// Items are handed out by one global ticket counter in steps of up to 1 + 2B2 + B + cp tickets:
+// step k = F(k-LAG_F), S(k-LAG_S), L(k-LAG_L), P(k) (classes whose window is out of range take no
+// ticket).  Every item
 // waits only on items with smaller tickets, so the schedule cannot deadlock; a scratch slot is reused
 // once its previous window is final (RSLOTS windows in flight).  Dependencies are counted
 // semaphores: __syncthreads() + red.release.gpu by one thread to signal, ld.acquire.gpu spin by one
@@ -78,14 +79,20 @@ constexpr u32 RCAP = (2 * (TCAP + 1) + 15) & ~15u;  // records per link bucket (
 
 
 
+constexpr int MAX_REG = 8;  // ticket regions (the 8 breakpoints 0, LAG_*, nw + LAG_* split at most 7)
 static_assert(RSLOTS > LAG_F && LAG_F > LAG_S && LAG_S > LAG_L && LAG_L >= 1, "schedule lags");
 
 struct Geo {
   u64 n, W, nw;
   u32 logB, B, cp, cp_last, R;
   u32 logB2, B2;    // side buckets per side: ceil(W / NODE_BUCKET) rounded up to a power of two
-  u64 ips;          // tickets per step
-  u64 total_items;  // (nw + LAG_F) * ips
+  // Ticket regions: steps [reg_k0[r], reg_k0[r+1]) all hold the same item classes (reg_mask bits:
+  // 1 F, 2 S, 4 L, 8 P), reg_ips[r] tickets each, starting at ticket reg_t0[r].  Steps with a class
+  // out of range (before its lag, or past the last window) simply have fewer tickets: no no-op items.
+  u32 nreg;
+  u32 reg_ips[MAX_REG], reg_mask[MAX_REG];
+  u64 reg_k0[MAX_REG], reg_t0[MAX_REG + 1];
+  u64 total_items;
   u32 flags;
   u64* ticket;
   u32* diag;
@@ -500,6 +507,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
     }
     total = warp_segments(wlo, wpre, nseg, lo, len);
   }
+  pt.mark(g, 1, 5);
   u64 k[KPT];
 #pragma unroll
   for (int j = 0; j < KPT; ++j) {
@@ -509,6 +517,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
       k[j] = ldcg64(ks + wlo[q] + (e - wpre[q]));
     }
   }
+  pt.mark(g, 1, 6);
   {
     ulonglong2* k2 = reinterpret_cast<ulonglong2*>(s.lkey);
     uint4* c4 = reinterpret_cast<uint4*>(s.lcnt);
@@ -518,8 +527,14 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
   for (int i = t; i <= (int)(2 * B2); i += FT) s.hist[i] = 0;
   if (t < 4) m.esc[t] = 0;
   if (t == 0) { m.flag = 0; m.pcnt[0] = 0; }
+  pt.mark(g, 1, 7);
   __syncthreads();
   pt.mark(g, 1, 0);
+#ifdef NSG_EXP_MARK_KEYS
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) asm volatile("" ::"l"(k[j]));
+  pt.mark(g, 1, 8);
+#endif
   for (u32 base = 0; base < total; base += 32 * KPT) {  // warp-uniform rounds
     if (base) {
 #pragma unroll
@@ -698,6 +713,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
       __threadfence_block();
       red_release_add32(&g.ldone[w], 1u);  // after the CTA barrier; warp 0's writes precede it
       prof_add(g, 1, clock64() - tstart, waited);
+      pt.mark(g, 1, 9);
     }
   }
 }
@@ -929,12 +945,14 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
       if (m.flag) mark_overflow(g, w);
       red_release_add32(&g.sdone[w], 1u);  // thread 0 wrote res itself: program order + release
       prof_add(g, 2, clock64() - tstart, waited);
+      pt.mark(g, 2, 9);
     }
   }
 }
 
 // ------------------------------------------------------------------------------------------
-// Ticket decoding: step k = tk / ips holds F(k-LAG_F), S(k-LAG_S) [2*B2], L(k-LAG_L) [B], P(k) [cp].
+// Ticket decoding: step k holds F(k-LAG_F), S(k-LAG_S) [2*B2], L(k-LAG_L) [B], P(k) [cp], each class
+// only while its window is in [0, nw).
 // ------------------------------------------------------------------------------------------
 enum : u32 { ITEM_P = 0, ITEM_L = 1, ITEM_S0 = 2, ITEM_S1 = 3, ITEM_F = 4, ITEM_NOP = 5, ITEM_DONE = 6 };
 
@@ -964,26 +982,45 @@ __device__ __forceinline__ void prof_wait(const Geo& g, const Item& it, long lon
 __device__ __forceinline__ Item decode_ticket(const Geo& g, u64 tk) {
   Item it{ITEM_DONE, 0, 0};
   if (tk >= g.total_items) return it;
+  u32 r = 0;
+  while (r + 1 < g.nreg && tk >= g.reg_t0[r + 1]) ++r;
+  const u64 rel = tk - g.reg_t0[r];
+  const u32 ips = g.reg_ips[r];
   u64 k, idx;
-  if (g.total_items <= 0xFFFFFFFFull) {  // 32-bit division when it fits (the usual case)
-    const u32 k32 = (u32)tk / (u32)g.ips;
-    k = k32;
-    idx = (u32)tk - k32 * (u32)g.ips;
+  if (rel <= 0xFFFFFFFFull) {  // 32-bit division when it fits (the usual case)
+    const u32 q = (u32)rel / ips;
+    k = q;
+    idx = (u32)rel - q * ips;
   } else {
-    k = tk / g.ips;
-    idx = tk - k * g.ips;
+    k = rel / ips;
+    idx = rel - k * ips;
   }
+  k += g.reg_k0[r];
+  const u32 mask = g.reg_mask[r];
   u64 w;
   u32 type;
-  if (idx == 0) { type = ITEM_F; w = k - LAG_F; }
-  else if ((idx -= 1) < 2ull * g.B2) { type = idx < g.B2 ? ITEM_S0 : ITEM_S1; idx &= g.B2 - 1; w = k - LAG_S; }
-  else if ((idx -= 2ull * g.B2) < g.B) { type = ITEM_L; w = k - LAG_L; }
-  else { idx -= g.B; type = ITEM_P; w = k; }
-  // windows before the first step of a class (w wrapped below 0) or past the end are no-ops
-  if (w >= g.nw) type = ITEM_NOP;
+  if ((mask & 1u) && idx == 0) { type = ITEM_F; w = k - LAG_F; }
+  else {
+    if (mask & 1u) idx -= 1;
+    if ((mask & 2u) && idx < 2ull * g.B2) { type = idx < g.B2 ? ITEM_S0 : ITEM_S1; idx &= g.B2 - 1; w = k - LAG_S; }
+    else {
+      if (mask & 2u) idx -= 2ull * g.B2;
+      if ((mask & 4u) && idx < g.B) { type = ITEM_L; w = k - LAG_L; }
+      else {
+        if (mask & 4u) idx -= g.B;
+        type = ITEM_P; w = k;
+      }
+    }
+  }
   it.type = type; it.w = w; it.idx = (u32)idx;
   return it;
 }
+
+#ifdef NSG_EXP_TRACE  // timing experiment: per-item (type|w|idx, start ns, end ns, smid) records
+constexpr u32 TRACE_CAP = 1u << 18;
+__device__ u64 g_trace[TRACE_CAP][4];
+__device__ u32 g_trace_n;
+#endif
 
 __global__ void __launch_bounds__(FT, 1024 / FT)
 fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, const u64* __restrict__ keys,
@@ -1019,6 +1056,10 @@ fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, con
       nxt = decode_ticket(g, tk_next);
       if (nxt.type != ITEM_DONE) tk_next = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
     }
+#ifdef NSG_EXP_TRACE
+    u64 tr0 = 0;
+    if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr0));
+#endif
     // every item function passes a __syncthreads() before the scheduler can overwrite m.type/m.w/m.idx
     if (type == ITEM_P) {
       if (idx < chunks_of(g, w)) {
@@ -1036,6 +1077,18 @@ fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, con
     } else {
       __syncthreads();  // no-op ticket
     }
+#ifdef NSG_EXP_TRACE
+    if (threadIdx.x == 0) {
+      u64 tr1, smid;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr1));
+      asm volatile("{ .reg .u32 r; mov.u32 r, %%smid; cvt.u64.u32 %0, r; }" : "=l"(smid));
+      const u32 e = atomicAdd(&g_trace_n, 1u);
+      if (e < TRACE_CAP) {
+        g_trace[e][0] = ((u64)type << 56) | ((w & 0xFFFFFFull) << 32) | idx;
+        g_trace[e][1] = tr0; g_trace[e][2] = tr1; g_trace[e][3] = smid;
+      }
+    }
+#endif
     // every item function passed a __syncthreads() after all threads read m.type/m.w/m.idx
     if (sched) {
       t_end = clock64();

@@ -60,9 +60,9 @@ for i, name in enumerate(["partition", "link", "side"]):
     if n:
         print(f"  {name:9s}: {n:7d} items, avg {cyc / n:9.0f} cyc ({cyc / n / clk * 1e6:6.2f} us), avg wait {wait / n:8.0f} cyc; max work {mx:8d};"
               f" total {cyc / clk * 1e3:8.2f} CTA-ms")
-        ph = prof[16 + 16 * i:16 + 16 * i + 8]
+        ph = prof[16 + 16 * i:16 + 16 * i + 12]
         print("     phases (avg cyc/item):", " ".join(f"{x / n:8.0f}" for x in ph if x))
-        pm = prof[64 + 16 * i:64 + 16 * i + 8]
+        pm = prof[64 + 16 * i:64 + 16 * i + 12]
         print("     phases (max cyc/item):", " ".join(f"{x:8d}" for x in pm if x))
         if prof[16 + 16 * i + 12]:
             print(f"     first-wave pending entries: avg {prof[16 + 16 * i + 12] / n:.1f}, max {prof[64 + 16 * i + 12]}")
