@@ -194,20 +194,37 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
       u64 pts[8] = {0, (u64)LAG_L, (u64)LAG_S, (u64)LAG_F, L.nw, L.nw + LAG_L, L.nw + LAG_S, L.nw + LAG_F};
       std::sort(pts, pts + 8);
       u64 t = 0;
+      bool bad = false;
       g.nreg = 0;
-      for (int i = 0; i + 1 < 8; ++i) {
-        const u64 a = pts[i], b = pts[i + 1];
-        if (a == b) continue;
+      auto add = [&](u64 a, u64 b, u32 keep) {  // steps [a, b), the classes in `keep` only
         u32 mask = 0, ips = 0;
         if (a >= (u64)LAG_F && a < L.nw + LAG_F) { mask |= 1u; ips += 1; }
         if (a >= (u64)LAG_S && a < L.nw + LAG_S) { mask |= 2u; ips += 2 * g.B2; }
         if (a >= (u64)LAG_L && a < L.nw + LAG_L) { mask |= 4u; ips += g.B; }
         if (a < L.nw) { mask |= 8u; ips += g.cp; }
-        if (!ips) continue;
+        if (!(mask & keep)) return;
+        if ((mask & keep) != mask) {  // recount for the kept classes
+          mask &= keep;
+          ips = ((mask & 1u) ? 1 : 0) + ((mask & 2u) ? 2 * g.B2 : 0) + ((mask & 4u) ? g.B : 0) + ((mask & 8u) ? g.cp : 0);
+        }
+        if (g.nreg >= (u32)MAX_REG) { bad = true; return; }
         g.reg_k0[g.nreg] = a; g.reg_t0[g.nreg] = t; g.reg_ips[g.nreg] = ips; g.reg_mask[g.nreg] = mask;
         t += (b - a) * ips;
         ++g.nreg;
+      };
+      for (int i = 0; i + 1 < 8; ++i) {
+        const u64 a = pts[i], b = pts[i + 1];
+        if (a == b) continue;
+        if (a >= L.nw && a < L.nw + LAG_L) {
+          // drain: once the last partition items are out, every remaining link item goes first (they
+          // head the longest remaining chains), then the side and final items of those steps
+          add(a, b, 4u);
+          add(a, b, 3u);
+        } else {
+          add(a, b, 15u);
+        }
       }
+      if (bad) return NSG_ERR_INTERNAL;
       g.reg_t0[g.nreg] = t;
       g.total_items = t;
     }

@@ -79,7 +79,7 @@ constexpr u32 RCAP = (2 * (TCAP + 1) + 15) & ~15u;  // records per link bucket (
 
 
 
-constexpr int MAX_REG = 8;  // ticket regions (the 8 breakpoints 0, LAG_*, nw + LAG_* split at most 7)
+constexpr int MAX_REG = 10;  // ticket regions: <= 7 between the breakpoints 0, LAG_*, nw + LAG_*, +2 drain splits
 static_assert(RSLOTS > LAG_F && LAG_F > LAG_S && LAG_S > LAG_L && LAG_L >= 1, "schedule lags");
 
 struct Geo {
@@ -342,8 +342,23 @@ __device__ __forceinline__ void prof_add(const Geo& g, int type, long long cyc, 
 // ------------------------------------------------------------------------------------------
 // P item: partition one chunk of window w by link bucket
 // ------------------------------------------------------------------------------------------
+// The scheduler thread's claim of the next ticket.  Items call now() late in their body (before their
+// last phase), so that the claim's round trip overlaps that phase but a claimed ticket is not held for
+// a whole item (which would delay the items on the critical path at the end of a launch).
+constexpr int SCHED_THREAD = 32;
+struct Claim {
+  u64 tk;
+  bool done;
+  __device__ __forceinline__ void now(const Geo& g) {
+    if (threadIdx.x == SCHED_THREAD && !done) {
+      tk = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
+      done = true;
+    }
+  }
+};
+
 __device__ void item_partition(const Geo& g, const u32* __restrict__ src, const u32* __restrict__ dst,
-                               const u64* __restrict__ keys, u64 w, u32 c, SmemP& s, SmemMisc& m) {
+                               const u64* __restrict__ keys, u64 w, u32 c, SmemP& s, SmemMisc& m, Claim& cl) {
   const int t = threadIdx.x;
   PhaseTimer pt;
   const long long tstart = clock64();
@@ -411,6 +426,7 @@ __device__ void item_partition(const Geo& g, const u32* __restrict__ src, const 
   }
   __syncthreads();
   pt.mark(g, 0, 2);
+  cl.now(g);
 #pragma unroll
   for (int j = 0; j < KPT; ++j) {
     if (full || t + j * FT < (int)len) {
@@ -478,7 +494,7 @@ __device__ __forceinline__ u32 warp_segments(u32* wlo, u32* wpre, u32 nseg, u32 
   return total;
 }
 
-__device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
+__device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Claim& cl) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   PhaseTimer pt;
   const u32 ncp = chunks_of(g, w);
@@ -628,6 +644,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m) {
   }
   __syncthreads();
   pt.mark(g, 1, 3);
+  cl.now(g);
   // One pass over the bucket's part of A_t: unique links (:181), max link packets (:183), sum of counts
   // (:180); and one record per link and side, node<<32 | 1<<20 | count.
   u64* rec = g.rscr + ((u64)slot * B + b) * RCAP;
@@ -775,7 +792,7 @@ __device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict_
 // ------------------------------------------------------------------------------------------
 // S item: merge side bucket sb of one side of window w
 // ------------------------------------------------------------------------------------------
-__device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemMisc& m) {
+__device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemMisc& m, Claim& cl) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
 #ifdef NSG_EXP_SKIP_S  // timing experiment only: results are wrong
   if (t == 0) { wait_geq(&g.ldone[w], g.B, 0); red_release_add32(&g.sdone[w], 1u); }
@@ -921,6 +938,7 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
   if (!ok) m.flag = 1;
   __syncthreads();
   pt.mark(g, 2, 2);
+  cl.now(g);
   // unique nodes (1^T|A_t 1|_0 or its mirror), max packets (max A_t 1), max fan (max |A_t|_0 1)
   u32 d = 0, mp = 0, mf = 0;
   for (int i = t; i < TCAP_S; i += FT) {
@@ -1028,19 +1046,16 @@ fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, con
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SmemMisc& m = *reinterpret_cast<SmemMisc*>(smem_raw);
   unsigned char* u = smem_raw + MISC_BYTES;
-  // The scheduler thread (lane 0 of warp 1) keeps the ticket pipeline: the item after the current one
-  // is fetched (atomicAdd) one item ahead and decoded at the start of the current item; at its end the
-  // scheduler waits for the next item's dependencies (acquire) while warp 0 is still doing the item's
-  // tail (result writes, release), so the two round trips overlap and the boundary barrier only
+  // The scheduler thread (lane 0 of warp 1) claims the next ticket late in the current item (Claim),
+  // and at its end decodes it and waits for its dependencies (acquire) while warp 0 is still doing the
+  // item's tail (result writes, release), so the round trips overlap and the boundary barrier only
   // publishes an already-decoded, ready descriptor.
-  const bool sched = threadIdx.x == 32;
-  u64 tk_next = 0;
-  Item nxt{ITEM_DONE, 0, 0};
+  const bool sched = threadIdx.x == SCHED_THREAD;
+  Claim cl{0, false};
   if (sched) {
     const Item first = decode_ticket(g, atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull));
     prof_wait(g, first, wait_item_deps(g, first));
     m.type = first.type; m.idx = first.idx; m.w = first.w;
-    if (first.type != ITEM_DONE) tk_next = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
   }
   long long t_end = 0;  // scheduler: clock at the end of the previous item (profiling)
   for (;;) {
@@ -1053,8 +1068,7 @@ fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, con
         atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[12]), (unsigned long long)(clock64() - t_end));
         atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[13]), 1ull);
       }
-      nxt = decode_ticket(g, tk_next);
-      if (nxt.type != ITEM_DONE) tk_next = atomicAdd(reinterpret_cast<unsigned long long*>(g.ticket), 1ull);
+      cl.done = false;
     }
 #ifdef NSG_EXP_TRACE
     u64 tr0 = 0;
@@ -1063,15 +1077,15 @@ fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, con
     // every item function passes a __syncthreads() before the scheduler can overwrite m.type/m.w/m.idx
     if (type == ITEM_P) {
       if (idx < chunks_of(g, w)) {
-        item_partition(g, src, dst, keys, w, idx, *reinterpret_cast<SmemP*>(u), m);
+        item_partition(g, src, dst, keys, w, idx, *reinterpret_cast<SmemP*>(u), m, cl);
       } else {  // a chunk past the end of the last (short) window: count it done
         if (threadIdx.x == 0) red_release_add32(&g.pdone[w], 1u);
         __syncthreads();
       }
     } else if (type == ITEM_L) {
-      item_link(g, w, idx, *reinterpret_cast<SmemL*>(u), m);
+      item_link(g, w, idx, *reinterpret_cast<SmemL*>(u), m, cl);
     } else if (type == ITEM_S0 || type == ITEM_S1) {
-      item_side(g, w, (int)(type - ITEM_S0), idx, *reinterpret_cast<SmemS*>(u), m);
+      item_side(g, w, (int)(type - ITEM_S0), idx, *reinterpret_cast<SmemS*>(u), m, cl);
     } else if (type == ITEM_F) {
       item_finalize(g, w, m, out);
     } else {
@@ -1092,6 +1106,8 @@ fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, con
     // every item function passed a __syncthreads() after all threads read m.type/m.w/m.idx
     if (sched) {
       t_end = clock64();
+      cl.now(g);  // items that did not claim (F, short items)
+      const Item nxt = decode_ticket(g, cl.tk);
       prof_wait(g, nxt, wait_item_deps(g, nxt));
       m.type = nxt.type; m.idx = nxt.idx; m.w = nxt.w;
     }

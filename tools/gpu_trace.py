@@ -73,3 +73,8 @@ for w in list(range(0, nw, max(1, nw // 16))) + [nw - 1]:
         return (t0[m].min(), t1[m].max()) if m.any() else (float("nan"), float("nan"))
     p, l, s, f = rng(0), rng(1), rng(2), rng(4)
     print(f"  {w:6d} {p[0]:7.1f} {p[1]:6.1f} {l[0]:7.1f} {l[1]:6.1f} {s[0]:7.1f} {s[1]:6.1f} {f[1]:6.1f}")
+if "--last" in sys.argv:
+    for k, v in ((0, "P"), (1, "L"), (2, "S0"), (3, "S1")):
+        m = (win == nw - 1) & (typ == k)
+        o = np.argsort(t0[m])
+        print(f"  last window {v}: " + " ".join(f"{a:.0f}-{b:.0f}" for a, b in zip(t0[m][o], t1[m][o])))
