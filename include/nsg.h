@@ -114,6 +114,27 @@ nsg_status nsg_window_stats_timed(const uint32_t* src, const uint32_t* dst, cons
                                   uint64_t window, uint64_t* out, void* workspace, size_t workspace_bytes,
                                   void* stream, uint32_t flags, void* ev_before, void* ev_after);
 
+/* End-to-end call on HOST input, overlapping the host->device copy with the computation (PAPER.md
+ * line 173: the per-window statistics of Table 2, as nsg_window_stats_packed).
+ *   keys_host     host u64[n_packets] (packed as in nsg_window_stats_packed); must be page-locked
+ *                 (cudaHostAlloc / cudaHostRegister) for the copies to be asynchronous; 8 B aligned.
+ *   keys_dev      device u64[n_packets] staging buffer the library copies the input into.
+ *   out           device u64[nsg_num_windows][9] result; out_host: optional (NULL: skipped) page-locked
+ *                 host copy of it, written by a D2H copy on `stream` after the computation.
+ *   copy_stream   a second stream (cudaStream_t as void*, != stream) for the host->device copies.
+ *   chunk_windows windows per copy chunk (0: default 8; 8-16 measured best on the C2 batch).
+ * The keys are copied in chunks on copy_stream, each followed by a stream write of a per-chunk
+ * arrival flag in `workspace`; the persistent kernel is launched on `stream` at once and each of its
+ * partition items waits for its chunk's flag, so the computation proceeds under the copies.  Before
+ * the call returns, `stream` is made to wait for copy_stream's copies (keys_dev is complete once the
+ * call's work on `stream` is).  Asynchronous like the other entry points: host buffers must stay alive
+ * and unmodified until `stream` has completed the call.  Errors as nsg_window_stats_packed, plus
+ * NSG_ERR_INVALID_ARGUMENT for a NULL keys_host / keys_dev / out / copy_stream or copy_stream == stream,
+ * and NSG_ERR_CUDA if the driver's stream-memory-operation entry point is unavailable. */
+nsg_status nsg_window_stats_from_host(const uint64_t* keys_host, uint64_t n_packets, uint64_t window,
+                                      uint64_t* keys_dev, uint64_t* out, uint64_t* out_host, void* workspace,
+                                      size_t workspace_bytes, void* stream, void* copy_stream, uint32_t chunk_windows);
+
 /* Diagnostics of the last call that used `workspace` (device memory; read it after the stream has
  * completed the call): byte offset inside the workspace of a u32[4] =
  *   {windows the fast path handed to the L2 path because an SMEM table would overflow,

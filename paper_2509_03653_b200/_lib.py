@@ -25,6 +25,7 @@ EXPORTS = (
     "nsg_window_stats_packed",
     "nsg_window_stats_ex",
     "nsg_window_stats_timed",
+    "nsg_window_stats_from_host",
     "nsg_diag_offset",
     "nsg_last_launches",
     "nsg_status_string",
@@ -79,6 +80,8 @@ def load() -> ctypes.CDLL:
     lib.nsg_window_stats_ex.argtypes = [vp, vp, vp, u64, u64, vp, vp, sz, vp, u32]
     lib.nsg_window_stats_timed.restype = ctypes.c_int
     lib.nsg_window_stats_timed.argtypes = [vp, vp, vp, u64, u64, vp, vp, sz, vp, u32, vp, vp]
+    lib.nsg_window_stats_from_host.restype = ctypes.c_int
+    lib.nsg_window_stats_from_host.argtypes = [vp, u64, u64, vp, vp, vp, vp, sz, vp, vp, u32]
     lib.nsg_diag_offset.restype = sz
     lib.nsg_diag_offset.argtypes = []
     lib.nsg_last_launches.restype = ctypes.c_uint

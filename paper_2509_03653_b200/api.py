@@ -165,27 +165,59 @@ def window_stats_packed(keys: torch.Tensor, window: int = DEFAULT_WINDOW, *, out
                    events=kernel_events)
 
 
+_copy_streams = {}
+
+
+def _copy_stream(device: torch.device):
+    cs = _copy_streams.get(device.index)
+    if cs is None:
+        cs = _copy_streams[device.index] = torch.cuda.Stream(device)
+    return cs
+
+
 def window_stats_from_host(keys_host: torch.Tensor, window: int = DEFAULT_WINDOW, *, device=None,
                            keys_dev: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None,
                            out_host: Optional[torch.Tensor] = None, workspace: Optional[Workspace] = None,
-                           stream=None) -> torch.Tensor:
-    """End-to-end call on HOST packed keys: H2D copy, the device computation, D2H copy of the result.
+                           stream=None, copy_stream=None, chunk_windows: int = 8,
+                           synchronize: bool = True) -> torch.Tensor:
+    """End-to-end call on HOST packed keys (nsg_window_stats_from_host): chunked H2D copies on a copy
+    stream overlapped with the device computation, then the D2H copy of the result.
 
-    `keys_host` should be pinned for an asynchronous copy.  Returns the CPU int64 [n_windows, 9] result
-    (synchronised).
+    `keys_host` must be a pinned 1-D int64/uint64 CPU tensor.  Returns the pinned CPU int64
+    [n_windows, 9] result (complete on return when `synchronize`, else once `stream` reaches it).
     """
-    if keys_host.is_cuda or keys_host.dtype not in _U64_TYPES or keys_host.dim() != 1:
-        raise ValueError("keys_host must be a 1-D host int64/uint64 tensor")
+    if (not isinstance(keys_host, torch.Tensor) or keys_host.is_cuda or keys_host.dtype not in _U64_TYPES
+            or keys_host.dim() != 1 or not keys_host.is_contiguous()):
+        raise ValueError("keys_host must be a contiguous 1-D host int64/uint64 tensor")
+    if keys_host.numel() and not keys_host.is_pinned():
+        raise ValueError("keys_host must be pinned (torch.Tensor.pin_memory())")
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    window = int(window)
+    if window < 1 or window > MAX_WINDOW:
+        raise ValueError(f"window must be in [1, 2^31], got {window}")
     n = keys_host.numel()
+    nw = num_windows(n, window)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    cs = copy_stream if copy_stream is not None else _copy_stream(dev)
     if keys_dev is None:
         keys_dev = torch.empty(n, dtype=keys_host.dtype, device=dev)
-    with torch.cuda.stream(s):
-        keys_dev[:n].copy_(keys_host, non_blocking=True)
-        res = window_stats_packed(keys_dev[:n], window, out=out, workspace=workspace, stream=s)
-        if out_host is None:
-            out_host = torch.empty(res.shape, dtype=torch.int64, pin_memory=True)
-        out_host.copy_(res, non_blocking=True)
-    s.synchronize()
-    return out_host
+    elif not keys_dev.is_cuda or keys_dev.dtype not in _U64_TYPES or keys_dev.numel() < n or not keys_dev.is_contiguous():
+        raise ValueError("keys_dev must be a contiguous CUDA int64/uint64 tensor with >= n elements")
+    if out is None:
+        out = torch.empty((nw, NUM_STATS), dtype=torch.int64, device=dev)
+    elif out.dtype not in _U64_TYPES or not out.is_contiguous() or out.numel() < nw * NUM_STATS or not out.is_cuda:
+        raise ValueError("out must be a contiguous CUDA int64/uint64 tensor with >= n_windows*9 elements")
+    if out_host is None:
+        out_host = torch.empty((nw, NUM_STATS), dtype=torch.int64, pin_memory=True)
+    elif out_host.is_cuda or not out_host.is_pinned() or out_host.numel() < nw * NUM_STATS or not out_host.is_contiguous():
+        raise ValueError("out_host must be a pinned contiguous CPU tensor with >= n_windows*9 elements")
+    if n:
+        ws = _workspace(n, window, dev, workspace)
+        rc = _lib.nsg_window_stats_from_host(
+            keys_host.data_ptr(), n, window, keys_dev.data_ptr(), out.data_ptr(), out_host.data_ptr(), ws.ptr,
+            ws.nbytes, ctypes.c_void_p(s.cuda_stream), ctypes.c_void_p(cs.cuda_stream), int(chunk_windows))
+        if rc != 0:
+            raise NsgError(rc, "nsg_window_stats_from_host")
+    if synchronize:
+        s.synchronize()
+    return out_host[:nw] if out_host.dim() == 2 else out_host

@@ -13,6 +13,7 @@
 //                    with global-memory hash tables.
 // This file holds the C ABI: argument checks, workspace layout, launches.
 #include <algorithm>
+#include <cuda.h>  // driver types for cuStreamWriteValue32 (resolved at run time: no libcuda link)
 #include "nsg.h"
 #include "nsg_common.cuh"
 #include "nsg_fast.cuh"
@@ -57,8 +58,8 @@ static Layout make_layout(u64 n, u64 W, int sms) {
   L.nw = (n + W - 1) / W;
   L.fast = W <= FAST_MAX_WINDOW;
   size_t o = CTRL_BYTES;
-  L.o_pw = o;
-  o = align256(o + 5 * sizeof(u32) * L.nw);
+  L.o_pw = o;  // per window: pdone, ldone, sdone, fin, ovf, arrived (streamed input)
+  o = align256(o + 6 * sizeof(u32) * L.nw);
   L.memset_bytes = o;
   if (L.fast) {
     const u64 want = (W + BUCKET_KEYS - 1) / BUCKET_KEYS;
@@ -141,8 +142,33 @@ static int sms_for_layout() {
   return sms;
 }
 
+// Streamed input (nsg_window_stats_from_host): the host keys are copied to `keys` (device) in chunks
+// of chunk_w windows on copy_stream, each chunk followed by a stream write of its arrival flag, while
+// the kernel already runs on the main stream; its partition items wait for their chunk's flag.
+struct StreamIn {
+  const u64* host;
+  cudaStream_t cs;
+  u32 chunk_w;
+};
+typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WriteValue32Fn write_value32() {
+  static WriteValue32Fn fn = nullptr;
+  static bool tried = false;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WriteValue32Fn>(p);
+  }
+  return fn;
+}
+
 static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u64 W, u64* out, void* ws,
-                      size_t ws_bytes, void* stream, u32 flags, void* ev_before = nullptr, void* ev_after = nullptr) {
+                      size_t ws_bytes, void* stream, u32 flags, void* ev_before = nullptr, void* ev_after = nullptr,
+                      const StreamIn* sin = nullptr) {
   g_last_launches = 0;
   if (W == 0 || W > NSG_MAX_WINDOW) return NSG_ERR_INVALID_ARGUMENT;
   if (n == 0) return NSG_OK;
@@ -161,6 +187,34 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   unsigned char* base = reinterpret_cast<unsigned char*>(ws);
   if (cudaMemsetAsync(base, 0, L.memset_bytes, s) != cudaSuccess) return NSG_ERR_CUDA;
+  u32* arrived = reinterpret_cast<u32*>(base + L.o_pw) + 5 * L.nw;
+  cudaEvent_t ev_copied = nullptr;
+  if (sin) {  // chunked H2D on the copy stream, after the workspace reset (which clears the flags)
+    WriteValue32Fn wv = write_value32();
+    if (!wv) return NSG_ERR_CUDA;
+    cudaEvent_t ev_reset = nullptr;
+    if (cudaEventCreateWithFlags(&ev_reset, cudaEventDisableTiming) != cudaSuccess) return NSG_ERR_CUDA;
+    if (cudaEventCreateWithFlags(&ev_copied, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventDestroy(ev_reset);
+      return NSG_ERR_CUDA;
+    }
+    bool okc = cudaEventRecord(ev_reset, s) == cudaSuccess && cudaStreamWaitEvent(sin->cs, ev_reset, 0) == cudaSuccess;
+    const u64 per = (u64)sin->chunk_w * W;
+    u64* kd = const_cast<u64*>(keys);
+    for (u64 c = 0, p0 = 0; okc && p0 < n; ++c, p0 += per) {
+      const u64 len = per < n - p0 ? per : n - p0;
+      okc = cudaMemcpyAsync(kd + p0, sin->host + p0, len * sizeof(u64), cudaMemcpyHostToDevice, sin->cs) == cudaSuccess &&
+            wv(sin->cs, reinterpret_cast<CUdeviceptr>(arrived + c), 1u, 0) == CUDA_SUCCESS;
+    }
+    okc = okc && cudaEventRecord(ev_copied, sin->cs) == cudaSuccess;
+    cudaEventDestroy(ev_reset);
+    if (!okc) { cudaEventDestroy(ev_copied); return NSG_ERR_CUDA; }
+  }
+  // every exit below joins the copy stream back into `s` (the input buffer is complete after the call)
+  struct Join {
+    cudaEvent_t ev; cudaStream_t s;
+    ~Join() { if (ev) { cudaStreamWaitEvent(s, ev, 0); cudaEventDestroy(ev); } }
+  } join{ev_copied, s};
 
   u32* pw = reinterpret_cast<u32*>(base + L.o_pw);
   GGeo gg;
@@ -183,6 +237,8 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
     g.diag = reinterpret_cast<u32*>(base + DIAG_OFFSET);
     g.prof = reinterpret_cast<u64*>(base + PROF_OFFSET);
     g.pdone = pw; g.ldone = pw + L.nw; g.sdone = pw + 2 * L.nw; g.fin = pw + 3 * L.nw; g.ovf = pw + 4 * L.nw;
+    g.arrived = sin ? arrived : nullptr;
+    g.chunk_w = sin ? sin->chunk_w : 1u;
     g.kscr = reinterpret_cast<u64*>(base + L.o_kscr);
     g.koff = reinterpret_cast<u32*>(base + L.o_koff);
     g.rscr = reinterpret_cast<u64*>(base + L.o_rscr);
@@ -235,6 +291,7 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
     g_last_launches++;
     if (cudaGetLastError() != cudaSuccess) return NSG_ERR_CUDA;
     if (ev_after && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_after), s) != cudaSuccess) return NSG_ERR_CUDA;
+    if (ev_copied && cudaStreamWaitEvent(s, ev_copied, 0) != cudaSuccess) return NSG_ERR_CUDA;
     if (!(flags & NSG_FLAG_NO_FALLBACK_CHECK)) {
       gg.only_overflowed = 1;
       global_kernel<<<L.G, GT, 0, s>>>(gg, src, dst, keys, out);
@@ -242,6 +299,7 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
       if (cudaGetLastError() != cudaSuccess) return NSG_ERR_CUDA;
     }
   } else {
+    if (ev_copied && cudaStreamWaitEvent(s, ev_copied, 0) != cudaSuccess) return NSG_ERR_CUDA;
     gg.only_overflowed = 0;
     if (ev_before && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_before), s) != cudaSuccess) return NSG_ERR_CUDA;
     global_kernel<<<L.G, GT, 0, s>>>(gg, src, dst, keys, out);
@@ -295,6 +353,27 @@ nsg_status nsg_window_stats_timed(const uint32_t* src, const uint32_t* dst, cons
                                   uint32_t flags, void* ev_before, void* ev_after) {
   return nsg::run(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_packets, window,
                   reinterpret_cast<nsg::u64*>(out), workspace, workspace_bytes, stream, flags, ev_before, ev_after);
+}
+
+nsg_status nsg_window_stats_from_host(const uint64_t* keys_host, uint64_t n_packets, uint64_t window,
+                                      uint64_t* keys_dev, uint64_t* out, uint64_t* out_host, void* workspace,
+                                      size_t workspace_bytes, void* stream, void* copy_stream, uint32_t chunk_windows) {
+  nsg::g_last_launches = 0;
+  if (window == 0 || window > NSG_MAX_WINDOW) return NSG_ERR_INVALID_ARGUMENT;
+  if (n_packets == 0) return NSG_OK;
+  if (!keys_host || !keys_dev || !out || !copy_stream || copy_stream == stream) return NSG_ERR_INVALID_ARGUMENT;
+  if ((reinterpret_cast<uintptr_t>(keys_host) & 7) || (reinterpret_cast<uintptr_t>(out_host) & 7))
+    return NSG_ERR_INVALID_ARGUMENT;
+  const nsg::StreamIn sin{reinterpret_cast<const nsg::u64*>(keys_host), reinterpret_cast<cudaStream_t>(copy_stream),
+                          chunk_windows ? chunk_windows : 8u};
+  const nsg_status st = nsg::run(nullptr, nullptr, reinterpret_cast<const nsg::u64*>(keys_dev), n_packets, window,
+                                 reinterpret_cast<nsg::u64*>(out), workspace, workspace_bytes, stream, 0, nullptr,
+                                 nullptr, &sin);
+  if (st != NSG_OK || !out_host) return st;
+  const size_t bytes = (size_t)nsg_num_windows(n_packets, window) * NSG_NUM_STATS * sizeof(uint64_t);
+  if (cudaMemcpyAsync(out_host, out, bytes, cudaMemcpyDeviceToHost, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
+    return NSG_ERR_CUDA;
+  return NSG_OK;
 }
 
 size_t nsg_diag_offset(void) { return nsg::DIAG_OFFSET; }

@@ -34,6 +34,12 @@ __host__ __device__ __forceinline__ u32 hash32(u32 x) {
 __device__ __forceinline__ u64 ldcg64(const u64* p) { return __ldcg(reinterpret_cast<const unsigned long long*>(p)); }
 __device__ __forceinline__ u32 ldcg32(const u32* p) { return __ldcg(reinterpret_cast<const unsigned int*>(p)); }
 
+// acquire at system scope: a flag written by a stream memory operation (cuStreamWriteValue32)
+__device__ __forceinline__ u32 ld_acquire_sys32(const u32* p) {
+  u32 v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ u32 ld_acquire32(const u32* p) {
   u32 v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

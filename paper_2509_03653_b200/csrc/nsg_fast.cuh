@@ -98,6 +98,8 @@ struct Geo {
   u32* diag;
   u64* prof;  // [3 item types][4] = {count, cycles, wait cycles, -} when NSG_FLAG_PROFILE
   u32 *pdone, *ldone, *sdone, *fin, *ovf;
+  const u32* arrived;  // streamed input (nsg_window_stats_from_host): arrived[w / chunk_w] != 0 once the
+  u32 chunk_w;         // chunk holding window w has been copied to the device; NULL: input resident
   u64* kscr;  // [R][cp*CH]      keys, chunk-major, each chunk sorted by link bucket
   u32* koff;  // [R][cp][B+1]    bucket offsets inside each chunk
   u64* rscr;  // [R][B][RCAP]    link records of each link bucket, sorted by (side, side bucket)
@@ -363,6 +365,17 @@ __device__ void item_partition(const Geo& g, const u32* __restrict__ src, const 
   PhaseTimer pt;
   const long long tstart = clock64();
   long long waited = 0;
+  if (g.arrived) {  // streamed input: wait until the copy engine has delivered this window's chunk
+    if (t == 0) {
+      const u32* f = &g.arrived[w / g.chunk_w];
+      if (ld_acquire_sys32(f) == 0) {
+        const long long t0 = clock64();
+        while (ld_acquire_sys32(f) == 0) __nanosleep(128);
+        waited += clock64() - t0;
+      }
+    }
+    __syncthreads();
+  }
   u32 dep = 1;
   if (t == 0 && w >= g.R) dep = ld_acquire32(&g.fin[w - g.R]);  // the slot's previous window is final
   for (int i = t; i <= (int)g.B; i += FT) s.hist[i] = 0;

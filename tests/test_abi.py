@@ -89,6 +89,28 @@ def test_argument_validation_without_gpu():
     assert lib.nsg_window_stats_packed(12, 10, 4, 8, 256, 1 << 20, None) == 1
 
 
+def test_from_host_argument_validation_without_gpu():
+    lib = ctypes.CDLL(LIB)
+    f = lib.nsg_window_stats_from_host
+    f.restype = ctypes.c_int
+    vp, u64 = ctypes.c_void_p, ctypes.c_uint64
+    f.argtypes = [vp, u64, u64, vp, vp, vp, vp, ctypes.c_size_t, vp, vp, ctypes.c_uint32]
+    # n == 0: OK, nothing launched or copied
+    assert f(None, 0, 1 << 17, None, None, None, None, 0, None, None, 0) == 0
+    # window 0 / too large
+    assert f(8, 10, 0, 8, 8, 8, 256, 1 << 20, None, 16, 0) == 1
+    assert f(8, 10, (1 << 31) + 1, 8, 8, 8, 256, 1 << 20, None, 16, 0) == 1
+    # NULL host keys / staging buffer / out / copy stream; copy stream == stream
+    assert f(None, 10, 4, 8, 8, 8, 256, 1 << 20, None, 16, 0) == 1
+    assert f(8, 10, 4, None, 8, 8, 256, 1 << 20, None, 16, 0) == 1
+    assert f(8, 10, 4, 8, None, 8, 256, 1 << 20, None, 16, 0) == 1
+    assert f(8, 10, 4, 8, 8, 8, 256, 1 << 20, None, None, 0) == 1
+    assert f(8, 10, 4, 8, 8, 8, 256, 1 << 20, 16, 16, 0) == 1
+    # misaligned host keys / host output
+    assert f(12, 10, 4, 8, 8, 8, 256, 1 << 20, None, 16, 0) == 1
+    assert f(8, 10, 4, 8, 8, 12, 256, 1 << 20, None, 16, 0) == 1
+
+
 def test_status_strings():
     lib = ctypes.CDLL(LIB)
     lib.nsg_status_string.restype = ctypes.c_char_p

@@ -149,6 +149,48 @@ def test_repeat_calls_reuse_workspace(nsg, cuda_device):
     assert nsg.last_launches() >= 1
 
 
+@pytest.mark.parametrize("n,window,chunk", [(3 * W + 777, W, 1), (8 * W, W, 3), (5 * W, W, 0), (100003, 4096, 5),
+                                             (7 * W + 1, 3 * W, 2)])
+def test_from_host_streamed(nsg, cuda_device, n, window, chunk):
+    """nsg_window_stats_from_host: chunked H2D on a copy stream overlapped with the kernel (partition
+    items wait on per-chunk arrival flags); parity with the oracle, and the staging buffer holds the
+    input afterwards.  Ragged: partial last window, chunk counts that do not divide the windows."""
+    c = CONFIGS["C2"]
+    keys = gen.generate_host(c.dist, 11, 0, n, packed=True)
+    host = torch.from_numpy(keys.view(np.int64)).pin_memory()
+    kd = torch.empty(n, dtype=torch.int64, device=cuda_device)
+    got = nsg.window_stats_from_host(host, window, device=cuda_device, keys_dev=kd, chunk_windows=chunk)
+    assert_parity(got.numpy().view(np.uint64), oracle.window_stats_sort(keys=keys, window=window))
+    assert torch.equal(kd.cpu(), host)
+
+
+def test_from_host_repeated_and_forced_l2(nsg, cuda_device):
+    c = CONFIGS["C3"]
+    keys = gen.generate_host(c.dist, c.seed, 0, 6 * W + 5, packed=True)
+    want = oracle.window_stats_sort(keys=keys, window=W)
+    host = torch.from_numpy(keys.view(np.int64)).pin_memory()
+    kd = torch.empty(host.numel(), dtype=torch.int64, device=cuda_device)
+    ws = nsg.Workspace(host.numel(), W)
+    for _ in range(3):
+        assert_parity(nsg.window_stats_from_host(host, W, keys_dev=kd, workspace=ws).numpy().view(np.uint64), want)
+    # a window above the fast path's limit goes to the L2 path after the copies
+    keys2 = gen.generate_host(c.dist, 2, 0, (1 << 21) + 3, packed=True)
+    host2 = torch.from_numpy(keys2.view(np.int64)).pin_memory()
+    got = nsg.window_stats_from_host(host2, 1 << 21).numpy().view(np.uint64)
+    assert_parity(got, oracle.window_stats_sort(keys=keys2, window=1 << 21))
+
+
+def test_from_host_rejects_bad_arguments(nsg, cuda_device):
+    host = torch.zeros(1000, dtype=torch.int64)
+    with pytest.raises(ValueError):
+        nsg.window_stats_from_host(host, W)  # not pinned
+    hp = host.pin_memory()
+    s = torch.cuda.current_stream(cuda_device)
+    with pytest.raises(nsg.NsgError):
+        nsg.window_stats_from_host(hp, W, stream=s, copy_stream=s)
+    assert tuple(nsg.window_stats_from_host(torch.zeros(0, dtype=torch.int64).pin_memory(), W).shape) == (0, 9)
+
+
 def test_device_generator_matches_host(nsg, cuda_device):
     for dist in (gen.Dist("uniform"), gen.Dist("zipf", 1.1, 1 << 20), gen.Dist("heavy")):
         kd = torch.empty(300000, dtype=torch.int64, device=cuda_device)
