@@ -10,6 +10,10 @@ Three procedures, each citing PAPER.md (= /root/reference/PAPER.md, arXiv 2509.0
 * ``window_stats_map``  — O1, the literal definition over ``std::map`` (oracle.cpp).
 * ``window_stats_sort`` — O2, the same definition via ``std::sort`` + run-length scans,
   thread-parallel over windows (oracle.cpp).
+* ``window_distributions`` — O1d, the vector-valued rows of Table 2 (link packets :182, packets
+  from source :185, source fan-out :187, their destination mirrors :173) and the four globally
+  unique IP set counts (:209) per window, from the same ``std::map`` definition (oracle.cpp);
+  ``window_distributions_dense`` is its dense O0 counterpart (dense.py).
 * ``window_stats_dense`` — O0, the "Matrix notation" column evaluated literally on a dense
   matrix after relabelling the (few) addresses of a tiny window (dense.py).
 
@@ -27,7 +31,7 @@ import threading
 
 import numpy as np
 
-from .dense import window_stats_dense  # noqa: F401
+from .dense import window_distributions_dense, window_stats_dense  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.cpp")
@@ -58,6 +62,10 @@ def _load():
                 f.restype = ctypes.c_int
                 f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                               ctypes.c_void_p, ctypes.c_int]
+            f = lib.nsg_oracle_window_distributions
+            f.restype = ctypes.c_int
+            f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64] + \
+                [ctypes.c_void_p] * 10 + [ctypes.c_int]
             lib.nsg_oracle_hardware_threads.restype = ctypes.c_uint
             _lib = lib
     return _lib
@@ -110,3 +118,52 @@ def window_stats_map(src=None, dst=None, window: int = 1 << 17, *, keys=None, th
 def window_stats_sort(src=None, dst=None, window: int = 1 << 17, *, keys=None, threads: int = 0) -> np.ndarray:
     """O2: std::sort + run-length scans, a thread per window group.  Returns uint64 [n_windows, 9]."""
     return _run("nsg_oracle_window_stats_sort", src, dst, keys, window, threads)
+
+
+IP_SETS = ("union", "src_only", "dst_only", "both")
+
+
+def window_distributions(src=None, dst=None, window: int = 1 << 17, *, keys=None, threads: int = 0) -> dict:
+    """O1d: per window, the nonzeros of A_t and the row/column sums and nnz, each in ascending key
+    order, plus the four IP set counts.
+
+    Returns a dict of numpy arrays:
+      link_key u64[n], link_packets u64[n]         window w's links at [w*window, w*window + counts[w,0])
+      src_node u32[n], src_packets u64[n], src_fan u64[n]     (counts[w,1] entries per window)
+      dst_node u32[n], dst_packets u64[n], dst_fan u64[n]     (counts[w,2] entries per window)
+      counts u64[nw, 3] = (links, sources, destinations); ip_sets u64[nw, 4] = IP_SETS order.
+    """
+    s, d = _split(src, dst, keys)
+    if s.shape != d.shape:
+        raise ValueError("src and dst must have the same length")
+    n = int(s.shape[0])
+    if window < 1:
+        raise ValueError("window must be >= 1")
+    nw = 0 if n == 0 else (n + window - 1) // window
+    r = {
+        "link_key": np.zeros(n, np.uint64), "link_packets": np.zeros(n, np.uint64),
+        "src_node": np.zeros(n, np.uint32), "src_packets": np.zeros(n, np.uint64), "src_fan": np.zeros(n, np.uint64),
+        "dst_node": np.zeros(n, np.uint32), "dst_packets": np.zeros(n, np.uint64), "dst_fan": np.zeros(n, np.uint64),
+        "counts": np.zeros((nw, 3), np.uint64), "ip_sets": np.zeros((nw, 4), np.uint64),
+    }
+    if n:
+        order = ("link_key", "link_packets", "src_node", "src_packets", "src_fan", "dst_node", "dst_packets",
+                 "dst_fan", "counts", "ip_sets")
+        rc = _load().nsg_oracle_window_distributions(s.ctypes.data, d.ctypes.data, n, int(window),
+                                                     *[r[k].ctypes.data for k in order], int(threads))
+        if rc != 0:
+            raise ValueError(f"nsg_oracle_window_distributions returned {rc}")
+    return r
+
+
+def window_slices(r: dict, window: int, w: int) -> dict:
+    """The entries of window w of a distributions dict (as returned by window_distributions)."""
+    b = w * window
+    nl, ns, nd = (int(x) for x in r["counts"][w])
+    out = {"link_key": r["link_key"][b:b + nl], "link_packets": r["link_packets"][b:b + nl]}
+    for k in ("src_node", "src_packets", "src_fan"):
+        out[k] = r[k][b:b + ns]
+    for k in ("dst_node", "dst_packets", "dst_fan"):
+        out[k] = r[k][b:b + nd]
+    out["ip_sets"] = r["ip_sets"][w]
+    return out

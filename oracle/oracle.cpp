@@ -26,7 +26,7 @@
 //   8 max destination fan-in   mirror of 5, max(1^T|A_t|_0)
 // Any max over an empty set is 0 (reading R7).
 //
-// Two procedures:
+// Procedures:
 //   O1 (nsg_oracle_window_stats_map): the literal definition with std::map, step by step
 //      in Table 2's order: build A_t as a map (i,j) -> count ("Link packets from i
 //      to j"), then the whole-matrix rows, then row sums / row nnz and the
@@ -34,6 +34,9 @@
 //   O2 (nsg_oracle_window_stats_sort): the same definition reached through a library sort
 //      (std::sort) and run-length scans; a thread pool over windows.  Windows are
 //      independent, so the thread count cannot change any result.
+//   O1d (nsg_oracle_window_distributions): the vector-valued rows of Table 2 (link packets,
+//      row sums / nnz and their column mirrors) and the four globally-unique-IP set counts, from
+//      the same std::map definition.
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
@@ -136,6 +139,60 @@ void window_sort(const uint32_t* src, const uint32_t* dst, uint64_t len, uint64_
   if (d.total != s.total || d.distinct_pairs != s.distinct_pairs || d.max_pair != s.max_pair) out[0] = ~0ull;
 }
 
+// ---- O1d: the vector-valued rows of Table 2 and the globally unique IPs ----
+// For window w, literally from the definition, in the same std::map form as O1:
+//   links       the nonzeros of A_t: (key = i<<32 | j, A_t(i,j))    P:182 "Link packets from i to j"
+//   sources     per nonzero row i: (i, (A_t 1)_i, (|A_t|_0 1)_i)     P:185 "Packets from source i",
+//                                                                    P:187 "Source fan-out from i"
+//   destinations the column mirrors (1^T A_t)_j, (1^T |A_t|_0)_j     P:173 "replace src and dst"
+//   ip sets     {|S u D|, |S \ D|, |D \ S|, |S n D|} with S = sources, D = destinations of the window:
+//               P:209 "Globally unique IP addresses ... unique() ... on each column and subsequently
+//               removing common values across the two unique sets"; all four counts (SPEC S:239-245,
+//               S:272), reading R13.
+// Every vector is written in ascending key order (std::map order) at offset w*window of
+// its array; cnt[w] = {links, sources, destinations}.
+struct DistOut {
+  uint64_t* link_key; uint64_t* link_packets;
+  uint32_t* src_node; uint64_t* src_packets; uint64_t* src_fan;
+  uint32_t* dst_node; uint64_t* dst_packets; uint64_t* dst_fan;
+  uint64_t* cnt;      // [nw][3]
+  uint64_t* ip_sets;  // [nw][4]
+};
+
+void window_dist(const uint32_t* src, const uint32_t* dst, uint64_t len, uint64_t w, uint64_t window,
+                 const DistOut& o) {
+  std::map<std::pair<uint32_t, uint32_t>, uint64_t> A;             // A_t(i,j)
+  for (uint64_t p = 0; p < len; ++p) A[{src[p], dst[p]}] += 1;
+  std::map<uint32_t, std::pair<uint64_t, uint64_t>> row, col;       // (sum, nnz) per row / column
+  for (const auto& e : A) {
+    row[e.first.first].first += e.second;   // (A_t 1)_i
+    row[e.first.first].second += 1;         // (|A_t|_0 1)_i
+    col[e.first.second].first += e.second;  // mirror
+    col[e.first.second].second += 1;
+  }
+  const uint64_t b = w * window;
+  uint64_t k = 0;
+  for (const auto& e : A) {
+    o.link_key[b + k] = (uint64_t(e.first.first) << 32) | e.first.second;
+    o.link_packets[b + k] = e.second;
+    ++k;
+  }
+  k = 0;
+  for (const auto& e : row) { o.src_node[b + k] = e.first; o.src_packets[b + k] = e.second.first; o.src_fan[b + k] = e.second.second; ++k; }
+  k = 0;
+  for (const auto& e : col) { o.dst_node[b + k] = e.first; o.dst_packets[b + k] = e.second.first; o.dst_fan[b + k] = e.second.second; ++k; }
+  o.cnt[w * 3 + 0] = A.size();
+  o.cnt[w * 3 + 1] = row.size();
+  o.cnt[w * 3 + 2] = col.size();
+  // The two unique sets and their common values.
+  uint64_t both = 0;
+  for (const auto& e : row) both += col.count(e.first);
+  o.ip_sets[w * 4 + 0] = row.size() + col.size() - both;  // |S u D|
+  o.ip_sets[w * 4 + 1] = row.size() - both;               // |S \ D|
+  o.ip_sets[w * 4 + 2] = col.size() - both;               // |D \ S|
+  o.ip_sets[w * 4 + 3] = both;                            // |S n D|
+}
+
 using WindowFn = void (*)(const uint32_t*, const uint32_t*, uint64_t, uint64_t*);
 
 int run_windows(WindowFn fn, const uint32_t* src, const uint32_t* dst, uint64_t n, uint64_t window,
@@ -176,6 +233,35 @@ int nsg_oracle_window_stats_map(const uint32_t* src, const uint32_t* dst, uint64
 int nsg_oracle_window_stats_sort(const uint32_t* src, const uint32_t* dst, uint64_t n, uint64_t window,
                                  uint64_t* out, int n_threads) {
   return run_windows(window_sort, src, dst, n, window, out, n_threads);
+}
+
+// Returns 0 on success, 1 on invalid arguments.  Every vector array is host [n] (window w's entries at
+// [w*window, w*window + cnt)); cnt is host [nw][3], ip_sets host [nw][4].
+int nsg_oracle_window_distributions(const uint32_t* src, const uint32_t* dst, uint64_t n, uint64_t window,
+                                    uint64_t* link_key, uint64_t* link_packets, uint32_t* src_node,
+                                    uint64_t* src_packets, uint64_t* src_fan, uint32_t* dst_node,
+                                    uint64_t* dst_packets, uint64_t* dst_fan, uint64_t* cnt, uint64_t* ip_sets,
+                                    int n_threads) {
+  if (window == 0) return 1;
+  if (n == 0) return 0;
+  if (!src || !dst || !link_key || !link_packets || !src_node || !src_packets || !src_fan || !dst_node ||
+      !dst_packets || !dst_fan || !cnt || !ip_sets)
+    return 1;
+  const DistOut o{link_key, link_packets, src_node, src_packets, src_fan, dst_node, dst_packets, dst_fan, cnt, ip_sets};
+  const uint64_t nw = num_windows(n, window);
+  unsigned T = n_threads > 0 ? unsigned(n_threads) : std::max(1u, std::thread::hardware_concurrency());
+  if (T > nw) T = unsigned(nw);
+  auto worker = [&](unsigned t) {
+    for (uint64_t w = t; w < nw; w += T) {
+      const uint64_t b = w * window;
+      window_dist(src + b, dst + b, std::min(window, n - b), w, window, o);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < T; ++t) pool.emplace_back(worker, t);
+  worker(0);
+  for (auto& th : pool) th.join();
+  return 0;
 }
 
 unsigned nsg_oracle_hardware_threads(void) { return std::max(1u, std::thread::hardware_concurrency()); }
