@@ -135,6 +135,40 @@ nsg_status nsg_window_stats_from_host(const uint64_t* keys_host, uint64_t n_pack
                                       uint64_t* keys_dev, uint64_t* out, uint64_t* out_host, void* workspace,
                                       size_t workspace_bytes, void* stream, void* copy_stream, uint32_t chunk_windows);
 
+/* Optional per-window vector outputs of nsg_window_vectors.
+ *   links        the nonzeros of A_t: key (src<<32 | dst) and A_t(src,dst)
+ *                ("Link packets from i to j")
+ *   sources      per source i with a nonzero row: i, (A_t 1)_i (packets from source i)
+ *                and (|A_t|_0 1)_i (source fan-out from i)
+ *   destinations the column mirrors (1^T A_t)_j and (1^T |A_t|_0)_j
+ *   ip_sets      [n_windows][4] u64: |S u D|, |S \ D|, |D \ S|, |S n D| with S / D the window's source /
+ *                destination address sets ("Globally unique IP addresses"; R13)
+ * Every vector array is device memory with n_packets elements: window w's entries are at
+ * [w*window, w*window + count), count = out[w][NSG_UNIQUE_LINKS] (links), out[w][NSG_UNIQUE_SOURCES]
+ * (sources) or out[w][NSG_UNIQUE_DESTINATIONS] (destinations); elements past count are unspecified.
+ * The ORDER of the entries inside a window is unspecified (hash order; it may differ between runs).
+ * A group is requested by non-NULL pointers: link_key and link_packets together; src_node,
+ * src_packets and src_fanout together; dst_* together; ip_sets alone.  Alignment: 8 B for link_key and
+ * ip_sets, 4 B for the rest; a half-specified group or a misaligned array is NSG_ERR_INVALID_ARGUMENT. */
+typedef struct {
+  uint64_t* link_key;
+  uint32_t* link_packets;
+  uint32_t* src_node;
+  uint32_t* src_packets;
+  uint32_t* src_fanout;
+  uint32_t* dst_node;
+  uint32_t* dst_packets;
+  uint32_t* dst_fanin;
+  uint64_t* ip_sets;
+} nsg_vectors;
+
+/* nsg_window_stats_ex plus the vector outputs requested in `*vectors` (not NULL; every member may be
+ * NULL).  out[][9] is written as by nsg_window_stats_ex.  Same conventions (asynchronous on `stream`,
+ * caller-owned buffers, same workspace size); the arrays of *vectors are read when the call is made. */
+nsg_status nsg_window_vectors(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
+                              uint64_t window, uint64_t* out, const nsg_vectors* vectors, void* workspace,
+                              size_t workspace_bytes, void* stream, uint32_t flags);
+
 /* Diagnostics of the last call that used `workspace` (device memory; read it after the stream has
  * completed the call): byte offset inside the workspace of a u32[4] =
  *   {windows the fast path handed to the L2 path because an SMEM table would overflow,

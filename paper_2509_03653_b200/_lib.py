@@ -26,6 +26,7 @@ EXPORTS = (
     "nsg_window_stats_ex",
     "nsg_window_stats_timed",
     "nsg_window_stats_from_host",
+    "nsg_window_vectors",
     "nsg_diag_offset",
     "nsg_last_launches",
     "nsg_status_string",
@@ -55,6 +56,13 @@ def build_libnsg(force: bool = False, verbose: bool = False) -> str:
     return LIB_PATH
 
 
+class NsgVectors(ctypes.Structure):
+    """struct nsg_vectors (include/nsg.h): device pointers, NULL = not requested."""
+    _fields_ = [(name, ctypes.c_void_p) for name in (
+        "link_key", "link_packets", "src_node", "src_packets", "src_fanout", "dst_node", "dst_packets", "dst_fanin",
+        "ip_sets")]
+
+
 class NsgError(RuntimeError):
     def __init__(self, status: int, what: str = ""):
         super().__init__(f"{what}: {STATUS.get(status, status)}")
@@ -82,6 +90,8 @@ def load() -> ctypes.CDLL:
     lib.nsg_window_stats_timed.argtypes = [vp, vp, vp, u64, u64, vp, vp, sz, vp, u32, vp, vp]
     lib.nsg_window_stats_from_host.restype = ctypes.c_int
     lib.nsg_window_stats_from_host.argtypes = [vp, u64, u64, vp, vp, vp, vp, sz, vp, vp, u32]
+    lib.nsg_window_vectors.restype = ctypes.c_int
+    lib.nsg_window_vectors.argtypes = [vp, vp, vp, u64, u64, vp, ctypes.POINTER(NsgVectors), vp, sz, vp, u32]
     lib.nsg_diag_offset.restype = sz
     lib.nsg_diag_offset.argtypes = []
     lib.nsg_last_launches.restype = ctypes.c_uint

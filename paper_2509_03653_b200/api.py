@@ -14,7 +14,7 @@ from typing import Optional
 
 import torch
 
-from ._lib import NsgError, load
+from ._lib import NsgError, NsgVectors, load
 
 _lib = load()  # raises ImportError if libnsg.so is missing: there is no fallback
 
@@ -221,3 +221,68 @@ def window_stats_from_host(keys_host: torch.Tensor, window: int = DEFAULT_WINDOW
     if synchronize:
         s.synchronize()
     return out_host[:nw] if out_host.dim() == 2 else out_host
+
+
+IP_SET_NAMES = ("union", "src_only", "dst_only", "both")
+
+
+def window_vectors(keys: Optional[torch.Tensor] = None, window: int = DEFAULT_WINDOW, *, src=None, dst=None,
+                   links: bool = True, sources: bool = True, destinations: bool = True, ip_sets: bool = True,
+                   out=None, workspace: Optional[Workspace] = None, stream=None, flags: int = 0) -> dict:
+    """The nine statistics plus the vector outputs of nsg_window_vectors.
+
+    Input: packed `keys` (device int64/uint64) or SoA `src`, `dst` (device int32/uint32).  Returns a dict of
+    device tensors (valid once `stream` completes): "stats" int64 [n_windows, 9]; when requested,
+    "link_key" int64 [n] with "link_packets" int32 [n] (PAPER.md:182), "src_node"/"src_packets"/"src_fanout"
+    int32 [n] (:185, :187), "dst_node"/"dst_packets"/"dst_fanin" int32 [n] (:173), "ip_sets" int64
+    [n_windows, 4] = (|S u D|, |S \\ D|, |D \\ S|, |S n D|) (:209).  Window w's entries of a vector are at
+    [w*window, w*window + count) with count = stats[w, 1] (links), stats[w, 3] (sources) or stats[w, 6]
+    (destinations), in unspecified (hash) order; 32-bit values are the u32 bit patterns.
+    """
+    if keys is not None:
+        if src is not None or dst is not None:
+            raise ValueError("pass either keys or (src, dst)")
+        _check(keys, "keys", _U64_TYPES)
+        n, device = keys.numel(), keys.device
+    else:
+        _check(src, "src", _U32_TYPES)
+        _check(dst, "dst", _U32_TYPES)
+        if src.numel() != dst.numel() or src.device != dst.device:
+            raise ValueError("src and dst must have the same length and device")
+        n, device = src.numel(), src.device
+    window = int(window)
+    if window < 1 or window > MAX_WINDOW:
+        raise ValueError(f"window must be in [1, 2^31], got {window}")
+    nw = num_windows(n, window)
+    if out is None:
+        out = torch.empty((nw, NUM_STATS), dtype=torch.int64, device=device)
+    elif out.dtype not in _U64_TYPES or not out.is_contiguous() or out.numel() < nw * NUM_STATS or not out.is_cuda:
+        raise ValueError("out must be a contiguous CUDA int64/uint64 tensor with >= n_windows*9 elements")
+    r = {"stats": out}
+    v = NsgVectors()
+    if links:
+        r["link_key"] = torch.empty(n, dtype=torch.int64, device=device)
+        r["link_packets"] = torch.empty(n, dtype=torch.int32, device=device)
+        v.link_key, v.link_packets = r["link_key"].data_ptr(), r["link_packets"].data_ptr()
+    if sources:
+        for k in ("src_node", "src_packets", "src_fanout"):
+            r[k] = torch.empty(n, dtype=torch.int32, device=device)
+        v.src_node, v.src_packets, v.src_fanout = (r[k].data_ptr() for k in ("src_node", "src_packets", "src_fanout"))
+    if destinations:
+        for k in ("dst_node", "dst_packets", "dst_fanin"):
+            r[k] = torch.empty(n, dtype=torch.int32, device=device)
+        v.dst_node, v.dst_packets, v.dst_fanin = (r[k].data_ptr() for k in ("dst_node", "dst_packets", "dst_fanin"))
+    if ip_sets:
+        r["ip_sets"] = torch.empty((nw, 4), dtype=torch.int64, device=device)
+        v.ip_sets = r["ip_sets"].data_ptr()
+    if n == 0:
+        return r
+    ws = _workspace(n, window, device, workspace)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_window_vectors(
+        None if src is None else src.data_ptr(), None if dst is None else dst.data_ptr(),
+        None if keys is None else keys.data_ptr(), n, window, out.data_ptr(), ctypes.byref(v), ws.ptr, ws.nbytes,
+        ctypes.c_void_p(s.cuda_stream), int(flags))
+    if rc != 0:
+        raise NsgError(rc, "nsg_window_vectors")
+    return r

@@ -43,7 +43,7 @@ struct Layout {
   u64 nw;
   // fast
   u32 logB, B, logB2, B2, cp, cp_last, R;
-  size_t o_pw, o_kscr, o_koff, o_rscr, o_roff, o_rend, o_lres, o_sres;
+  size_t o_pw, o_s0win, o_kscr, o_koff, o_rscr, o_roff, o_rend, o_lres, o_sres, o_s0list;
   size_t memset_bytes;
   // global
   u64 LC;
@@ -57,10 +57,6 @@ static Layout make_layout(u64 n, u64 W, int sms) {
   memset(&L, 0, sizeof(L));
   L.nw = (n + W - 1) / W;
   L.fast = W <= FAST_MAX_WINDOW;
-  size_t o = CTRL_BYTES;
-  L.o_pw = o;  // per window: pdone, ldone, sdone, fin, ovf, arrived (streamed input)
-  o = align256(o + 6 * sizeof(u32) * L.nw);
-  L.memset_bytes = o;
   if (L.fast) {
     const u64 want = (W + BUCKET_KEYS - 1) / BUCKET_KEYS;
     L.B = (u32)next_pow2(want < 1 ? 1 : want);
@@ -72,6 +68,17 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     const u64 last = n - (L.nw - 1) * W;
     L.cp_last = (u32)((last + CH - 1) / CH);
     L.R = (u32)(L.nw < (u64)RSLOTS ? next_pow2(L.nw) : (u64)RSLOTS);
+  }
+  size_t o = CTRL_BYTES;
+  // zeroed at every call: per window pdone, ldone, sdone, fin, ovf, arrived (streamed input) and the
+  // three vector fill counters; per (slot, side bucket) the published-window word and list length of
+  // the side-0 node lists (IP sets)
+  L.o_pw = o;
+  o = align256(o + 9 * sizeof(u32) * L.nw);
+  L.o_s0win = o;
+  o = align256(o + 2 * sizeof(u32) * (size_t)L.R * L.B2);
+  L.memset_bytes = o;
+  if (L.fast) {
     L.o_kscr = o; o = align256(o + (size_t)L.R * L.cp * CH * sizeof(u64));
     L.o_koff = o; o = align256(o + (size_t)L.R * L.cp * (L.B + 1) * sizeof(u32));
     L.o_rscr = o; o = align256(o + (size_t)L.R * L.B * RCAP * sizeof(u64));
@@ -79,6 +86,7 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     L.o_rend = o; o = align256(o + (size_t)L.R * L.B * (2 * L.B2) * sizeof(u32));
     L.o_lres = o; o = align256(o + (size_t)L.R * L.B * 4 * sizeof(u32));
     L.o_sres = o; o = align256(o + (size_t)L.R * 2 * L.B2 * 4 * sizeof(u32));
+    L.o_s0list = o; o = align256(o + (size_t)L.R * L.B2 * TCAP_S * sizeof(u32));
   }
   // L2-path table sets: the full path for large windows, the overflow hand-off otherwise.
   L.LC = next_pow2(2 * W);
@@ -168,7 +176,7 @@ static WriteValue32Fn write_value32() {
 
 static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u64 W, u64* out, void* ws,
                       size_t ws_bytes, void* stream, u32 flags, void* ev_before = nullptr, void* ev_after = nullptr,
-                      const StreamIn* sin = nullptr) {
+                      const StreamIn* sin = nullptr, const nsg_vectors* vec = nullptr) {
   g_last_launches = 0;
   if (W == 0 || W > NSG_MAX_WINDOW) return NSG_ERR_INVALID_ARGUMENT;
   if (n == 0) return NSG_OK;
@@ -177,6 +185,19 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
   if (!out || !ws) return NSG_ERR_INVALID_ARGUMENT;
   if ((reinterpret_cast<uintptr_t>(ws) & 255) || (reinterpret_cast<uintptr_t>(out) & 7)) return NSG_ERR_INVALID_ARGUMENT;
   if (keys && (reinterpret_cast<uintptr_t>(keys) & 7)) return NSG_ERR_INVALID_ARGUMENT;
+  nsg_vectors V;
+  memset(&V, 0, sizeof(V));
+  if (vec) {
+    V = *vec;
+    // a vector is requested only as a whole: its arrays are all NULL or all non-NULL, naturally aligned
+    if (!V.link_key != !V.link_packets) return NSG_ERR_INVALID_ARGUMENT;
+    if (!V.src_node != !V.src_packets || !V.src_node != !V.src_fanout) return NSG_ERR_INVALID_ARGUMENT;
+    if (!V.dst_node != !V.dst_packets || !V.dst_node != !V.dst_fanin) return NSG_ERR_INVALID_ARGUMENT;
+    const void* a8[] = {V.link_key, V.ip_sets};
+    const void* a4[] = {V.link_packets, V.src_node, V.src_packets, V.src_fanout, V.dst_node, V.dst_packets, V.dst_fanin};
+    for (const void* p : a8) if (reinterpret_cast<uintptr_t>(p) & 7) return NSG_ERR_INVALID_ARGUMENT;
+    for (const void* p : a4) if (reinterpret_cast<uintptr_t>(p) & 3) return NSG_ERR_INVALID_ARGUMENT;
+  }
   if (src && ((reinterpret_cast<uintptr_t>(src) & 3) || (reinterpret_cast<uintptr_t>(dst) & 3)))
     return NSG_ERR_INVALID_ARGUMENT;
   DevInfo d;
@@ -226,6 +247,10 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
   gg.nF = reinterpret_cast<u32*>(base + L.o_gnf);
   gg.ovf = pw + 4 * L.nw;
   gg.diag = reinterpret_cast<u32*>(base + DIAG_OFFSET);
+  gg.v_lkey = reinterpret_cast<u64*>(V.link_key); gg.v_lpk = V.link_packets;
+  gg.v_node[0] = V.src_node; gg.v_pk[0] = V.src_packets; gg.v_fan[0] = V.src_fanout;
+  gg.v_node[1] = V.dst_node; gg.v_pk[1] = V.dst_packets; gg.v_fan[1] = V.dst_fanin;
+  gg.v_ipsets = reinterpret_cast<u64*>(V.ip_sets);
 
   const bool use_fast = L.fast && !(flags & NSG_FLAG_FORCE_GLOBAL);
   if (use_fast) {
@@ -246,6 +271,13 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
     g.rend = reinterpret_cast<u32*>(base + L.o_rend);
     g.lres = reinterpret_cast<u32*>(base + L.o_lres);
     g.sres = reinterpret_cast<u32*>(base + L.o_sres);
+    g.v_lkey = gg.v_lkey; g.v_lpk = gg.v_lpk;
+    for (int sd = 0; sd < 2; ++sd) { g.v_node[sd] = gg.v_node[sd]; g.v_pk[sd] = gg.v_pk[sd]; g.v_fan[sd] = gg.v_fan[sd]; }
+    g.v_ipsets = gg.v_ipsets;
+    g.vfill = pw + 6 * L.nw;
+    g.s0win = reinterpret_cast<u32*>(base + L.o_s0win);
+    g.s0cnt = g.s0win + (size_t)L.R * L.B2;
+    g.s0list = reinterpret_cast<u32*>(base + L.o_s0list);
     {  // ticket regions (see Geo): breakpoints where an item class enters or leaves the schedule
       u64 pts[8] = {0, (u64)LAG_L, (u64)LAG_S, (u64)LAG_F, L.nw, L.nw + LAG_L, L.nw + LAG_S, L.nw + LAG_F};
       std::sort(pts, pts + 8);
@@ -374,6 +406,15 @@ nsg_status nsg_window_stats_from_host(const uint64_t* keys_host, uint64_t n_pack
   if (cudaMemcpyAsync(out_host, out, bytes, cudaMemcpyDeviceToHost, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
     return NSG_ERR_CUDA;
   return NSG_OK;
+}
+
+nsg_status nsg_window_vectors(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
+                              uint64_t window, uint64_t* out, const nsg_vectors* vectors, void* workspace,
+                              size_t workspace_bytes, void* stream, uint32_t flags) {
+  if (!vectors) return NSG_ERR_INVALID_ARGUMENT;
+  return nsg::run(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_packets, window,
+                  reinterpret_cast<nsg::u64*>(out), workspace, workspace_bytes, stream, flags, nullptr, nullptr,
+                  nullptr, vectors);
 }
 
 size_t nsg_diag_offset(void) { return nsg::DIAG_OFFSET; }

@@ -75,4 +75,15 @@ __device__ __forceinline__ u32 warp_max(u32 v) {
   return v;
 }
 
+// Rank of this lane among the lanes of its warp with `want`, offset by a CTA-shared counter that the
+// warp advances once (warp-aggregated append).  All lanes of the warp must call it.
+__device__ __forceinline__ u32 warp_append(bool want, u32* ctr) {
+  const u32 mask = __ballot_sync(0xffffffffu, want);
+  const int lane = threadIdx.x & 31;
+  u32 base = 0;
+  if (mask && lane == 0) base = atomicAdd(ctr, (u32)__popc(mask));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  return base + (u32)__popc(mask & ((1u << lane) - 1u));
+}
+
 }  // namespace nsg

@@ -71,7 +71,7 @@ constexpr u32 REC_PBITS = 20, REC_FMAX = 4095;
 __host__ __device__ __forceinline__ u64 make_rec(u32 node, u32 f, u32 p) {
   return ((u64)node << 32) | ((u64)f << REC_PBITS) | p;
 }
-static_assert(TCAP % FT == 0, "emission loop is warp-uniform");
+static_assert(TCAP % FT == 0 && TCAP_S % FT == 0, "emission / vector loops are warp-uniform");
 constexpr int LAG_L = 8, LAG_S = 20, LAG_F = 26;  // pipeline lags (steps) of L, S, F items behind P (measured plateau)
 constexpr int LOG_RSLOTS = 5;
 constexpr int RSLOTS = 1 << LOG_RSLOTS;      // scratch slots (windows in flight), > LAG_S
@@ -106,7 +106,16 @@ struct Geo {
   u32* roff;  // [R][B][2B+1]    start offsets of (side, side bucket) inside each link bucket's records
   u32* rend;  // [R][B][2B]      end offsets (records are aggregated per node, so segments may be short)
   u32* lres;  // [R][B][4]       per link bucket: unique links, max count, sum of counts
-  u32* sres;  // [R][2][B][4]    per side bucket: unique nodes, max packets, max fan
+  u32* sres;  // [R][2][B][4]    per side bucket: unique nodes, max packets, max fan, |S n D| (side 1)
+  // Optional vector outputs (nsg_window_vectors); NULL = not requested.  Window
+  // w's entries go to [w*W, w*W + count) of each array, in hash order.
+  u64* v_lkey; u32* v_lpk;                   // links: key, A_t(i,j)
+  u32* v_node[2]; u32* v_pk[2]; u32* v_fan[2];  // per side: node, packets, fan              (:185, :187, :173)
+  u64* v_ipsets;                             // [nw][4] |S u D|, |S \ D|, |D \ S|, |S n D|   (:209)
+  u32* vfill;   // [nw][3] fill counters of the link / source / destination vectors
+  u32* s0list;  // [R][B2][TCAP_S] node list of each side-0 item (read by the side-1 item of the bucket)
+  u32* s0cnt;   // [R][B2]
+  u32* s0win;   // [R][B2]         w+1 once side item S0(w, sb) has published its list (release)
 };
 
 struct SmemP { u64 stage[CH]; u32 hist[MAXB + 1]; };
@@ -130,6 +139,8 @@ struct SmemMisc {
   u32 type, idx;
   u32 pcnt[2];  // pending-list fill counters
   u32 hot[2];   // link item: per side, a side bucket holding >= 8x the average records (or ~0u)
+  u32 vbase, vcnt;  // vector outputs: the item's base inside its window's region, its fill counter
+  u32 n0, both;     // side-1 item with IP sets: entries in S0's node list, nodes found on both sides
   u64 w;
 };
 constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
@@ -507,6 +518,16 @@ __device__ __forceinline__ u32 warp_segments(u32* wlo, u32* wpre, u32 nseg, u32 
   return total;
 }
 
+// Vector output of one link (all lanes of the warp call it; `valid` lanes write).
+__device__ __forceinline__ void emit_link(const Geo& g, u64 w, SmemMisc& m, bool valid, u64 key, u32 c) {
+  const u32 r = warp_append(valid, &m.vcnt);
+  if (valid) {
+    const u64 p = w * g.W + m.vbase + r;
+    g.v_lkey[p] = key;
+    g.v_lpk[p] = c;
+  }
+}
+
 __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Claim& cl) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   PhaseTimer pt;
@@ -654,6 +675,10 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Cla
     __syncwarp();
     u32* off = g.roff + ((u64)slot * B + b) * (2 * B2 + 1);
     for (int i = t; i <= (int)(2 * B2); i += 32) off[i] = s.hist[i];
+    if (t == 0 && g.v_lkey) {  // this bucket's links (two records each) get a contiguous part of the window's region
+      m.vbase = atomicAdd(&g.vfill[w * 3], s.hist[2 * B2] / 2);
+      m.vcnt = 0;
+    }
   }
   __syncthreads();
   pt.mark(g, 1, 3);
@@ -667,13 +692,15 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Cla
   if (hot0 == ~0u && hot1 == ~0u) {  // CTA-uniform: no skewed side bucket (the common case)
     for (int i = t; i < TCAP; i += FT) {
       const u64 key = s.lkey[i];
+      u32 c = 0;
       if (key != EMPTY64) {
-        const u32 c = s.lcnt[i];
+        c = s.lcnt[i];
         nl += 1; mx = max(mx, c); sm += c;
         const u32 sn = (u32)(key >> 32), dn = (u32)key;
         rec[atomicAdd(&s.hist[side_bucket(sn, logB2)], 1u)] = make_rec(sn, 1u, c);
         rec[atomicAdd(&s.hist[B2 + side_bucket(dn, logB2)], 1u)] = make_rec(dn, 1u, c);
       }
+      if (g.v_lkey) emit_link(g, w, m, key != EMPTY64, key, c);  // CTA-uniform
     }
   } else {
     // per side, a warp cache node (seeded from the hot bucket's first record of the warp while it has
@@ -700,6 +727,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Cla
         }
         if (valid && !hit) rec[atomicAdd(&s.hist[side * B2 + sbk], 1u)] = make_rec(node, 1u, c);
       }
+      if (g.v_lkey) emit_link(g, w, m, valid, key, c);
     }
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
@@ -723,6 +751,10 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Cla
     const u64 r = make_rec(EMPTY32, 1u, c);
     rec[atomicAdd(&s.hist[side_bucket(EMPTY32, logB2)], 1u)] = r;
     rec[atomicAdd(&s.hist[B2 + side_bucket(EMPTY32, logB2)], 1u)] = r;
+    if (g.v_lkey) {
+      const u64 p = w * g.W + m.vbase + atomicAdd(&m.vcnt, 1u);
+      g.v_lkey[p] = EMPTY64; g.v_lpk[p] = c;
+    }
   }
   nl = warp_sum(nl); mx = warp_max(mx); sm = warp_sum(sm);
   if (lane == 0) { m.wtmp[4 * NWARP + wid] = nl; m.wtmp[5 * NWARP + wid] = mx; m.wtmp[6 * NWARP + wid] = sm; }
@@ -757,7 +789,7 @@ __device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict_
   // all side items of window w are complete (waited for at the previous item boundary)
   // sums: 0 links, 1 sum of counts, 2 unique sources, 3 unique destinations;
   // maxes: 4 max link, 5 max source packets, 6 max fan-out, 7 max destination packets, 8 max fan-in
-  u32 v[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  u32 v[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // [9]: |S n D| (IP sets)
   for (u32 i = t; i < g.B; i += FT) {
     const u32* r = g.lres + ((u64)slot * g.B + i) * 4;
     v[0] += ldcg32(r); v[4] = max(v[4], ldcg32(r + 1)); v[1] += ldcg32(r + 2);
@@ -767,21 +799,24 @@ __device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict_
     const u32* s1 = g.sres + (((u64)slot * 2 + 1) * g.B2 + i) * 4;
     v[2] += ldcg32(s0); v[5] = max(v[5], ldcg32(s0 + 1)); v[6] = max(v[6], ldcg32(s0 + 2));
     v[3] += ldcg32(s1); v[7] = max(v[7], ldcg32(s1 + 1)); v[8] = max(v[8], ldcg32(s1 + 2));
+    v[9] += ldcg32(s1 + 3);
   }
 #pragma unroll
   for (int j = 0; j < 4; ++j) v[j] = warp_sum(v[j]);
 #pragma unroll
   for (int j = 4; j < 9; ++j) v[j] = warp_max(v[j]);
+  v[9] = warp_sum(v[9]);
   const int lane = t & 31, wid = t >> 5;
   __syncthreads();
   if (lane == 0)
-    for (int j = 0; j < 9; ++j) m.wtmp[j * NWARP + wid] = v[j];
+    for (int j = 0; j < 10; ++j) m.wtmp[j * NWARP + wid] = v[j];
   __syncthreads();
   if (t == 0) {
-    u32 r[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    u32 r[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     for (int i = 0; i < NWARP; ++i) {
       for (int j = 0; j < 4; ++j) r[j] += m.wtmp[j * NWARP + i];
       for (int j = 4; j < 9; ++j) r[j] = max(r[j], m.wtmp[j * NWARP + i]);
+      r[9] += m.wtmp[9 * NWARP + i];
     }
     const u64 wlen = min(g.W, g.n - w * g.W);
     u64* o = out + w * NSG_NUM_STATS;
@@ -794,6 +829,10 @@ __device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict_
     o[NSG_UNIQUE_DESTINATIONS] = r[3];
     o[NSG_MAX_DESTINATION_PACKETS] = r[7];
     o[NSG_MAX_DESTINATION_FANIN] = r[8];
+    if (g.v_ipsets) {  // |S u D|, |S \ D|, |D \ S|, |S n D|
+      u64* ip = g.v_ipsets + w * 4;
+      ip[0] = (u64)r[2] + r[3] - r[9]; ip[1] = r[2] - r[9]; ip[2] = r[3] - r[9]; ip[3] = r[9];
+    }
     if ((u64)r[1] != wlen && ld_acquire32(&g.ovf[w]) == 0) atomicAdd(&g.diag[1], 1u);
     if ((g.flags & NSG_FLAG_INJECT_OVERFLOW) && (w & 1)) mark_overflow(g, w);
     // The slot may now be reused: every reader of it has signalled sdone.  (Dropping its dead L2
@@ -805,6 +844,92 @@ __device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict_
 // ------------------------------------------------------------------------------------------
 // S item: merge side bucket sb of one side of window w
 // ------------------------------------------------------------------------------------------
+// Is `node` in the (complete) node table?  Linear probing from its home slot; slots never empty again.
+__device__ __forceinline__ bool node_present(const u32* key, u32 node) {
+  const u32 home = node_home(node);
+  for (u32 probe = 0; probe < (u32)TCAP_S; ++probe) {
+    const u32 k = key[probe_slot_s(home, probe)];
+    if (k == node) return true;
+    if (k == EMPTY32) return false;
+  }
+  return false;
+}
+
+// Vector outputs of a side item (after its table is final and m.wtmp holds the per-warp node counts):
+//  - the nodes with their packets and fan (A_t 1 / |A_t|_0 1 or the mirrors)
+//    into the window's region of v_node/v_pk/v_fan[side];
+//  - IP sets: side 0 publishes its node list; side 1 waits for the list of the side-0
+//    item of the same bucket (same node hash partition: side_bucket() is one function of the address)
+//    and counts the listed nodes present in its own table, i.e. |S n D| restricted to the bucket.
+// S0(w, sb) holds a smaller ticket than S1(w, sb), so the wait cannot deadlock.
+// (Takes its pointers by value: a Geo& to a __noinline__ function would put the kernel's parameter
+// block in local memory.)
+struct SideVec {
+  u32 *node, *pk, *fan;  // this side's vectors (node NULL: not requested)
+  bool ipsets;
+  u32 *vfill, *s0list, *s0cnt, *s0win;
+  u64 W;
+  u32 B2;
+};
+__device__ __noinline__ void side_vectors(const SideVec g, u64 w, int side, u32 sb, u32 slot, SmemS& s, SmemMisc& m) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const bool nodes = g.node != nullptr;
+  const bool list0 = side == 0 && g.ipsets;
+  u32* list = g.s0list + ((u64)slot * g.B2 + sb) * TCAP_S;
+  if (t == 0) {
+    u32 tot = 0;
+    for (int i = 0; i < NWARP; ++i) tot += m.wtmp[4 * NWARP + i];
+    m.vbase = nodes ? atomicAdd(&g.vfill[w * 3 + 1 + side], tot) : 0u;
+    m.vcnt = 0;
+  }
+  __syncthreads();
+  const u64 wb = w * g.W + m.vbase;
+  if (nodes || list0) {
+    for (int i = t; i < TCAP_S; i += FT) {  // TCAP_S % FT == 0: warp-uniform trip count
+      const u32 node = s.key[i];
+      const bool valid = node != EMPTY32;
+      const u32 r = warp_append(valid, &m.vcnt);
+      if (valid) {
+        if (nodes) { g.node[wb + r] = node; g.pk[wb + r] = s.P[i]; g.fan[wb + r] = s.F[i]; }
+        if (list0) list[r] = node;
+      }
+    }
+    if (t == 0 && m.esc[2]) {  // the address ~0 (255.255.255.255), kept outside the table
+      const u32 r = atomicAdd(&m.vcnt, 1u);
+      if (nodes) { g.node[wb + r] = EMPTY32; g.pk[wb + r] = m.esc[1]; g.fan[wb + r] = m.esc[2]; }
+      if (list0) list[r] = EMPTY32;
+    }
+    __syncthreads();
+  }
+  if (list0 && t == 0) {
+    g.s0cnt[(u64)slot * g.B2 + sb] = m.vcnt;
+    st_release32(&g.s0win[(u64)slot * g.B2 + sb], (u32)w + 1u);  // after the barrier: publishes every lane's list writes
+  }
+  if (side == 1 && g.ipsets) {
+    if (t == 0) {
+      const u32* f = &g.s0win[(u64)slot * g.B2 + sb];
+      while (ld_acquire32(f) != (u32)w + 1u) __nanosleep(64);
+      m.n0 = ldcg32(&g.s0cnt[(u64)slot * g.B2 + sb]);
+    }
+    __syncthreads();
+    const u32 n0 = m.n0;
+    u32 hits = 0;
+    for (u32 i = t; i < n0; i += FT) {
+      const u32 node = ldcg32(&list[i]);
+      hits += node == EMPTY32 ? (m.esc[2] != 0u) : (u32)node_present(s.key, node);
+    }
+    hits = warp_sum(hits);
+    if (lane == 0) m.wtmp[7 * NWARP + wid] = hits;
+    __syncthreads();
+    if (t == 0) {
+      u32 b = 0;
+      for (int i = 0; i < NWARP; ++i) b += m.wtmp[7 * NWARP + i];
+      m.both = b;
+    }
+    __syncthreads();
+  }
+}
+
 __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemMisc& m, Claim& cl) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
 #ifdef NSG_EXP_SKIP_S  // timing experiment only: results are wrong
@@ -962,6 +1087,11 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
   if (lane == 0) { m.wtmp[4 * NWARP + wid] = d; m.wtmp[5 * NWARP + wid] = mp; m.wtmp[6 * NWARP + wid] = mf; }
   __syncthreads();
   pt.mark(g, 2, 3);
+  if ((side ? g.v_node[1] : g.v_node[0]) || g.v_ipsets) {  // CTA-uniform
+    const SideVec sv{side ? g.v_node[1] : g.v_node[0], side ? g.v_pk[1] : g.v_pk[0], side ? g.v_fan[1] : g.v_fan[0],
+                     g.v_ipsets != nullptr, g.vfill, g.s0list, g.s0cnt, g.s0win, g.W, g.B2};
+    side_vectors(sv, w, side, sb, slot, s, m);
+  }
   if (wid == 0) {
     u32 a = lane < NWARP ? m.wtmp[4 * NWARP + lane] : 0u;
     u32 bp = lane < NWARP ? m.wtmp[5 * NWARP + lane] : 0u;
@@ -972,7 +1102,7 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
     }
     if (lane == 0) {
       u32* res = g.sres + (((u64)slot * 2 + side) * B2 + sb) * 4;
-      res[0] = a; res[1] = bp; res[2] = cf;
+      res[0] = a; res[1] = bp; res[2] = cf; res[3] = (side == 1 && g.v_ipsets) ? m.both : 0u;
       if (m.flag) mark_overflow(g, w);
       red_release_add32(&g.sdone[w], 1u);  // thread 0 wrote res itself: program order + release
       prof_add(g, 2, clock64() - tstart, waited);

@@ -21,6 +21,10 @@ struct GGeo {
   u32* nF;      // [G][2][LC]
   const u32* ovf;
   u32* diag;
+  // optional vector outputs (as Geo): window w's entries at [w*W, w*W + count), hash order
+  u64* v_lkey; u32* v_lpk;
+  u32* v_node[2]; u32* v_pk[2]; u32* v_fan[2];
+  u64* v_ipsets;
 };
 
 __device__ __forceinline__ void glob_link_insert(u64* lkey, u32* lcnt, u64 LC, u64 key) {
@@ -51,11 +55,22 @@ __device__ __forceinline__ void glob_node_upsert(u32* key, u32* P, u32* F, u64 L
   }
 }
 
+__device__ __forceinline__ bool glob_node_present(const u32* key, u64 LC, u32 node) {
+  u64 slot = ((u64)hash32(node) * 0x9E3779B97F4A7C15ull >> 11) & (LC - 1);
+  for (;;) {
+    const u32 k = ldcg32(&key[slot]);
+    if (k == node) return true;
+    if (k == EMPTY32) return false;
+    slot = (slot + 1) & (LC - 1);
+  }
+}
+
 __global__ void __launch_bounds__(GT)
 global_kernel(GGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, const u64* __restrict__ keys,
               u64* __restrict__ out) {
   __shared__ u32 esc[5];
   __shared__ u32 red[9 * (GT / 32)];
+  __shared__ u32 vcnt[3], both_s;
   if (g.only_overflowed && ldcg32(&g.diag[0]) == 0) return;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const u64 LC = g.LC;
@@ -73,6 +88,8 @@ global_kernel(GGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, 
       }
     }
     if (t < 5) esc[t] = 0;
+    if (t < 3) vcnt[t] = 0;
+    if (t == 0) both_s = 0;
     __syncthreads();
     for (u64 i = t; i < len; i += GT) {
       const u64 key = keys ? keys[base + i] : (((u64)src[base + i] << 32) | dst[base + i]);
@@ -87,28 +104,62 @@ global_kernel(GGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, 
     u32* F0 = g.nF + ((u64)blockIdx.x * 2 + 0) * LC;
     u32* F1 = g.nF + ((u64)blockIdx.x * 2 + 1) * LC;
     u32 nl = 0, mx = 0, sm = 0;
-    for (u64 i = t; i < LC; i += GT) {
-      const u64 key = ldcg64(&lkey[i]);
+    const u64 wb = w * g.W;  // the window's region of the vector outputs
+    for (u64 i0 = 0; i0 < LC; i0 += GT) {  // warp-uniform trip count (vector appends are warp-collective)
+      const u64 i = i0 + t;
+      const u64 key = i < LC ? ldcg64(&lkey[i]) : EMPTY64;
+      u32 c = 0;
       if (key != EMPTY64) {
-        const u32 c = ldcg32(&lcnt[i]);
+        c = ldcg32(&lcnt[i]);
         nl += 1; mx = max(mx, c); sm += c;
         glob_node_upsert(k0, P0, F0, LC, &esc[1], &esc[2], (u32)(key >> 32), c, 1);
         glob_node_upsert(k1, P1, F1, LC, &esc[3], &esc[4], (u32)key, c, 1);
+      }
+      if (g.v_lkey) {
+        const u32 r = warp_append(key != EMPTY64, &vcnt[0]);
+        if (key != EMPTY64) { g.v_lkey[wb + r] = key; g.v_lpk[wb + r] = c; }
       }
     }
     if (t == 0 && esc[0]) {
       const u32 c = esc[0];
       nl += 1; mx = max(mx, c); sm += c;
       atomicAdd(&esc[1], c); atomicAdd(&esc[2], 1u); atomicAdd(&esc[3], c); atomicAdd(&esc[4], 1u);
+      if (g.v_lkey) { const u32 r = atomicAdd(&vcnt[0], 1u); g.v_lkey[wb + r] = EMPTY64; g.v_lpk[wb + r] = c; }
     }
     __syncthreads();
-    u32 d0 = 0, p0 = 0, f0 = 0, d1 = 0, p1 = 0, f1 = 0;
-    for (u64 i = t; i < LC; i += GT) {
-      if (ldcg32(&k0[i]) != EMPTY32) { d0 += 1; p0 = max(p0, ldcg32(&P0[i])); f0 = max(f0, ldcg32(&F0[i])); }
-      if (ldcg32(&k1[i]) != EMPTY32) { d1 += 1; p1 = max(p1, ldcg32(&P1[i])); f1 = max(f1, ldcg32(&F1[i])); }
+    u32 d0 = 0, p0 = 0, f0 = 0, d1 = 0, p1 = 0, f1 = 0, both = 0;
+    for (u64 i0 = 0; i0 < LC; i0 += GT) {
+      const u64 i = i0 + t;
+      const u32 n0 = i < LC ? ldcg32(&k0[i]) : EMPTY32, n1 = i < LC ? ldcg32(&k1[i]) : EMPTY32;
+      u32 a0 = 0, b0 = 0, a1 = 0, b1 = 0;
+      if (n0 != EMPTY32) {
+        a0 = ldcg32(&P0[i]); b0 = ldcg32(&F0[i]);
+        d0 += 1; p0 = max(p0, a0); f0 = max(f0, b0);
+        if (g.v_ipsets) both += (u32)glob_node_present(k1, LC, n0);
+      }
+      if (n1 != EMPTY32) { a1 = ldcg32(&P1[i]); b1 = ldcg32(&F1[i]); d1 += 1; p1 = max(p1, a1); f1 = max(f1, b1); }
+      if (g.v_node[0]) {
+        const u32 r = warp_append(n0 != EMPTY32, &vcnt[1]);
+        if (n0 != EMPTY32) { g.v_node[0][wb + r] = n0; g.v_pk[0][wb + r] = a0; g.v_fan[0][wb + r] = b0; }
+      }
+      if (g.v_node[1]) {
+        const u32 r = warp_append(n1 != EMPTY32, &vcnt[2]);
+        if (n1 != EMPTY32) { g.v_node[1][wb + r] = n1; g.v_pk[1][wb + r] = a1; g.v_fan[1][wb + r] = b1; }
+      }
     }
-    if (t == 0 && esc[1]) { d0 += 1; p0 = max(p0, esc[1]); f0 = max(f0, esc[2]); }
-    if (t == 0 && esc[3]) { d1 += 1; p1 = max(p1, esc[3]); f1 = max(f1, esc[4]); }
+    if (t == 0 && esc[1]) {
+      d0 += 1; p0 = max(p0, esc[1]); f0 = max(f0, esc[2]);
+      both += esc[3] != 0u;  // the address ~0 is a source; is it a destination too?
+      if (g.v_node[0]) { const u32 r = atomicAdd(&vcnt[1], 1u); g.v_node[0][wb + r] = EMPTY32; g.v_pk[0][wb + r] = esc[1]; g.v_fan[0][wb + r] = esc[2]; }
+    }
+    if (t == 0 && esc[3]) {
+      d1 += 1; p1 = max(p1, esc[3]); f1 = max(f1, esc[4]);
+      if (g.v_node[1]) { const u32 r = atomicAdd(&vcnt[2], 1u); g.v_node[1][wb + r] = EMPTY32; g.v_pk[1][wb + r] = esc[3]; g.v_fan[1][wb + r] = esc[4]; }
+    }
+    if (g.v_ipsets) {
+      both = warp_sum(both);
+      if (lane == 0 && both) atomicAdd(&both_s, both);
+    }
     u32 v[9] = {nl, sm, d0, d1, mx, p0, f0, p1, f1};
 #pragma unroll
     for (int j = 0; j < 4; ++j) v[j] = warp_sum(v[j]);
@@ -134,6 +185,11 @@ global_kernel(GGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, 
       o[NSG_MAX_DESTINATION_PACKETS] = r[7];
       o[NSG_MAX_DESTINATION_FANIN] = r[8];
       if ((u64)r[1] != len) atomicAdd(&g.diag[1], 1u);
+      if (g.v_ipsets) {  // |S u D|, |S \ D|, |D \ S|, |S n D|
+        const u32 b = both_s;
+        u64* ip = g.v_ipsets + w * 4;
+        ip[0] = (u64)r[2] + r[3] - b; ip[1] = r[2] - b; ip[2] = r[3] - b; ip[3] = b;
+      }
     }
     __syncthreads();
   }

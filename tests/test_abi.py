@@ -129,3 +129,31 @@ def test_sass_is_sm100a():
         pytest.skip("cuobjdump not available")
     out = subprocess.run(["cuobjdump", "--list-elf", LIB], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_vectors_argument_validation_without_gpu():
+    from paper_2509_03653_b200._lib import NsgVectors
+
+    lib = ctypes.CDLL(LIB)
+    f = lib.nsg_window_vectors
+    f.restype = ctypes.c_int
+    vp, u64 = ctypes.c_void_p, ctypes.c_uint64
+    f.argtypes = [vp, vp, vp, u64, u64, vp, ctypes.POINTER(NsgVectors), vp, ctypes.c_size_t, vp, ctypes.c_uint32]
+    ok = NsgVectors()
+    # n == 0: OK, nothing launched
+    assert f(None, None, None, 0, 4, None, ctypes.byref(ok), None, 0, None, 0) == 0
+    # NULL vectors struct
+    assert f(None, None, 8, 10, 4, 8, None, 256, 1 << 20, None, 0) == 1
+    # a half-specified group
+    for half in ({"link_key": 8}, {"link_packets": 8}, {"src_node": 8, "src_packets": 8},
+                 {"dst_node": 8, "dst_fanin": 8}, {"src_fanout": 4}):
+        v = NsgVectors(**half)
+        assert f(None, None, 8, 10, 4, 8, ctypes.byref(v), 256, 1 << 20, None, 0) == 1, half
+    # misaligned arrays
+    for bad in ({"link_key": 12, "link_packets": 8}, {"link_key": 8, "link_packets": 6}, {"ip_sets": 4},
+                {"src_node": 8, "src_packets": 8, "src_fanout": 2}):
+        v = NsgVectors(**bad)
+        assert f(None, None, 8, 10, 4, 8, ctypes.byref(v), 256, 1 << 20, None, 0) == 1, bad
+    # input / window errors are still checked first
+    assert f(None, None, None, 10, 4, 8, ctypes.byref(ok), 256, 1 << 20, None, 0) == 1
+    assert f(None, None, 8, 10, 0, 8, ctypes.byref(ok), 256, 1 << 20, None, 0) == 1
