@@ -188,6 +188,9 @@ def main():
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--once", action="store_true", help="a single untimed call (for ncu)")
+    ap.add_argument("--outputs", choices=["stats", "vectors"], default="stats",
+                    help="stats: the nine statistics (north_star); vectors: + per-window link / source / "
+                         "destination vectors and IP set counts (nsg_window_vectors, SURVEY §8(f) f1, f3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -227,13 +230,25 @@ def main():
     torch.cuda.synchronize(dev)
     ws = nsg.Workspace(n, WINDOW, dev)
     outs = [torch.empty((WINDOWS_PER_STEP, 9), dtype=torch.int64, device=dev) for _ in range(RING)]
+    vec = args.outputs == "vectors"
+    vbuf = nsg.window_vectors(ring[0], WINDOW, out=outs[0], workspace=ws) if vec else None
     if args.once:
-        nsg.window_stats_packed(ring[0], WINDOW, out=outs[0], workspace=ws)
+        if vec:
+            nsg.window_vectors(ring[0], WINDOW, out=outs[0], workspace=ws, buffers=vbuf)
+        else:
+            nsg.window_stats_packed(ring[0], WINDOW, out=outs[0], workspace=ws)
         torch.cuda.synchronize(dev)
         return 0
 
     def step(i, evs=None):
-        r = nsg.window_stats_packed(ring[i % RING], WINDOW, out=outs[i % RING], workspace=ws, kernel_events=evs)
+        if vec:  # events around the whole call (workspace reset + persistent kernel + overflow check)
+            if evs:
+                evs[0].record()
+            r = nsg.window_vectors(ring[i % RING], WINDOW, out=outs[i % RING], workspace=ws, buffers=vbuf)["stats"]
+            if evs:
+                evs[1].record()
+        else:
+            r = nsg.window_stats_packed(ring[i % RING], WINDOW, out=outs[i % RING], workspace=ws, kernel_events=evs)
         if world > 1:
             gather_window_stats(r, WINDOWS_PER_STEP * world)
         return r
@@ -279,17 +294,30 @@ def main():
     keys_dev = torch.empty(n, dtype=torch.int64, device=dev)
     out_host = torch.empty((WINDOWS_PER_STEP, 9), dtype=torch.int64, pin_memory=True)
     e2e_steps = max(3, min(args.steps, 50))
+    if vec:  # H2D of the keys, the call, D2H of the statistics and every vector array
+        vhost = {k: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for k, t in vbuf.items() if k != "stats"}
+
+        def e2e_once():
+            keys_dev.copy_(host, non_blocking=True)
+            r = nsg.window_vectors(keys_dev, WINDOW, out=outs[0], workspace=ws, buffers=vbuf)
+            out_host.copy_(r["stats"], non_blocking=True)
+            for k, t in vhost.items():
+                t.copy_(r[k], non_blocking=True)
+        d2h_bytes = WINDOWS_PER_STEP * 9 * 8 + sum(t.numel() * t.element_size() for t in vhost.values())
+    else:
+        def e2e_once():
+            nsg.window_stats_from_host(host, WINDOW, device=dev, keys_dev=keys_dev, out=outs[0], out_host=out_host,
+                                       workspace=ws)
+        d2h_bytes = WINDOWS_PER_STEP * 9 * 8
     for _ in range(2):
-        nsg.window_stats_from_host(host, WINDOW, device=dev, keys_dev=keys_dev, out=outs[0], out_host=out_host,
-                                   workspace=ws)
+        e2e_once()
     if world > 1:
         tdist.barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(e2e_steps):
-        nsg.window_stats_from_host(host, WINDOW, device=dev, keys_dev=keys_dev, out=outs[0], out_host=out_host,
-                                   workspace=ws)
+        e2e_once()
     e1.record()
     torch.cuda.synchronize(dev)
     e2e_ms = e0.elapsed_time(e1)
@@ -302,6 +330,9 @@ def main():
     if rank == 0:
         peak, peak_src = peaks()
         alg_bytes = n * BYTES_PER_PACKET + WINDOWS_PER_STEP * BYTES_PER_WINDOW_OUT
+        if vec:  # + the vectors written: 12 B per link / source / destination, 32 B of IP sets per window
+            cnt = outs[0][:, [1, 3, 6]].sum().item()
+            alg_bytes += 12 * cnt + 32 * WINDOWS_PER_STEP
         achieved = alg_bytes / (k_avg / 1e3) / 1e9
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -310,15 +341,18 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": desc + f"; {WINDOWS_PER_STEP} windows x 2^17 packets per GPU per step (C2 batch)",
+            "config": {"workload": desc + f"; {WINDOWS_PER_STEP} windows x 2^17 packets per GPU per step (C2 batch)"
+                       + ("; outputs: stats + link/source/destination vectors + IP sets" if vec else ""),
                        "window": WINDOW, "packets_per_gpu_per_step": n, "parallelism": f"windows sharded dp{world}",
                        "l2": f"inputs larger than L2: ring of {RING} x {n * 8 >> 20} MiB batches per GPU, no flush",
                        "input": "device-resident packed u64 keys (src<<32|dst)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 8,
-                    "d2h_bytes_per_step": WINDOWS_PER_STEP * 9 * 8, "steps": e2e_steps},
+                    "d2h_bytes_per_step": d2h_bytes, "steps": e2e_steps},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic_per_launch(args.workload), "peak_source": peak_src,
-                         "kernel": "nsg::fast_kernel", "kernel_ms_avg": k_avg,
+                         "traffic": traffic_per_launch(args.workload + ("-vectors" if vec else "")), "peak_source": peak_src,
+                         "kernel": "nsg::fast_kernel" + (" (+ reset and overflow-check launches: events around "
+                                                          "the whole nsg_window_vectors call)" if vec else ""),
+                         "kernel_ms_avg": k_avg,
                          "algorithmic_bytes_per_launch": alg_bytes},
             "cpu_baseline": cpu,
             "clocks": clocks,

@@ -228,7 +228,8 @@ IP_SET_NAMES = ("union", "src_only", "dst_only", "both")
 
 def window_vectors(keys: Optional[torch.Tensor] = None, window: int = DEFAULT_WINDOW, *, src=None, dst=None,
                    links: bool = True, sources: bool = True, destinations: bool = True, ip_sets: bool = True,
-                   out=None, workspace: Optional[Workspace] = None, stream=None, flags: int = 0) -> dict:
+                   out=None, workspace: Optional[Workspace] = None, stream=None, flags: int = 0,
+                   buffers: Optional[dict] = None) -> dict:
     """The nine statistics plus the vector outputs of nsg_window_vectors.
 
     Input: packed `keys` (device int64/uint64) or SoA `src`, `dst` (device int32/uint32).  Returns a dict of
@@ -238,6 +239,8 @@ def window_vectors(keys: Optional[torch.Tensor] = None, window: int = DEFAULT_WI
     [n_windows, 4] = (|S u D|, |S \\ D|, |D \\ S|, |S n D|) (:209).  Window w's entries of a vector are at
     [w*window, w*window + count) with count = stats[w, 1] (links), stats[w, 3] (sources) or stats[w, 6]
     (destinations), in unspecified (hash) order; 32-bit values are the u32 bit patterns.
+    `buffers`: optional preallocated output tensors (a dict as returned by an earlier call with the same
+    n and window), reused instead of allocating.
     """
     if keys is not None:
         if src is not None or dst is not None:
@@ -260,20 +263,29 @@ def window_vectors(keys: Optional[torch.Tensor] = None, window: int = DEFAULT_WI
         raise ValueError("out must be a contiguous CUDA int64/uint64 tensor with >= n_windows*9 elements")
     r = {"stats": out}
     v = NsgVectors()
+
+    def alloc(name, shape, dtype):
+        t = None if buffers is None else buffers.get(name)
+        if t is None:
+            return torch.empty(shape, dtype=dtype, device=device)
+        if t.dtype != dtype or tuple(t.shape) != tuple(shape) or not t.is_contiguous() or t.device != device:
+            raise ValueError(f"buffers[{name!r}] must be a contiguous {dtype} tensor of shape {shape} on {device}")
+        return t
+
     if links:
-        r["link_key"] = torch.empty(n, dtype=torch.int64, device=device)
-        r["link_packets"] = torch.empty(n, dtype=torch.int32, device=device)
+        r["link_key"] = alloc("link_key", (n,), torch.int64)
+        r["link_packets"] = alloc("link_packets", (n,), torch.int32)
         v.link_key, v.link_packets = r["link_key"].data_ptr(), r["link_packets"].data_ptr()
     if sources:
         for k in ("src_node", "src_packets", "src_fanout"):
-            r[k] = torch.empty(n, dtype=torch.int32, device=device)
+            r[k] = alloc(k, (n,), torch.int32)
         v.src_node, v.src_packets, v.src_fanout = (r[k].data_ptr() for k in ("src_node", "src_packets", "src_fanout"))
     if destinations:
         for k in ("dst_node", "dst_packets", "dst_fanin"):
-            r[k] = torch.empty(n, dtype=torch.int32, device=device)
+            r[k] = alloc(k, (n,), torch.int32)
         v.dst_node, v.dst_packets, v.dst_fanin = (r[k].data_ptr() for k in ("dst_node", "dst_packets", "dst_fanin"))
     if ip_sets:
-        r["ip_sets"] = torch.empty((nw, 4), dtype=torch.int64, device=device)
+        r["ip_sets"] = alloc("ip_sets", (nw, 4), torch.int64)
         v.ip_sets = r["ip_sets"].data_ptr()
     if n == 0:
         return r
