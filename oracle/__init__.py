@@ -14,6 +14,8 @@ Three procedures, each citing PAPER.md (= /root/reference/PAPER.md, arXiv 2509.0
   from source :185, source fan-out :187, their destination mirrors :173) and the four globally
   unique IP set counts (:209) per window, from the same ``std::map`` definition (oracle.cpp);
   ``window_distributions_dense`` is its dense O0 counterpart (dense.py).
+* ``window_stats_weighted`` — O1w, O1 on weighted rows (src, dst, n_packets): the paper's three-column
+  frame (:207; valid packets = sum of n_packets, :180); rows of weight 0 add nothing.
 * ``window_stats_dense`` — O0, the "Matrix notation" column evaluated literally on a dense
   matrix after relabelling the (few) addresses of a tiny window (dense.py).
 
@@ -62,6 +64,10 @@ def _load():
                 f.restype = ctypes.c_int
                 f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
                               ctypes.c_void_p, ctypes.c_int]
+            f = lib.nsg_oracle_window_stats_weighted
+            f.restype = ctypes.c_int
+            f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64,
+                          ctypes.c_void_p, ctypes.c_int]
             f = lib.nsg_oracle_window_distributions
             f.restype = ctypes.c_int
             f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64] + \
@@ -166,4 +172,25 @@ def window_slices(r: dict, window: int, w: int) -> dict:
     for k in ("dst_node", "dst_packets", "dst_fan"):
         out[k] = r[k][b:b + nd]
     out["ip_sets"] = r["ip_sets"][w]
+    return out
+
+
+def window_stats_weighted(src=None, dst=None, weights=None, window: int = 1 << 17, *, keys=None,
+                          threads: int = 0) -> np.ndarray:
+    """O1w: Table 2 on weighted rows, A_t(i,j) = sum of the weights of the window's rows i -> j.
+    `weights` u32 [n].  Returns uint64 [n_windows, 9]."""
+    s, d = _split(src, dst, keys)
+    w8 = _u32(weights)
+    if s.shape != d.shape or w8.shape != s.shape:
+        raise ValueError("src, dst and weights must have the same length")
+    n = int(s.shape[0])
+    if window < 1:
+        raise ValueError("window must be >= 1")
+    nw = 0 if n == 0 else (n + window - 1) // window
+    out = np.zeros((nw, NUM_STATS), dtype=np.uint64)
+    if n:
+        rc = _load().nsg_oracle_window_stats_weighted(s.ctypes.data, d.ctypes.data, w8.ctypes.data, n, int(window),
+                                                      out.ctypes.data, int(threads))
+        if rc != 0:
+            raise ValueError(f"nsg_oracle_window_stats_weighted returned {rc}")
     return out

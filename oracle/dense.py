@@ -22,7 +22,7 @@ from __future__ import annotations
 import numpy as np
 
 
-def _one_window(s: np.ndarray, d: np.ndarray, max_vertices: int) -> list[int]:
+def _one_window(s: np.ndarray, d: np.ndarray, max_vertices: int, wt=None) -> list[int]:
     if s.size == 0:
         return [0] * 9
     labels, inv = np.unique(np.concatenate([s, d]), return_inverse=True)
@@ -31,7 +31,9 @@ def _one_window(s: np.ndarray, d: np.ndarray, max_vertices: int) -> list[int]:
         raise ValueError(f"dense oracle is for tiny windows (V={V} > {max_vertices})")
     i, j = inv[: s.size], inv[s.size:]
     A = np.zeros((V, V), dtype=np.int64)
-    np.add.at(A, (i, j), 1)                      # A_t(i,j) = packets i -> j
+    np.add.at(A, (i, j), 1 if wt is None else wt)   # A_t(i,j) = packets (or summed n_packets) i -> j
+    if not A.any():
+        return [0] * 9
     nz = (A != 0).astype(np.int64)               # |A_t|_0
     row_sum, col_sum = A.sum(axis=1), A.sum(axis=0)          # A_t 1, 1^T A_t
     row_nnz, col_nnz = nz.sum(axis=1), nz.sum(axis=0)        # |A_t|_0 1, 1^T |A_t|_0
@@ -48,10 +50,12 @@ def _one_window(s: np.ndarray, d: np.ndarray, max_vertices: int) -> list[int]:
     ]
 
 
-def window_stats_dense(src, dst, window: int, *, max_vertices: int = 256) -> np.ndarray:
-    """O0 over every window of (src, dst).  Returns uint64 [n_windows, 9]."""
+def window_stats_dense(src, dst, window: int, *, max_vertices: int = 256, weights=None) -> np.ndarray:
+    """O0 over every window of (src, dst) (optionally weighted rows: A_t sums the weights, PAPER.md:180,
+    :207).  Returns uint64 [n_windows, 9]."""
     s = np.asarray(src, dtype=np.int64).ravel()
     d = np.asarray(dst, dtype=np.int64).ravel()
+    wt = None if weights is None else np.asarray(weights, dtype=np.int64).ravel()
     if s.shape != d.shape:
         raise ValueError("src and dst must have the same length")
     if window < 1:
@@ -60,7 +64,8 @@ def window_stats_dense(src, dst, window: int, *, max_vertices: int = 256) -> np.
     nw = 0 if n == 0 else (n + window - 1) // window
     out = np.zeros((nw, 9), dtype=np.uint64)
     for w in range(nw):
-        out[w] = _one_window(s[w * window:(w + 1) * window], d[w * window:(w + 1) * window], max_vertices)
+        sl = slice(w * window, (w + 1) * window)
+        out[w] = _one_window(s[sl], d[sl], max_vertices, None if wt is None else wt[sl])
     return out
 
 

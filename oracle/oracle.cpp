@@ -34,6 +34,8 @@
 //   O2 (nsg_oracle_window_stats_sort): the same definition reached through a library sort
 //      (std::sort) and run-length scans; a thread pool over windows.  Windows are
 //      independent, so the thread count cannot change any result.
+//   O1w (nsg_oracle_window_stats_weighted): O1 on weighted rows (src, dst, n_packets), the paper's
+//      three-column frame; SURVEY §8(f) row f4a.
 //   O1d (nsg_oracle_window_distributions): the vector-valued rows of Table 2 (link packets,
 //      row sums / nnz and their column mirrors) and the four globally-unique-IP set counts, from
 //      the same std::map definition.
@@ -139,6 +141,44 @@ void window_sort(const uint32_t* src, const uint32_t* dst, uint64_t len, uint64_
   if (d.total != s.total || d.distinct_pairs != s.distinct_pairs || d.max_pair != s.max_pair) out[0] = ~0ull;
 }
 
+// ---- O1w: weighted (aggregated) input rows ----------------------------
+// The paper's frame has three columns src, dst, n_packets and sums n_packets for the valid
+// packets.  With row p carrying weight n_p, A_t(i,j) = sum of n_p over the window's rows with
+// src = i, dst = j; a link is a nonzero of A_t (|A_t|_0), so a row of weight 0 adds nothing
+// (reading R14).  Everything else is Table 2 on this A_t, as O1.  Raw packets are the
+// special case n_p = 1 (reading R2); SPEC S:142 states the raw / aggregated equivalence.
+void window_map_weighted(const uint32_t* src, const uint32_t* dst, const uint32_t* wgt, uint64_t len, uint64_t* out) {
+  std::map<std::pair<uint32_t, uint32_t>, uint64_t> A;
+  for (uint64_t p = 0; p < len; ++p)
+    if (wgt[p] != 0) A[{src[p], dst[p]}] += wgt[p];
+  uint64_t valid = 0, max_link = 0;
+  for (const auto& e : A) {
+    valid += e.second;
+    max_link = std::max(max_link, e.second);
+  }
+  std::map<uint32_t, uint64_t> row_sum, row_nnz, col_sum, col_nnz;
+  for (const auto& e : A) {
+    row_sum[e.first.first] += e.second;
+    row_nnz[e.first.first] += 1;
+    col_sum[e.first.second] += e.second;
+    col_nnz[e.first.second] += 1;
+  }
+  auto max_of = [](const std::map<uint32_t, uint64_t>& m) {
+    uint64_t r = 0;
+    for (const auto& e : m) r = std::max(r, e.second);
+    return r;
+  };
+  out[0] = valid;             // P:180 df['n_packets'].sum()
+  out[1] = A.size();
+  out[2] = max_link;
+  out[3] = row_sum.size();
+  out[4] = max_of(row_sum);
+  out[5] = max_of(row_nnz);
+  out[6] = col_sum.size();    // mirrors
+  out[7] = max_of(col_sum);
+  out[8] = max_of(col_nnz);
+}
+
 // ---- O1d: the vector-valued rows of Table 2 and the globally unique IPs ----
 // For window w, literally from the definition, in the same std::map form as O1:
 //   links       the nonzeros of A_t: (key = i<<32 | j, A_t(i,j))    P:182 "Link packets from i to j"
@@ -233,6 +273,28 @@ int nsg_oracle_window_stats_map(const uint32_t* src, const uint32_t* dst, uint64
 int nsg_oracle_window_stats_sort(const uint32_t* src, const uint32_t* dst, uint64_t n, uint64_t window,
                                  uint64_t* out, int n_threads) {
   return run_windows(window_sort, src, dst, n, window, out, n_threads);
+}
+
+// Weighted rows: wgt[n] u32 weights (n_packets).  Returns 0 on success, 1 on invalid arguments.
+int nsg_oracle_window_stats_weighted(const uint32_t* src, const uint32_t* dst, const uint32_t* wgt, uint64_t n,
+                                     uint64_t window, uint64_t* out, int n_threads) {
+  if (window == 0) return 1;
+  if (n == 0) return 0;
+  if (!src || !dst || !wgt || !out) return 1;
+  const uint64_t nw = num_windows(n, window);
+  unsigned T = n_threads > 0 ? unsigned(n_threads) : std::max(1u, std::thread::hardware_concurrency());
+  if (T > nw) T = unsigned(nw);
+  auto worker = [&](unsigned t) {
+    for (uint64_t w = t; w < nw; w += T) {
+      const uint64_t b = w * window;
+      window_map_weighted(src + b, dst + b, wgt + b, std::min(window, n - b), out + w * kStats);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (unsigned t = 1; t < T; ++t) pool.emplace_back(worker, t);
+  worker(0);
+  for (auto& th : pool) th.join();
+  return 0;
 }
 
 // Returns 0 on success, 1 on invalid arguments.  Every vector array is host [n] (window w's entries at

@@ -70,3 +70,31 @@ def load_golden_dist(name):
                 cur[mode].append([int(x) for x in line.split()])
     flush()
     return cases
+
+
+def load_golden_weighted(name):
+    """Parse a weighted-rows fixture into [(window, src, dst, weights, expected_rows)]."""
+    cases, cur, mode = [], None, None
+
+    def flush():
+        if cur is not None:
+            cases.append((cur["window"], np.array(cur["s"], np.uint32), np.array(cur["d"], np.uint32),
+                          np.array(cur["w"], np.uint32), np.array(cur["e"], np.uint64)))
+
+    with open(os.path.join(GOLDEN, name)) as f:
+        for raw in f:
+            line = raw.split("#", 1)[0].strip()
+            if not line:
+                continue
+            if line.startswith("window"):
+                flush()
+                cur = {"window": int(line.split()[1]), "s": [], "d": [], "w": [], "e": []}
+            elif line in ("rows", "expect"):
+                mode = line
+            elif mode == "rows":
+                a, b, c = line.split()
+                cur["s"].append(int(a)); cur["d"].append(int(b)); cur["w"].append(int(c))
+            else:
+                cur["e"].append([int(x) for x in line.split()])
+    flush()
+    return cases

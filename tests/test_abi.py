@@ -38,7 +38,8 @@ def test_binding_export_list_matches_header():
 
 def test_no_oracle_or_gen_symbols_in_libnsg():
     lib = ctypes.CDLL(LIB)
-    for name in ("nsg_oracle_window_stats_map", "nsg_oracle_window_stats_sort", "nsg_gen_host", "nsg_gen_device"):
+    for name in ("nsg_oracle_window_stats_map", "nsg_oracle_window_stats_sort", "nsg_oracle_window_stats_weighted",
+                 "nsg_oracle_window_distributions", "nsg_gen_host", "nsg_gen_device"):
         assert not hasattr(lib, name)
 
 
