@@ -188,6 +188,9 @@ def main():
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--once", action="store_true", help="a single untimed call (for ncu)")
+    ap.add_argument("--input", choices=["packets", "weighted"], default="packets",
+                    help="packets: raw packets (north_star); weighted: rows (src, dst, n_packets) with n_packets "
+                         "uniform in [1, 8] (nsg_window_stats_weighted, SURVEY §8(f) f4a); unit = rows/s")
     ap.add_argument("--outputs", choices=["stats", "vectors"], default="stats",
                     help="stats: the nine statistics (north_star); vectors: + per-window link / source / "
                          "destination vectors and IP set counts (nsg_window_vectors, SURVEY §8(f) f1, f3)")
@@ -231,6 +234,14 @@ def main():
     ws = nsg.Workspace(n, WINDOW, dev)
     outs = [torch.empty((WINDOWS_PER_STEP, 9), dtype=torch.int64, device=dev) for _ in range(RING)]
     vec = args.outputs == "vectors"
+    wtd = args.input == "weighted"
+    if wtd and vec:
+        raise SystemExit("--input weighted supports --outputs stats only")
+    wring = None
+    if wtd:  # n_packets per row, seeded, uniform in [1, 8]
+        gw = torch.Generator(device=dev)
+        gw.manual_seed(1000 + seed + rank)
+        wring = torch.randint(1, 9, (RING, n), generator=gw, device=dev, dtype=torch.int32)
     vbuf = nsg.window_vectors(ring[0], WINDOW, out=outs[0], workspace=ws) if vec else None
     if args.once:
         if vec:
@@ -245,6 +256,12 @@ def main():
             if evs:
                 evs[0].record()
             r = nsg.window_vectors(ring[i % RING], WINDOW, out=outs[i % RING], workspace=ws, buffers=vbuf)["stats"]
+            if evs:
+                evs[1].record()
+        elif wtd:  # events around the whole call (workspace reset + persistent kernel + overflow check)
+            if evs:
+                evs[0].record()
+            r = nsg.window_stats_weighted(ring[i % RING], wring[i % RING], WINDOW, out=outs[i % RING], workspace=ws)
             if evs:
                 evs[1].record()
         else:
@@ -304,6 +321,16 @@ def main():
             for k, t in vhost.items():
                 t.copy_(r[k], non_blocking=True)
         d2h_bytes = WINDOWS_PER_STEP * 9 * 8 + sum(t.numel() * t.element_size() for t in vhost.values())
+    elif wtd:  # H2D of the rows (keys + n_packets), the call, D2H of the statistics
+        whost = wring[0].cpu().pin_memory()
+        wdev = torch.empty(n, dtype=torch.int32, device=dev)
+
+        def e2e_once():
+            keys_dev.copy_(host, non_blocking=True)
+            wdev.copy_(whost, non_blocking=True)
+            r = nsg.window_stats_weighted(keys_dev, wdev, WINDOW, out=outs[0], workspace=ws)
+            out_host.copy_(r, non_blocking=True)
+        d2h_bytes = WINDOWS_PER_STEP * 9 * 8
     else:
         def e2e_once():
             nsg.window_stats_from_host(host, WINDOW, device=dev, keys_dev=keys_dev, out=outs[0], out_host=out_host,
@@ -329,7 +356,7 @@ def main():
 
     if rank == 0:
         peak, peak_src = peaks()
-        alg_bytes = n * BYTES_PER_PACKET + WINDOWS_PER_STEP * BYTES_PER_WINDOW_OUT
+        alg_bytes = n * (BYTES_PER_PACKET + (4 if wtd else 0)) + WINDOWS_PER_STEP * BYTES_PER_WINDOW_OUT
         if vec:  # + the vectors written: 12 B per link / source / destination, 32 B of IP sets per window
             cnt = outs[0][:, [1, 3, 6]].sum().item()
             alg_bytes += 12 * cnt + 32 * WINDOWS_PER_STEP
@@ -342,16 +369,17 @@ def main():
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": desc + f"; {WINDOWS_PER_STEP} windows x 2^17 packets per GPU per step (C2 batch)"
-                       + ("; outputs: stats + link/source/destination vectors + IP sets" if vec else ""),
+                       + ("; outputs: stats + link/source/destination vectors + IP sets" if vec else "")
+                       + ("; weighted rows (src, dst, n_packets ~ U[1,8]), unit rows/s" if wtd else ""),
                        "window": WINDOW, "packets_per_gpu_per_step": n, "parallelism": f"windows sharded dp{world}",
                        "l2": f"inputs larger than L2: ring of {RING} x {n * 8 >> 20} MiB batches per GPU, no flush",
                        "input": "device-resident packed u64 keys (src<<32|dst)"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 8,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * (12 if wtd else 8),
                     "d2h_bytes_per_step": d2h_bytes, "steps": e2e_steps},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic_per_launch(args.workload + ("-vectors" if vec else "")), "peak_source": peak_src,
+                         "traffic": traffic_per_launch(args.workload + ("-vectors" if vec else "-weighted" if wtd else "")), "peak_source": peak_src,
                          "kernel": "nsg::fast_kernel" + (" (+ reset and overflow-check launches: events around "
-                                                          "the whole nsg_window_vectors call)" if vec else ""),
+                                                          "the whole call)" if (vec or wtd) else ""),
                          "kernel_ms_avg": k_avg,
                          "algorithmic_bytes_per_launch": alg_bytes},
             "cpu_baseline": cpu,

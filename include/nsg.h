@@ -135,6 +135,20 @@ nsg_status nsg_window_stats_from_host(const uint64_t* keys_host, uint64_t n_pack
                                       uint64_t* keys_dev, uint64_t* out, uint64_t* out_host, void* workspace,
                                       size_t workspace_bytes, void* stream, void* copy_stream, uint32_t chunk_windows);
 
+/* Weighted rows: the paper's three-column frame src, dst, n_packets
+ * (PAPER.md:207).  Row p adds its weight n_packets[p] to A_t(src_p, dst_p), so valid packets is the sum
+ * of n_packets and a link is a nonzero of A_t: a row of weight 0 adds
+ * nothing (R14).  Windows are cut by ROW index (window w = rows [w*window, ...)).  Raw packets
+ * are the case n_packets = 1 (nsg_window_stats*).
+ *   n_packets  device u32[n_rows], 4 B aligned; the input rows as for nsg_window_stats_ex (exactly one
+ *              of keys / (src, dst)).
+ * Per window the weights must sum to < 2^32 (32-bit device counters); a window that does not is counted
+ * in diag[2] (nsg_diag_offset) and its row is unspecified.  Same workspace size, conventions and errors
+ * as nsg_window_stats_ex, plus NSG_ERR_INVALID_ARGUMENT for a NULL or misaligned n_packets. */
+nsg_status nsg_window_stats_weighted(const uint32_t* src, const uint32_t* dst, const uint64_t* keys,
+                                     const uint32_t* n_packets, uint64_t n_rows, uint64_t window, uint64_t* out,
+                                     void* workspace, size_t workspace_bytes, void* stream, uint32_t flags);
+
 /* Optional per-window vector outputs of nsg_window_vectors.
  *   links        the nonzeros of A_t: key (src<<32 | dst) and A_t(src,dst)
  *                ("Link packets from i to j")
@@ -172,8 +186,8 @@ nsg_status nsg_window_vectors(const uint32_t* src, const uint32_t* dst, const ui
 /* Diagnostics of the last call that used `workspace` (device memory; read it after the stream has
  * completed the call): byte offset inside the workspace of a u32[4] =
  *   {windows the fast path handed to the L2 path because an SMEM table would overflow,
- *    windows whose self-check failed (sum of link counts != window length; 0 unless there is a bug),
- *    reserved, reserved}. */
+ *    windows whose self-check failed (sum of link counts != window length, or != the sum of n_packets;
+ *    0 unless there is a bug), weighted windows whose n_packets sum to >= 2^32 (unsupported), reserved}. */
 size_t nsg_diag_offset(void);
 
 /* Number of kernels the calling host thread's most recent nsg_window_stats* call launched. */

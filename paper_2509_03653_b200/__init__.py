@@ -25,6 +25,7 @@ from .api import (  # noqa: F401
     window_stats,
     window_stats_from_host,
     window_stats_packed,
+    window_stats_weighted,
     window_vectors,
     workspace_bytes,
 )

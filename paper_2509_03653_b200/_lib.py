@@ -27,6 +27,7 @@ EXPORTS = (
     "nsg_window_stats_timed",
     "nsg_window_stats_from_host",
     "nsg_window_vectors",
+    "nsg_window_stats_weighted",
     "nsg_diag_offset",
     "nsg_last_launches",
     "nsg_status_string",
@@ -92,6 +93,8 @@ def load() -> ctypes.CDLL:
     lib.nsg_window_stats_from_host.argtypes = [vp, u64, u64, vp, vp, vp, vp, sz, vp, vp, u32]
     lib.nsg_window_vectors.restype = ctypes.c_int
     lib.nsg_window_vectors.argtypes = [vp, vp, vp, u64, u64, vp, ctypes.POINTER(NsgVectors), vp, sz, vp, u32]
+    lib.nsg_window_stats_weighted.restype = ctypes.c_int
+    lib.nsg_window_stats_weighted.argtypes = [vp, vp, vp, vp, u64, u64, vp, vp, sz, vp, u32]
     lib.nsg_diag_offset.restype = sz
     lib.nsg_diag_offset.argtypes = []
     lib.nsg_last_launches.restype = ctypes.c_uint

@@ -298,3 +298,47 @@ def window_vectors(keys: Optional[torch.Tensor] = None, window: int = DEFAULT_WI
     if rc != 0:
         raise NsgError(rc, "nsg_window_vectors")
     return r
+
+
+def window_stats_weighted(keys: Optional[torch.Tensor] = None, n_packets: Optional[torch.Tensor] = None,
+                          window: int = DEFAULT_WINDOW, *, src=None, dst=None, out=None,
+                          workspace: Optional[Workspace] = None, stream=None, flags: int = 0) -> torch.Tensor:
+    """Nine quantities per window of WEIGHTED rows (src, dst, n_packets): the paper's three-column frame
+    (PAPER.md:207; valid packets = sum of n_packets, :180).  Rows are packed `keys`
+    (device int64/uint64) or SoA `src`, `dst` (device int32/uint32); `n_packets` device int32/uint32 (u32
+    bit patterns).  Windows are cut by row index; a row of weight 0 adds nothing.  Returns a device int64
+    tensor [n_windows, 9] (nsg_window_stats_weighted).
+    """
+    if keys is not None:
+        if src is not None or dst is not None:
+            raise ValueError("pass either keys or (src, dst)")
+        _check(keys, "keys", _U64_TYPES)
+        n, device = keys.numel(), keys.device
+    else:
+        _check(src, "src", _U32_TYPES)
+        _check(dst, "dst", _U32_TYPES)
+        if src.numel() != dst.numel() or src.device != dst.device:
+            raise ValueError("src and dst must have the same length and device")
+        n, device = src.numel(), src.device
+    _check(n_packets, "n_packets", _U32_TYPES)
+    if n_packets.numel() != n or n_packets.device != device:
+        raise ValueError("n_packets must have one entry per row, on the rows' device")
+    window = int(window)
+    if window < 1 or window > MAX_WINDOW:
+        raise ValueError(f"window must be in [1, 2^31], got {window}")
+    nw = num_windows(n, window)
+    if out is None:
+        out = torch.empty((nw, NUM_STATS), dtype=torch.int64, device=device)
+    elif out.dtype not in _U64_TYPES or not out.is_contiguous() or out.numel() < nw * NUM_STATS or not out.is_cuda:
+        raise ValueError("out must be a contiguous CUDA int64/uint64 tensor with >= n_windows*9 elements")
+    if n == 0:
+        return out
+    ws = _workspace(n, window, device, workspace)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_window_stats_weighted(
+        None if src is None else src.data_ptr(), None if dst is None else dst.data_ptr(),
+        None if keys is None else keys.data_ptr(), n_packets.data_ptr(), n, window, out.data_ptr(), ws.ptr,
+        ws.nbytes, ctypes.c_void_p(s.cuda_stream), int(flags))
+    if rc != 0:
+        raise NsgError(rc, "nsg_window_stats_weighted")
+    return out

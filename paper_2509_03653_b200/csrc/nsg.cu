@@ -43,7 +43,7 @@ struct Layout {
   u64 nw;
   // fast
   u32 logB, B, logB2, B2, cp, cp_last, R;
-  size_t o_pw, o_s0win, o_kscr, o_koff, o_rscr, o_roff, o_rend, o_lres, o_sres, o_s0list;
+  size_t o_pw, o_s0win, o_kscr, o_koff, o_rscr, o_roff, o_rend, o_lres, o_sres, o_s0list, o_wscr;
   size_t memset_bytes;
   // global
   u64 LC;
@@ -87,6 +87,7 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     L.o_lres = o; o = align256(o + (size_t)L.R * L.B * 4 * sizeof(u32));
     L.o_sres = o; o = align256(o + (size_t)L.R * 2 * L.B2 * 4 * sizeof(u32));
     L.o_s0list = o; o = align256(o + (size_t)L.R * L.B2 * TCAP_S * sizeof(u32));
+    L.o_wscr = o; o = align256(o + (size_t)L.R * L.cp * CH * sizeof(u32));
   }
   // L2-path table sets: the full path for large windows, the overflow hand-off otherwise.
   L.LC = next_pow2(2 * W);
@@ -110,7 +111,8 @@ struct DevInfo {
   bool init = false;
   bool supported = false;
   int sms = 0;
-  int fast_blocks = 0;  // co-resident fast_kernel CTAs
+  int fast_blocks = 0;    // co-resident fast_kernel<false> CTAs
+  int fast_blocks_w = 0;  // co-resident fast_kernel<true> CTAs (weighted rows)
 };
 static std::mutex g_mu;
 static DevInfo g_dev[64];
@@ -129,13 +131,16 @@ static nsg_status dev_info(DevInfo& out) {
     if (cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return NSG_ERR_CUDA;
     d.supported = (major == 10 && minor == 0);
     if (d.supported) {
-      if (cudaFuncSetAttribute(fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FAST_SMEM) != cudaSuccess)
+      if (cudaFuncSetAttribute(fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FAST_SMEM) != cudaSuccess ||
+          cudaFuncSetAttribute(fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FAST_SMEM) != cudaSuccess)
         return NSG_ERR_CUDA;
-      int per_sm = 0;
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast_kernel, FT, FAST_SMEM) != cudaSuccess)
+      int per_sm = 0, per_sm_w = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast_kernel<false>, FT, FAST_SMEM) != cudaSuccess ||
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, fast_kernel<true>, FT, FAST_SMEM) != cudaSuccess)
         return NSG_ERR_CUDA;
-      if (per_sm < 1) return NSG_ERR_UNSUPPORTED_DEVICE;
+      if (per_sm < 1 || per_sm_w < 1) return NSG_ERR_UNSUPPORTED_DEVICE;
       d.fast_blocks = per_sm * d.sms;
+      d.fast_blocks_w = per_sm_w * d.sms;
     }
     d.init = true;
   }
@@ -176,7 +181,7 @@ static WriteValue32Fn write_value32() {
 
 static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u64 W, u64* out, void* ws,
                       size_t ws_bytes, void* stream, u32 flags, void* ev_before = nullptr, void* ev_after = nullptr,
-                      const StreamIn* sin = nullptr, const nsg_vectors* vec = nullptr) {
+                      const StreamIn* sin = nullptr, const nsg_vectors* vec = nullptr, const u32* wgt = nullptr) {
   g_last_launches = 0;
   if (W == 0 || W > NSG_MAX_WINDOW) return NSG_ERR_INVALID_ARGUMENT;
   if (n == 0) return NSG_OK;
@@ -185,6 +190,7 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
   if (!out || !ws) return NSG_ERR_INVALID_ARGUMENT;
   if ((reinterpret_cast<uintptr_t>(ws) & 255) || (reinterpret_cast<uintptr_t>(out) & 7)) return NSG_ERR_INVALID_ARGUMENT;
   if (keys && (reinterpret_cast<uintptr_t>(keys) & 7)) return NSG_ERR_INVALID_ARGUMENT;
+  if (wgt && (reinterpret_cast<uintptr_t>(wgt) & 3)) return NSG_ERR_INVALID_ARGUMENT;
   nsg_vectors V;
   memset(&V, 0, sizeof(V));
   if (vec) {
@@ -251,6 +257,7 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
   gg.v_node[0] = V.src_node; gg.v_pk[0] = V.src_packets; gg.v_fan[0] = V.src_fanout;
   gg.v_node[1] = V.dst_node; gg.v_pk[1] = V.dst_packets; gg.v_fan[1] = V.dst_fanin;
   gg.v_ipsets = reinterpret_cast<u64*>(V.ip_sets);
+  gg.wgt = wgt;
 
   const bool use_fast = L.fast && !(flags & NSG_FLAG_FORCE_GLOBAL);
   if (use_fast) {
@@ -278,6 +285,8 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
     g.s0win = reinterpret_cast<u32*>(base + L.o_s0win);
     g.s0cnt = g.s0win + (size_t)L.R * L.B2;
     g.s0list = reinterpret_cast<u32*>(base + L.o_s0list);
+    g.wgt = wgt;
+    g.wscr = reinterpret_cast<u32*>(base + L.o_wscr);
     {  // ticket regions (see Geo): breakpoints where an item class enters or leaves the schedule
       u64 pts[8] = {0, (u64)LAG_L, (u64)LAG_S, (u64)LAG_F, L.nw, L.nw + LAG_L, L.nw + LAG_S, L.nw + LAG_F};
       std::sort(pts, pts + 8);
@@ -316,10 +325,11 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
       g.reg_t0[g.nreg] = t;
       g.total_items = t;
     }
-    u64 grid = (u64)d.fast_blocks;
+    u64 grid = (u64)(wgt ? d.fast_blocks_w : d.fast_blocks);
     if (grid > g.total_items) grid = g.total_items;
     if (ev_before && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_before), s) != cudaSuccess) return NSG_ERR_CUDA;
-    fast_kernel<<<(unsigned)grid, FT, FAST_SMEM, s>>>(g, src, dst, keys, out);
+    if (wgt) fast_kernel<true><<<(unsigned)grid, FT, FAST_SMEM, s>>>(g, src, dst, keys, out);
+    else fast_kernel<false><<<(unsigned)grid, FT, FAST_SMEM, s>>>(g, src, dst, keys, out);
     g_last_launches++;
     if (cudaGetLastError() != cudaSuccess) return NSG_ERR_CUDA;
     if (ev_after && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_after), s) != cudaSuccess) return NSG_ERR_CUDA;
@@ -415,6 +425,14 @@ nsg_status nsg_window_vectors(const uint32_t* src, const uint32_t* dst, const ui
   return nsg::run(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_packets, window,
                   reinterpret_cast<nsg::u64*>(out), workspace, workspace_bytes, stream, flags, nullptr, nullptr,
                   nullptr, vectors);
+}
+
+nsg_status nsg_window_stats_weighted(const uint32_t* src, const uint32_t* dst, const uint64_t* keys,
+                                     const uint32_t* n_packets, uint64_t n_rows, uint64_t window, uint64_t* out,
+                                     void* workspace, size_t workspace_bytes, void* stream, uint32_t flags) {
+  if (n_rows && !n_packets) return NSG_ERR_INVALID_ARGUMENT;
+  return nsg::run(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_rows, window, reinterpret_cast<nsg::u64*>(out),
+                  workspace, workspace_bytes, stream, flags, nullptr, nullptr, nullptr, nullptr, n_packets);
 }
 
 size_t nsg_diag_offset(void) { return nsg::DIAG_OFFSET; }

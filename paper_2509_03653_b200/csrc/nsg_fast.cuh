@@ -116,9 +116,12 @@ struct Geo {
   u32* s0list;  // [R][B2][TCAP_S] node list of each side-0 item (read by the side-1 item of the bucket)
   u32* s0cnt;   // [R][B2]
   u32* s0win;   // [R][B2]         w+1 once side item S0(w, sb) has published its list (release)
+  // Weighted rows (nsg_window_stats_weighted): n_packets per row, or NULL.
+  const u32* wgt;
+  u32* wscr;    // [R][cp*CH]      the weights, laid out like kscr
 };
 
-struct SmemP { u64 stage[CH]; u32 hist[MAXB + 1]; };
+struct SmemP { u64 stage[CH]; u32 hist[MAXB + 1]; u32 stagew[CH]; };  // stagew: weighted rows only
 // Per-warp gather tables: warp w gathers segments w, w + NWARP, ... (chunks for L, link buckets for S).
 constexpr int WSEG_L = (MAXCP + NWARP - 1) / NWARP;
 constexpr int WSEG_S = (MAXB + NWARP - 1) / NWARP;
@@ -126,6 +129,14 @@ static_assert(WSEG_L <= 32 && WSEG_S <= 32, "one segment per lane");
 // Pending lists are SoA: a = the key (link item) or node<<32 | F<<20 | P (side item), p = next probe.
 struct SmemL {
   u64 lkey[TCAP]; u32 lcnt[TCAP]; u64 pa[2][PCAP]; u16 pp[2][PCAP]; u32 wlo[NWARP][WSEG_L]; u32 wpre[NWARP][WSEG_L + 1];
+  u32 hist[2 * MAXB2 + 1];
+};
+// The weighted-rows link item carries a weight per pending entry; its pending lists are half as long so
+// that the CTA still fits two per SM.
+constexpr int PCAP_W = NSG_PCAP / 2;
+struct SmemLW {
+  u64 lkey[TCAP]; u32 lcnt[TCAP]; u64 pa[2][PCAP_W]; u16 pp[2][PCAP_W]; u32 pw[2][PCAP_W]; u32 wlo[NWARP][WSEG_L];
+  u32 wpre[NWARP][WSEG_L + 1];
   u32 hist[2 * MAXB2 + 1];
 };
 struct SmemS {
@@ -142,10 +153,11 @@ struct SmemMisc {
   u32 vbase, vcnt;  // vector outputs: the item's base inside its window's region, its fill counter
   u32 n0, both;     // side-1 item with IP sets: entries in S0's node list, nodes found on both sides
   u64 w;
+  unsigned long long wsum;  // weighted link item: sum of the bucket's weights
 };
 constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
 constexpr size_t MISC_BYTES = (sizeof(SmemMisc) + 15) & ~size_t(15);
-constexpr size_t FAST_SMEM = MISC_BYTES + cmax(sizeof(SmemP), cmax(sizeof(SmemL), sizeof(SmemS)));
+constexpr size_t FAST_SMEM = MISC_BYTES + cmax(cmax(sizeof(SmemP), sizeof(SmemLW)), cmax(sizeof(SmemL), sizeof(SmemS)));
 
 // ------------------------------------------------------------------------------------------
 // Block helpers
@@ -284,7 +296,8 @@ __device__ __noinline__ bool node_flush(u32* key, u32* P, u32* F, u32* esc, u32 
 
 // Warp-aggregated append of the lanes with `want` to pending list `list`; must be called by all
 // lanes of the warp.  Returns false for a lane whose entry did not fit (the caller finishes it).
-__device__ __forceinline__ bool pend_push(u64* la, u16* lp, u32* cnt, bool want, u64 a, u32 probe, u32 cap) {
+__device__ __forceinline__ bool pend_push(u64* la, u16* lp, u32* cnt, bool want, u64 a, u32 probe, u32 cap,
+                                          u32* lw = nullptr, u32 wt = 0) {
   const u32 mask = __ballot_sync(0xffffffffu, want);
   if (mask == 0) return true;
   const int lane = threadIdx.x & 31, leader = __ffs(mask) - 1;
@@ -296,6 +309,7 @@ __device__ __forceinline__ bool pend_push(u64* la, u16* lp, u32* cnt, bool want,
   if (pos >= cap) return false;
   la[pos] = a;
   lp[pos] = (u16)probe;
+  if (lw) lw[pos] = wt;
   return true;
 }
 
@@ -370,6 +384,7 @@ struct Claim {
   }
 };
 
+template <bool WT>
 __device__ void item_partition(const Geo& g, const u32* __restrict__ src, const u32* __restrict__ dst,
                                const u64* __restrict__ keys, u64 w, u32 c, SmemP& s, SmemMisc& m, Claim& cl) {
   const int t = threadIdx.x;
@@ -434,12 +449,31 @@ __device__ void item_partition(const Geo& g, const u32* __restrict__ src, const 
         k[j] = (t + j * FT < (int)len) ? (((u64)__ldcs(ps + t + j * FT) << 32) | __ldcs(pd + t + j * FT)) : 0ull;
     }
   }
+  // Weighted rows: the weight of each element (same element order as the key loads above); a row of
+  // weight 0 is not an element (it adds nothing to A_t, R14).
+  u32 wv[KPT];
+  bool el[KPT];
+  if constexpr (WT) {
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) el[j] = full || t + j * FT < (int)len;
+    const bool v2 = full && keys && ((reinterpret_cast<uintptr_t>(keys + base) & 15) == 0);
+    const bool v4 = full && !keys && ((reinterpret_cast<uintptr_t>(src + base) & 15) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(dst + base) & 15) == 0);
+    const u32* pw = g.wgt + base;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const int e = v2 ? 2 * (t + (j >> 1) * FT) + (j & 1) : v4 ? 4 * (t + (j >> 2) * FT) + (j & 3) : t + j * FT;
+      wv[j] = el[j] ? __ldcs(pw + e) : 0u;
+      el[j] = el[j] && wv[j] != 0u;
+    }
+  }
   if (t == 0 && w >= g.R) waited = wait_geq(&g.fin[w - g.R], 1u, dep);
   __syncthreads();  // hist cleared; thread 0's wait for the slot is published
   pt.mark(g, 0, 0);
+#define NSG_ELEMENT(j) (WT ? el[j] : (full || t + (j) * FT < (int)len))
 #pragma unroll
   for (int j = 0; j < KPT; ++j)
-    if (full || t + j * FT < (int)len) atomicAdd(&s.hist[link_bucket(k[j], g.logB)], 1u);
+    if (NSG_ELEMENT(j)) atomicAdd(&s.hist[link_bucket(k[j], g.logB)], 1u);
   __syncthreads();
   pt.mark(g, 0, 1);
   warp0_exclusive_scan(s.hist, (int)g.B);  // warp 0 scans and publishes the chunk's bucket offsets
@@ -453,11 +487,13 @@ __device__ void item_partition(const Geo& g, const u32* __restrict__ src, const 
   cl.now(g);
 #pragma unroll
   for (int j = 0; j < KPT; ++j) {
-    if (full || t + j * FT < (int)len) {
+    if (NSG_ELEMENT(j)) {
       const u32 pos = atomicAdd(&s.hist[link_bucket(k[j], g.logB)], 1u);
       s.stage[pos] = k[j];
+      if constexpr (WT) s.stagew[pos] = wv[j];
     }
   }
+#undef NSG_ELEMENT
   __syncthreads();
   pt.mark(g, 0, 3);
   u64* out = g.kscr + (u64)slot * g.cp * CH + (u64)c * CH;
@@ -468,6 +504,10 @@ __device__ void item_partition(const Geo& g, const u32* __restrict__ src, const 
     for (int i = t; i < CH / 2; i += FT) o2[i] = s2[i];
   } else {
     for (u32 i = t; i < len; i += FT) out[i] = s.stage[i];
+  }
+  if constexpr (WT) {
+    u32* ow = g.wscr + (u64)slot * g.cp * CH + (u64)c * CH;
+    for (u32 i = t; i < len; i += FT) ow[i] = s.stagew[i];
   }
   __syncthreads();
   pt.mark(g, 0, 4);
@@ -528,7 +568,9 @@ __device__ __forceinline__ void emit_link(const Geo& g, u64 w, SmemMisc& m, bool
   }
 }
 
-__device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Claim& cl) {
+template <bool WT, class SL>
+__device__ void item_link(const Geo& g, u64 w, u32 b, SL& s, SmemMisc& m, Claim& cl) {
+  constexpr int pcap = WT ? PCAP_W : PCAP;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   PhaseTimer pt;
   const u32 ncp = chunks_of(g, w);
@@ -559,12 +601,19 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Cla
   }
   pt.mark(g, 1, 5);
   u64 k[KPT];
+  u32 wv[KPT];  // weighted rows: the weight of each gathered key
+  const u32* wsc = WT ? g.wscr + (u64)slot * g.cp * CH : nullptr;
+  u32* pwl[2] = {nullptr, nullptr};
+  if constexpr (WT) { pwl[0] = s.pw[0]; pwl[1] = s.pw[1]; }
+  unsigned long long wl = 0;  // this lane's sum of weights
 #pragma unroll
   for (int j = 0; j < KPT; ++j) {
     const u32 e = lane + 32 * j;
+    wv[j] = 1u;
     if (e < total) {
       const u32 q = find_seg(wpre, nseg, e);
       k[j] = ldcg64(ks + wlo[q] + (e - wpre[q]));
+      if constexpr (WT) wv[j] = ldcg32(wsc + wlo[q] + (e - wpre[q]));
     }
   }
   pt.mark(g, 1, 6);
@@ -576,7 +625,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Cla
   }
   for (int i = t; i <= (int)(2 * B2); i += FT) s.hist[i] = 0;
   if (t < 4) m.esc[t] = 0;
-  if (t == 0) { m.flag = 0; m.pcnt[0] = 0; }
+  if (t == 0) { m.flag = 0; m.pcnt[0] = 0; m.wsum = 0; }
   pt.mark(g, 1, 7);
   __syncthreads();
   pt.mark(g, 1, 0);
@@ -593,6 +642,7 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Cla
         if (e < total) {
           const u32 q = find_seg(wpre, nseg, e);
           k[j] = ldcg64(ks + wlo[q] + (e - wpre[q]));
+          if constexpr (WT) wv[j] = ldcg32(wsc + wlo[q] + (e - wpre[q]));
         }
       }
     }
@@ -601,14 +651,21 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Cla
     for (int j = 0; j < KPT; ++j) {
       if (base + 32 * j >= total) break;  // warp-uniform
       bool entry = base + lane + 32 * j < total;
-      if (entry && k[j] == EMPTY64) { atomicAdd(&m.esc[0], 1u); entry = false; }
+      const u32 a = WT ? wv[j] : 1u;  // A_t(i,j) += n_packets of the row (1 for raw packets)
+      if constexpr (WT) wl += entry ? a : 0u;
+      if (entry && k[j] == EMPTY64) { atomicAdd(&m.esc[0], a); entry = false; }
       bool placed = true;
       u32 home = 0;
-      if (entry) { home = link_home(k[j]); placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, home); }
-      if (!placed) placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, probe_slot(home, 1u));
-      if (!pend_push(s.pa[0], s.pp[0], &m.pcnt[0], !placed, k[j], 2u, PCAP))
-        ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], 1u, 2u) && ok;
+      if (entry) { home = link_home(k[j]); placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], a, home); }
+      if (!placed) placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], a, probe_slot(home, 1u));
+      if (!pend_push(s.pa[0], s.pp[0], &m.pcnt[0], !placed, k[j], 2u, pcap, pwl[0], a))
+        ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, k[j], a, 2u) && ok;
     }
+  }
+  if constexpr (WT) {  // the bucket's weight sum bounds every count in it: records carry counts < 2^20
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wl += __shfl_xor_sync(0xffffffffu, wl, o);
+    if (lane == 0 && wl) atomicAdd(&m.wsum, wl);
   }
   __syncthreads();
   pt.mark(g, 1, 1);
@@ -616,10 +673,11 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Cla
   {
     // waves 1..: the pending list, densely, one probe further each wave; a short tail finishes per lane
     int cur = 0;
-    u32 n = min(m.pcnt[0], (u32)PCAP);
+    u32 n = min(m.pcnt[0], (u32)pcap);
     while (n) {
       if (n <= WAVE_TAIL) {
-        if ((u32)t < n) ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, s.pa[cur][t], 1u, s.pp[cur][t]) && ok;
+        if ((u32)t < n)
+          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, s.pa[cur][t], WT ? pwl[cur][t] : 1u, s.pp[cur][t]) && ok;
         break;
       }
       if (t == 0) m.pcnt[cur ^ 1] = 0;
@@ -627,24 +685,28 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SmemL& s, SmemMisc& m, Cla
       for (u32 i0 = 0; i0 < n; i0 += FT) {
         const u32 i = i0 + t;
         u64 a = 0;
-        u32 probe = 0;
+        u32 probe = 0, wt = 1u;
         bool placed = true;
         if (i < n) {
           a = s.pa[cur][i];
           probe = s.pp[cur][i];
+          if constexpr (WT) wt = pwl[cur][i];
           if (probe >= (u32)TCAP) ok = false;
-          else placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, a, 1u, probe_slot(link_home(a), probe));
+          else placed = link_try_h(s.lkey, s.lcnt, s.hist, B2, logB2, a, wt, probe_slot(link_home(a), probe));
         }
         probe += 1;
-        if (!pend_push(s.pa[cur ^ 1], s.pp[cur ^ 1], &m.pcnt[cur ^ 1], !placed, a, probe, PCAP))
-          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, a, 1u, probe) && ok;
+        if (!pend_push(s.pa[cur ^ 1], s.pp[cur ^ 1], &m.pcnt[cur ^ 1], !placed, a, probe, pcap, pwl[cur ^ 1], wt))
+          ok = link_finish_h(s.lkey, s.lcnt, s.hist, B2, logB2, a, wt, probe) && ok;
       }
       __syncthreads();
       cur ^= 1;
-      n = min(m.pcnt[cur], (u32)PCAP);
+      n = min(m.pcnt[cur], (u32)pcap);
     }
   }
   if (!ok) m.flag = 1;
+  // weighted rows: a bucket whose weights sum to >= 2^20 cannot use 20-bit record counts: the window
+  // goes to the L2 path (64-bit-safe sums there)
+  if (WT && t == 0 && m.wsum >= (1ull << REC_PBITS)) m.flag = 1;
   if (t == 0 && m.esc[0]) {  // the key ~0 (255.255.255.255 -> 255.255.255.255) is one more link
     atomicAdd(&s.hist[side_bucket(EMPTY32, logB2)], 1u);
     atomicAdd(&s.hist[B2 + side_bucket(EMPTY32, logB2)], 1u);
@@ -833,7 +895,7 @@ __device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict_
       u64* ip = g.v_ipsets + w * 4;
       ip[0] = (u64)r[2] + r[3] - r[9]; ip[1] = r[2] - r[9]; ip[2] = r[3] - r[9]; ip[3] = r[9];
     }
-    if ((u64)r[1] != wlen && ld_acquire32(&g.ovf[w]) == 0) atomicAdd(&g.diag[1], 1u);
+    if (!g.wgt && (u64)r[1] != wlen && ld_acquire32(&g.ovf[w]) == 0) atomicAdd(&g.diag[1], 1u);
     if ((g.flags & NSG_FLAG_INJECT_OVERFLOW) && (w & 1)) mark_overflow(g, w);
     // The slot may now be reused: every reader of it has signalled sdone.  (Dropping its dead L2
     // lines with discard.global.L2 first halves DRAM writes but was measured 14% slower on C2.)
@@ -1183,6 +1245,7 @@ __device__ u64 g_trace[TRACE_CAP][4];
 __device__ u32 g_trace_n;
 #endif
 
+template <bool WT>
 __global__ void __launch_bounds__(FT, 1024 / FT)
 fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, const u64* __restrict__ keys,
             u64* __restrict__ out) {
@@ -1220,13 +1283,14 @@ fast_kernel(Geo g, const u32* __restrict__ src, const u32* __restrict__ dst, con
     // every item function passes a __syncthreads() before the scheduler can overwrite m.type/m.w/m.idx
     if (type == ITEM_P) {
       if (idx < chunks_of(g, w)) {
-        item_partition(g, src, dst, keys, w, idx, *reinterpret_cast<SmemP*>(u), m, cl);
+        item_partition<WT>(g, src, dst, keys, w, idx, *reinterpret_cast<SmemP*>(u), m, cl);
       } else {  // a chunk past the end of the last (short) window: count it done
         if (threadIdx.x == 0) red_release_add32(&g.pdone[w], 1u);
         __syncthreads();
       }
     } else if (type == ITEM_L) {
-      item_link(g, w, idx, *reinterpret_cast<SmemL*>(u), m, cl);
+      if constexpr (WT) item_link<true>(g, w, idx, *reinterpret_cast<SmemLW*>(u), m, cl);
+      else item_link<false>(g, w, idx, *reinterpret_cast<SmemL*>(u), m, cl);
     } else if (type == ITEM_S0 || type == ITEM_S1) {
       item_side(g, w, (int)(type - ITEM_S0), idx, *reinterpret_cast<SmemS*>(u), m, cl);
     } else if (type == ITEM_F) {

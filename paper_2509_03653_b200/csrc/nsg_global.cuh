@@ -25,9 +25,10 @@ struct GGeo {
   u64* v_lkey; u32* v_lpk;
   u32* v_node[2]; u32* v_pk[2]; u32* v_fan[2];
   u64* v_ipsets;
+  const u32* wgt;  // weighted rows: n_packets per row (NULL: raw packets, weight 1)
 };
 
-__device__ __forceinline__ void glob_link_insert(u64* lkey, u32* lcnt, u64 LC, u64 key) {
+__device__ __forceinline__ void glob_link_insert(u64* lkey, u32* lcnt, u64 LC, u64 key, u32 add) {
   u64 slot = hash64(key) & (LC - 1);
   for (;;) {
     u64 k = ldcg64(&lkey[slot]);
@@ -35,7 +36,7 @@ __device__ __forceinline__ void glob_link_insert(u64* lkey, u32* lcnt, u64 LC, u
       const u64 old = atomicCAS(reinterpret_cast<unsigned long long*>(&lkey[slot]), EMPTY64, key);
       k = (old == EMPTY64) ? key : old;
     }
-    if (k == key) { atomicAdd(&lcnt[slot], 1u); return; }
+    if (k == key) { atomicAdd(&lcnt[slot], add); return; }
     slot = (slot + 1) & (LC - 1);  // the table has >= 2x the window's slots: never full
   }
 }
@@ -71,6 +72,7 @@ global_kernel(GGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, 
   __shared__ u32 esc[5];
   __shared__ u32 red[9 * (GT / 32)];
   __shared__ u32 vcnt[3], both_s;
+  __shared__ unsigned long long wtot;
   if (g.only_overflowed && ldcg32(&g.diag[0]) == 0) return;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const u64 LC = g.LC;
@@ -89,13 +91,18 @@ global_kernel(GGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, 
     }
     if (t < 5) esc[t] = 0;
     if (t < 3) vcnt[t] = 0;
-    if (t == 0) both_s = 0;
+    if (t == 0) { both_s = 0; wtot = 0; }
     __syncthreads();
+    unsigned long long wl = 0;
     for (u64 i = t; i < len; i += GT) {
+      const u32 a = g.wgt ? g.wgt[base + i] : 1u;  // A_t(i,j) += n_packets (1 for raw packets); 0 adds nothing
+      if (a == 0) continue;
+      wl += a;
       const u64 key = keys ? keys[base + i] : (((u64)src[base + i] << 32) | dst[base + i]);
-      if (key == EMPTY64) atomicAdd(&esc[0], 1u);
-      else glob_link_insert(lkey, lcnt, LC, key);
+      if (key == EMPTY64) atomicAdd(&esc[0], a);
+      else glob_link_insert(lkey, lcnt, LC, key, a);
     }
+    if (wl) atomicAdd(&wtot, wl);
     __syncthreads();
     u32* k0 = g.nkey + ((u64)blockIdx.x * 2 + 0) * LC;
     u32* k1 = g.nkey + ((u64)blockIdx.x * 2 + 1) * LC;
@@ -184,7 +191,10 @@ global_kernel(GGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, 
       o[NSG_UNIQUE_DESTINATIONS] = r[3];
       o[NSG_MAX_DESTINATION_PACKETS] = r[7];
       o[NSG_MAX_DESTINATION_FANIN] = r[8];
-      if ((u64)r[1] != len) atomicAdd(&g.diag[1], 1u);
+      // self-check: the counts sum to the window's packets (sum of n_packets for weighted rows, which the
+      // 32-bit counters support up to 2^32 - 1 per window: beyond that the window is reported in diag[2])
+      if (wtot >= (1ull << 32)) atomicAdd(&g.diag[2], 1u);
+      else if ((u64)r[1] != wtot) atomicAdd(&g.diag[1], 1u);
       if (g.v_ipsets) {  // |S u D|, |S \ D|, |D \ S|, |S n D|
         const u32 b = both_s;
         u64* ip = g.v_ipsets + w * 4;
