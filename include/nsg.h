@@ -183,6 +183,49 @@ nsg_status nsg_window_vectors(const uint32_t* src, const uint32_t* dst, const ui
                               uint64_t window, uint64_t* out, const nsg_vectors* vectors, void* workspace,
                               size_t workspace_bytes, void* stream, uint32_t flags);
 
+/* ---- Whole-trace path ------------------------------------------------
+ * Table 2 on the traffic matrix of the WHOLE input, A = sum over t of A_t (the paper's
+ * frame holds the whole capture), i.e. the nine statistics with window = n_packets, but with HBM-resident
+ * hash tables filled by every SM, so the input may be far larger than a window.  Per-link and per-node
+ * sums are kept in 32 bits (n_packets < 2^32 per call).  The work is split into steps so that a multi-GPU
+ * driver can exchange data between them (paper_2509_03653_b200/distributed.py, NCCL all-to-all):
+ *   1. nsg_trace_partition: group this rank's keys by the rank that owns their link.
+ *   2. (all-to-all of the keys)  nsg_trace_links: aggregate the owned links -> link_stats u64[3] =
+ *      {valid packets (sum of A), unique links, max link packets} and one record
+ *      (node << 32 | A(i,j)) per link and side, grouped by the node's owner rank.
+ *   3. (all-to-all of the records)  nsg_trace_nodes, once per side: node_stats u64[3] = {unique nodes,
+ *      max packets, max fan} (PAPER.md:184, :186, :188; the destination mirrors, :173).
+ *   4. (sum / max over ranks).
+ * Owners: link (key) -> top bits of a 64-bit mix of the key times world; node -> a 32-bit mix.  Every
+ * pointer is device memory, 8 B aligned; all calls are asynchronous on `stream`; the workspace (256 B
+ * aligned, nsg_trace_workspace_bytes) may be reused by the next step once this one is enqueued (steps on
+ * one stream are ordered).  Capacities: n <= key_capacity keys per links call, m <= record_capacity
+ * records per nodes call, 1 <= world <= 1024; violations are NSG_ERR_INVALID_ARGUMENT. */
+size_t nsg_trace_workspace_bytes(uint64_t key_capacity, uint64_t record_capacity, uint32_t world);
+
+/* send_keys u64[n] (device): the keys grouped by owner rank, rank o's segment at the exclusive prefix
+ * of send_counts; send_counts u64[world] (device).  Input as nsg_window_stats_ex (keys or src/dst). */
+nsg_status nsg_trace_partition(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n,
+                               uint32_t world, uint64_t* send_keys, uint64_t* send_counts, void* workspace,
+                               size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity, void* stream);
+
+/* link_stats u64[3]; rec_src, rec_dst u64[n] (at most one record per distinct link and side), grouped by
+ * owner rank at the exclusive prefix of rec_counts[0][*] / rec_counts[1][*]; rec_counts u64[2][world]. */
+nsg_status nsg_trace_links(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n, uint32_t world,
+                           uint64_t* link_stats, uint64_t* rec_src, uint64_t* rec_dst, uint64_t* rec_counts,
+                           void* workspace, size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity,
+                           void* stream);
+
+/* node_stats u64[3] from m records (node << 32 | packets), each record one link of the node. */
+nsg_status nsg_trace_nodes(const uint64_t* records, uint64_t m, uint64_t* node_stats, void* workspace,
+                           size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity, void* stream);
+
+/* One GPU: the nine whole-trace statistics into out u64[9] (device), north_star column order; the steps
+ * above with world = 1 and no host synchronisation.  Workspace: nsg_trace_stats_workspace_bytes(n). */
+size_t nsg_trace_stats_workspace_bytes(uint64_t n_packets);
+nsg_status nsg_trace_stats(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
+                           uint64_t* out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* Diagnostics of the last call that used `workspace` (device memory; read it after the stream has
  * completed the call): byte offset inside the workspace of a u32[4] =
  *   {windows the fast path handed to the L2 path because an SMEM table would overflow,

@@ -18,9 +18,14 @@ from .api import (  # noqa: F401
     IP_SET_NAMES,
     NUM_STATS,
     STAT_NAMES,
+    TraceWorkspace,
     Workspace,
     last_launches,
     num_windows,
+    trace_links,
+    trace_nodes,
+    trace_partition,
+    trace_stats,
     version,
     window_stats,
     window_stats_from_host,

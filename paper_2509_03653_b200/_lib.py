@@ -12,7 +12,8 @@ import subprocess
 _PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.path.join(_PKG, "libnsg.so")
-SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("nsg.cu", "nsg_common.cuh", "nsg_fast.cuh", "nsg_global.cuh")]
+SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("nsg.cu", "nsg_common.cuh", "nsg_fast.cuh", "nsg_global.cuh",
+                                                   "nsg_trace.cuh")]
 HEADER = os.path.join(ROOT, "include", "nsg.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
@@ -28,6 +29,12 @@ EXPORTS = (
     "nsg_window_stats_from_host",
     "nsg_window_vectors",
     "nsg_window_stats_weighted",
+    "nsg_trace_workspace_bytes",
+    "nsg_trace_partition",
+    "nsg_trace_links",
+    "nsg_trace_nodes",
+    "nsg_trace_stats_workspace_bytes",
+    "nsg_trace_stats",
     "nsg_diag_offset",
     "nsg_last_launches",
     "nsg_status_string",
@@ -95,6 +102,18 @@ def load() -> ctypes.CDLL:
     lib.nsg_window_vectors.argtypes = [vp, vp, vp, u64, u64, vp, ctypes.POINTER(NsgVectors), vp, sz, vp, u32]
     lib.nsg_window_stats_weighted.restype = ctypes.c_int
     lib.nsg_window_stats_weighted.argtypes = [vp, vp, vp, vp, u64, u64, vp, vp, sz, vp, u32]
+    lib.nsg_trace_workspace_bytes.restype = sz
+    lib.nsg_trace_workspace_bytes.argtypes = [u64, u64, u32]
+    lib.nsg_trace_partition.restype = ctypes.c_int
+    lib.nsg_trace_partition.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp, sz, u64, u64, vp]
+    lib.nsg_trace_links.restype = ctypes.c_int
+    lib.nsg_trace_links.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp, vp, vp, sz, u64, u64, vp]
+    lib.nsg_trace_nodes.restype = ctypes.c_int
+    lib.nsg_trace_nodes.argtypes = [vp, u64, vp, vp, sz, u64, u64, vp]
+    lib.nsg_trace_stats_workspace_bytes.restype = sz
+    lib.nsg_trace_stats_workspace_bytes.argtypes = [u64]
+    lib.nsg_trace_stats.restype = ctypes.c_int
+    lib.nsg_trace_stats.argtypes = [vp, vp, vp, u64, vp, vp, sz, vp]
     lib.nsg_diag_offset.restype = sz
     lib.nsg_diag_offset.argtypes = []
     lib.nsg_last_launches.restype = ctypes.c_uint

@@ -342,3 +342,107 @@ def window_stats_weighted(keys: Optional[torch.Tensor] = None, n_packets: Option
     if rc != 0:
         raise NsgError(rc, "nsg_window_stats_weighted")
     return out
+
+
+# ---------------------------------------------------------------------------------------------------
+# Whole-trace path: Table 2 on A = sum of the A_t, HBM-resident tables
+# ---------------------------------------------------------------------------------------------------
+class _Scratch:
+    """Caller-owned, 256 B aligned device scratch of a given size."""
+
+    def __init__(self, nbytes: int, device):
+        self.nbytes = int(nbytes)
+        self.buffer = torch.empty(max(self.nbytes, 1) + 256, dtype=torch.uint8, device=device)
+        base = self.buffer.data_ptr()
+        self.ptr = base + (-base) % 256
+
+
+class TraceWorkspace(_Scratch):
+    """Scratch of the trace steps for up to key_capacity keys per links call and record_capacity records
+    per nodes call (nsg_trace_workspace_bytes)."""
+
+    def __init__(self, key_capacity: int, record_capacity: int, world: int = 1, device=None):
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.key_capacity, self.record_capacity, self.world = int(key_capacity), int(record_capacity), int(world)
+        nb = int(_lib.nsg_trace_workspace_bytes(self.key_capacity, self.record_capacity, self.world))
+        if nb == 0:
+            raise ValueError("world must be in [1, 1024]")
+        super().__init__(nb, dev)
+
+
+def _rows(keys, src, dst):
+    if keys is not None:
+        if src is not None or dst is not None:
+            raise ValueError("pass either keys or (src, dst)")
+        _check(keys, "keys", _U64_TYPES)
+        return keys.numel(), keys.device
+    _check(src, "src", _U32_TYPES)
+    _check(dst, "dst", _U32_TYPES)
+    if src.numel() != dst.numel() or src.device != dst.device:
+        raise ValueError("src and dst must have the same length and device")
+    return src.numel(), src.device
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def trace_stats(keys: Optional[torch.Tensor] = None, *, src=None, dst=None, out=None, stream=None) -> torch.Tensor:
+    """The nine statistics of the WHOLE input (A = sum of the A_t; nsg_trace_stats, one GPU).  Returns a
+    device int64 [9] tensor, valid when `stream` completes."""
+    n, device = _rows(keys, src, dst)
+    if out is None:
+        out = torch.empty(NUM_STATS, dtype=torch.int64, device=device)
+    if n == 0:
+        return out.zero_()
+    ws = _Scratch(_lib.nsg_trace_stats_workspace_bytes(n), device)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_trace_stats(_p(src), _p(dst), _p(keys), n, out.data_ptr(), ws.ptr, ws.nbytes,
+                              ctypes.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise NsgError(rc, "nsg_trace_stats")
+    return out
+
+
+def trace_partition(keys: torch.Tensor, world: int, workspace: TraceWorkspace, stream=None):
+    """Step 1: keys grouped by the rank owning their link.  Returns (send_keys int64 [n], send_counts int64
+    [world]) on the device."""
+    n, device = _rows(keys, None, None)
+    send = torch.empty(n, dtype=torch.int64, device=device)
+    counts = torch.zeros(world, dtype=torch.int64, device=device)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_trace_partition(None, None, keys.data_ptr(), n, int(world), send.data_ptr(), counts.data_ptr(),
+                                  workspace.ptr, workspace.nbytes, workspace.key_capacity, workspace.record_capacity,
+                                  ctypes.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise NsgError(rc, "nsg_trace_partition")
+    return send, counts
+
+
+def trace_links(keys: torch.Tensor, world: int, workspace: TraceWorkspace, stream=None):
+    """Step 2: the owned links.  Returns (link_stats int64 [3] = valid, unique links, max link; rec_src,
+    rec_dst int64 [n] records (node << 32 | packets) grouped by owner; rec_counts int64 [2, world])."""
+    n, device = _rows(keys, None, None)
+    stats = torch.zeros(3, dtype=torch.int64, device=device)
+    rs = torch.empty(max(n, 1), dtype=torch.int64, device=device)
+    rd = torch.empty(max(n, 1), dtype=torch.int64, device=device)
+    rc_ = torch.zeros((2, world), dtype=torch.int64, device=device)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_trace_links(None, None, keys.data_ptr() if n else None, n, int(world), stats.data_ptr(), rs.data_ptr(),
+                              rd.data_ptr(), rc_.data_ptr(), workspace.ptr, workspace.nbytes, workspace.key_capacity,
+                              workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise NsgError(rc, "nsg_trace_links")
+    return stats, rs, rd, rc_
+
+
+def trace_nodes(records: torch.Tensor, workspace: TraceWorkspace, stream=None) -> torch.Tensor:
+    """Step 3: int64 [3] = unique nodes, max packets, max fan of one side's records."""
+    m, device = records.numel(), records.device
+    stats = torch.zeros(3, dtype=torch.int64, device=device)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_trace_nodes(records.data_ptr() if m else None, m, stats.data_ptr(), workspace.ptr, workspace.nbytes,
+                              workspace.key_capacity, workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise NsgError(rc, "nsg_trace_nodes")
+    return stats

@@ -11,6 +11,8 @@
 //                    SMEM hash tables, exchange through L2-resident scratch).
 //   nsg_global.cuh — any window <= 2^31 and the fast path's overflow hand-off: one CTA per window
 //                    with global-memory hash tables.
+//   nsg_trace.cuh  — the whole-trace path (A = sum of the A_t): HBM-resident tables filled by every SM,
+//                    in steps a multi-GPU driver interleaves with all-to-all exchanges.
 // This file holds the C ABI: argument checks, workspace layout, launches.
 #include <algorithm>
 #include <cuda.h>  // driver types for cuStreamWriteValue32 (resolved at run time: no libcuda link)
@@ -18,6 +20,7 @@
 #include "nsg_common.cuh"
 #include "nsg_fast.cuh"
 #include "nsg_global.cuh"
+#include "nsg_trace.cuh"
 
 #include <cstdio>
 #include <cstring>
@@ -352,6 +355,121 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
   return NSG_OK;
 }
 
+// ------------------------------------------------------------------------------------------
+// Whole-trace path (nsg_trace.cuh): workspace layout and step launches
+// ------------------------------------------------------------------------------------------
+struct TLayout {
+  u64 LC, NC;
+  u32 grid, world;
+  size_t o_acc, o_ccount, o_coff, o_lkey, o_lcnt, o_nkey, o_nP, o_nF, total;
+};
+
+static TLayout trace_layout(u64 key_cap, u64 rec_cap, u32 world, int sms) {
+  TLayout T;
+  memset(&T, 0, sizeof(T));
+  T.LC = next_pow2(2 * (key_cap ? key_cap : 1));
+  T.NC = next_pow2(2 * (rec_cap ? rec_cap : 1));
+  T.grid = (u32)(sms * (2048 / TT));
+  T.world = world;
+  size_t o = 0;
+  T.o_acc = o; o = align256(o + 64 * sizeof(u64));  // u32 esc[0] (link key ~0), esc[2..3] (node ~0 P, F)
+  T.o_ccount = o; o = align256(o + (size_t)T.grid * 2 * world * sizeof(u32));
+  T.o_coff = o; o = align256(o + (size_t)T.grid * 2 * world * sizeof(u64));
+  T.o_lkey = o; o = align256(o + (size_t)T.LC * sizeof(u64));
+  T.o_lcnt = o; o = align256(o + (size_t)T.LC * sizeof(u32));
+  T.o_nkey = o; o = align256(o + (size_t)T.NC * sizeof(u32));
+  T.o_nP = o; o = align256(o + (size_t)T.NC * sizeof(u32));
+  T.o_nF = o; o = align256(o + (size_t)T.NC * sizeof(u32));
+  T.total = o;
+  return T;
+}
+
+struct TraceCall {
+  TLayout T;
+  unsigned char* base;
+  cudaStream_t s;
+};
+
+static nsg_status trace_begin(void* ws, size_t ws_bytes, u64 key_cap, u64 rec_cap, u32 world, void* stream,
+                              TraceCall& c) {
+  if (!ws || (reinterpret_cast<uintptr_t>(ws) & 255)) return NSG_ERR_INVALID_ARGUMENT;
+  if (world < 1 || world > (u32)TRACE_MAX_WORLD) return NSG_ERR_INVALID_ARGUMENT;
+  DevInfo d;
+  const nsg_status st = dev_info(d);
+  if (st != NSG_OK) return st;
+  c.T = trace_layout(key_cap, rec_cap, world, d.sms);
+  if (ws_bytes < c.T.total) return NSG_ERR_WORKSPACE_TOO_SMALL;
+  c.base = reinterpret_cast<unsigned char*>(ws);
+  c.s = reinterpret_cast<cudaStream_t>(stream);
+  return NSG_OK;
+}
+
+static bool input_ok(const u32* src, const u32* dst, const u64* keys) {
+  if ((keys == nullptr) == (src == nullptr && dst == nullptr)) return false;
+  if (!keys && (!src || !dst)) return false;
+  if (keys && (reinterpret_cast<uintptr_t>(keys) & 7)) return false;
+  if (src && ((reinterpret_cast<uintptr_t>(src) & 3) || (reinterpret_cast<uintptr_t>(dst) & 3))) return false;
+  return true;
+}
+
+static nsg_status trace_links_impl(const u32* src, const u32* dst, const u64* keys, u64 n, u32 world, u64* link_stats,
+                                   u64* rec_src, u64* rec_dst, u64* rec_counts, TraceCall& c) {
+  const TLayout& T = c.T;
+  u32* esc = reinterpret_cast<u32*>(c.base + T.o_acc);
+  u64* lkey = reinterpret_cast<u64*>(c.base + T.o_lkey);
+  u32* lcnt = reinterpret_cast<u32*>(c.base + T.o_lcnt);
+  u32* ccount = reinterpret_cast<u32*>(c.base + T.o_ccount);
+  u64* coff = reinterpret_cast<u64*>(c.base + T.o_coff);
+  if (cudaMemsetAsync(esc, 0, 16, c.s) != cudaSuccess || cudaMemsetAsync(lkey, 0xFF, T.LC * 8, c.s) != cudaSuccess ||
+      cudaMemsetAsync(lcnt, 0, T.LC * 4, c.s) != cudaSuccess || cudaMemsetAsync(link_stats, 0, 24, c.s) != cudaSuccess)
+    return NSG_ERR_CUDA;
+  if (n) {
+    trace_link_insert<<<T.grid, TT, 0, c.s>>>(keys, src, dst, n, lkey, lcnt, T.LC, esc);
+    g_last_launches++;
+  }
+  trace_link_count<<<T.grid, TT, 0, c.s>>>(lkey, lcnt, T.LC, esc, world, ccount,
+                                           reinterpret_cast<unsigned long long*>(link_stats));
+  trace_scan<<<1, TRACE_MAX_WORLD, 0, c.s>>>(ccount, T.grid, 2, world, coff, rec_counts);
+  trace_link_emit<<<T.grid, TT, 0, c.s>>>(lkey, lcnt, T.LC, esc, world, coff, rec_src, rec_dst);
+  g_last_launches += 3;
+  return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
+}
+
+static nsg_status trace_nodes_counted(const u64* rec, const u64* m_dev, u64* node_stats, TraceCall& c) {
+  const TLayout& T = c.T;
+  u32* esc = reinterpret_cast<u32*>(c.base + T.o_acc) + 2;
+  u32* nkey = reinterpret_cast<u32*>(c.base + T.o_nkey);
+  u32* nP = reinterpret_cast<u32*>(c.base + T.o_nP);
+  u32* nF = reinterpret_cast<u32*>(c.base + T.o_nF);
+  if (cudaMemsetAsync(esc, 0, 8, c.s) != cudaSuccess || cudaMemsetAsync(nkey, 0xFF, T.NC * 4, c.s) != cudaSuccess ||
+      cudaMemsetAsync(nP, 0, T.NC * 4, c.s) != cudaSuccess || cudaMemsetAsync(nF, 0, T.NC * 4, c.s) != cudaSuccess ||
+      cudaMemsetAsync(node_stats, 0, 24, c.s) != cudaSuccess)
+    return NSG_ERR_CUDA;
+  trace_node_insert_dev<<<T.grid, TT, 0, c.s>>>(rec, m_dev, nkey, nP, nF, T.NC, esc);
+  trace_node_scan<<<T.grid, TT, 0, c.s>>>(nkey, nP, nF, T.NC, esc, reinterpret_cast<unsigned long long*>(node_stats));
+  g_last_launches += 2;
+  return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
+}
+
+static nsg_status trace_nodes_impl(const u64* rec, u64 m, u64* node_stats, TraceCall& c) {
+  const TLayout& T = c.T;
+  u32* esc = reinterpret_cast<u32*>(c.base + T.o_acc) + 2;
+  u32* nkey = reinterpret_cast<u32*>(c.base + T.o_nkey);
+  u32* nP = reinterpret_cast<u32*>(c.base + T.o_nP);
+  u32* nF = reinterpret_cast<u32*>(c.base + T.o_nF);
+  if (cudaMemsetAsync(esc, 0, 8, c.s) != cudaSuccess || cudaMemsetAsync(nkey, 0xFF, T.NC * 4, c.s) != cudaSuccess ||
+      cudaMemsetAsync(nP, 0, T.NC * 4, c.s) != cudaSuccess || cudaMemsetAsync(nF, 0, T.NC * 4, c.s) != cudaSuccess ||
+      cudaMemsetAsync(node_stats, 0, 24, c.s) != cudaSuccess)
+    return NSG_ERR_CUDA;
+  if (m) {
+    trace_node_insert<<<T.grid, TT, 0, c.s>>>(rec, m, nkey, nP, nF, T.NC, esc);
+    g_last_launches++;
+  }
+  trace_node_scan<<<T.grid, TT, 0, c.s>>>(nkey, nP, nF, T.NC, esc, reinterpret_cast<unsigned long long*>(node_stats));
+  g_last_launches++;
+  return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
+}
+
 }  // namespace nsg
 
 // ------------------------------------------------------------------------------------------
@@ -433,6 +551,100 @@ nsg_status nsg_window_stats_weighted(const uint32_t* src, const uint32_t* dst, c
   if (n_rows && !n_packets) return NSG_ERR_INVALID_ARGUMENT;
   return nsg::run(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_rows, window, reinterpret_cast<nsg::u64*>(out),
                   workspace, workspace_bytes, stream, flags, nullptr, nullptr, nullptr, nullptr, n_packets);
+}
+
+size_t nsg_trace_workspace_bytes(uint64_t key_capacity, uint64_t record_capacity, uint32_t world) {
+  if (world < 1 || world > (uint32_t)nsg::TRACE_MAX_WORLD) return 0;
+  return nsg::trace_layout(key_capacity, record_capacity, world, nsg::sms_for_layout()).total;
+}
+
+size_t nsg_trace_stats_workspace_bytes(uint64_t n_packets) {
+  const size_t t = nsg::align256(nsg_trace_workspace_bytes(n_packets, n_packets, 1));
+  return t + 2 * nsg::align256((size_t)(n_packets ? n_packets : 1) * 8) + 256;
+}
+
+nsg_status nsg_trace_partition(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n,
+                               uint32_t world, uint64_t* send_keys, uint64_t* send_counts, void* workspace,
+                               size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity, void* stream) {
+  nsg::g_last_launches = 0;
+  if (n && !nsg::input_ok(src, dst, reinterpret_cast<const nsg::u64*>(keys))) return NSG_ERR_INVALID_ARGUMENT;
+  if (!send_keys || !send_counts || (reinterpret_cast<uintptr_t>(send_keys) & 7) ||
+      (reinterpret_cast<uintptr_t>(send_counts) & 7))
+    return NSG_ERR_INVALID_ARGUMENT;
+  nsg::TraceCall c;
+  nsg_status st = nsg::trace_begin(workspace, workspace_bytes, key_capacity, record_capacity, world, stream, c);
+  if (st != NSG_OK) return st;
+  nsg::u32* ccount = reinterpret_cast<nsg::u32*>(c.base + c.T.o_ccount);
+  nsg::u64* coff = reinterpret_cast<nsg::u64*>(c.base + c.T.o_coff);
+  const nsg::u64* k = reinterpret_cast<const nsg::u64*>(keys);
+  nsg::trace_part_count<<<c.T.grid, nsg::TT, 0, c.s>>>(k, src, dst, n, world, ccount);
+  nsg::trace_scan<<<1, nsg::TRACE_MAX_WORLD, 0, c.s>>>(ccount, c.T.grid, 1, world, coff,
+                                                        reinterpret_cast<nsg::u64*>(send_counts));
+  nsg::trace_part_scatter<<<c.T.grid, nsg::TT, 0, c.s>>>(k, src, dst, n, world, coff,
+                                                         reinterpret_cast<nsg::u64*>(send_keys));
+  nsg::g_last_launches = 3;
+  return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
+}
+
+nsg_status nsg_trace_links(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n, uint32_t world,
+                           uint64_t* link_stats, uint64_t* rec_src, uint64_t* rec_dst, uint64_t* rec_counts,
+                           void* workspace, size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity,
+                           void* stream) {
+  nsg::g_last_launches = 0;
+  if (n > key_capacity) return NSG_ERR_INVALID_ARGUMENT;
+  if (n && !nsg::input_ok(src, dst, reinterpret_cast<const nsg::u64*>(keys))) return NSG_ERR_INVALID_ARGUMENT;
+  const void* p8[] = {link_stats, rec_src, rec_dst, rec_counts};
+  for (const void* p : p8)
+    if (!p || (reinterpret_cast<uintptr_t>(p) & 7)) return NSG_ERR_INVALID_ARGUMENT;
+  nsg::TraceCall c;
+  nsg_status st = nsg::trace_begin(workspace, workspace_bytes, key_capacity, record_capacity, world, stream, c);
+  if (st != NSG_OK) return st;
+  return nsg::trace_links_impl(src, dst, reinterpret_cast<const nsg::u64*>(keys), n, world,
+                               reinterpret_cast<nsg::u64*>(link_stats), reinterpret_cast<nsg::u64*>(rec_src),
+                               reinterpret_cast<nsg::u64*>(rec_dst), reinterpret_cast<nsg::u64*>(rec_counts), c);
+}
+
+nsg_status nsg_trace_nodes(const uint64_t* records, uint64_t m, uint64_t* node_stats, void* workspace,
+                           size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity, void* stream) {
+  nsg::g_last_launches = 0;
+  if (m > record_capacity || (m && !records) || (reinterpret_cast<uintptr_t>(records) & 7)) return NSG_ERR_INVALID_ARGUMENT;
+  if (!node_stats || (reinterpret_cast<uintptr_t>(node_stats) & 7)) return NSG_ERR_INVALID_ARGUMENT;
+  nsg::TraceCall c;
+  nsg_status st = nsg::trace_begin(workspace, workspace_bytes, key_capacity, record_capacity, 1, stream, c);
+  if (st != NSG_OK) return st;
+  return nsg::trace_nodes_impl(reinterpret_cast<const nsg::u64*>(records), m, reinterpret_cast<nsg::u64*>(node_stats), c);
+}
+
+nsg_status nsg_trace_stats(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
+                           uint64_t* out, void* workspace, size_t workspace_bytes, void* stream) {
+  nsg::g_last_launches = 0;
+  if (n_packets == 0) return NSG_OK;
+  if (!nsg::input_ok(src, dst, reinterpret_cast<const nsg::u64*>(keys))) return NSG_ERR_INVALID_ARGUMENT;
+  if (!out || (reinterpret_cast<uintptr_t>(out) & 7)) return NSG_ERR_INVALID_ARGUMENT;
+  if (workspace_bytes < nsg_trace_stats_workspace_bytes(n_packets)) return NSG_ERR_WORKSPACE_TOO_SMALL;
+  nsg::TraceCall c;
+  const size_t tb = nsg::align256(nsg_trace_workspace_bytes(n_packets, n_packets, 1));
+  nsg_status st = nsg::trace_begin(workspace, tb, n_packets, n_packets, 1, stream, c);
+  if (st != NSG_OK) return st;
+  unsigned char* extra = c.base + tb;
+  nsg::u64* rec_src = reinterpret_cast<nsg::u64*>(extra);
+  nsg::u64* rec_dst = reinterpret_cast<nsg::u64*>(extra + nsg::align256((size_t)n_packets * 8));
+  nsg::u64* part = reinterpret_cast<nsg::u64*>(extra + 2 * nsg::align256((size_t)n_packets * 8));  // [12] + [2] counts
+  // 256 B tail: link [0..2], src [4..6], dst [8..10], record counts [12..13]
+  st = nsg::trace_links_impl(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_packets, 1, part, rec_src, rec_dst,
+                             part + 12, c);
+  if (st != NSG_OK) return st;
+  // with one rank every record stays here; the node steps read the record counts from device memory, so
+  // the whole call is asynchronous (no host sync for the counts)
+  st = nsg::trace_nodes_counted(rec_src, part + 12, part + 4, c);
+  if (st != NSG_OK) return st;
+  st = nsg::trace_nodes_counted(rec_dst, part + 13, part + 8, c);
+  if (st != NSG_OK) return st;
+  nsg::trace_finish<<<1, 32, 0, c.s>>>(reinterpret_cast<unsigned long long*>(part),
+                                       reinterpret_cast<unsigned long long*>(part + 4),
+                                       reinterpret_cast<unsigned long long*>(part + 8), reinterpret_cast<nsg::u64*>(out));
+  nsg::g_last_launches += 1;
+  return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }
 
 size_t nsg_diag_offset(void) { return nsg::DIAG_OFFSET; }

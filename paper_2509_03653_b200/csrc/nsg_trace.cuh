@@ -1,0 +1,252 @@
+// nsg_trace.cuh — the whole-trace path of libnsg: Table 2 on the traffic
+// matrix of the WHOLE input, A = sum over t of A_t (PAPER.md:145, :207 — the paper's cuDF frame holds the
+// whole capture).  Its distinct links far exceed any SMEM, so the tables live in HBM (global-memory
+// open addressing), and the path is split into steps that a multi-GPU driver interleaves with NCCL
+// all-to-all exchanges (paper_2509_03653_b200/distributed.py):
+//   partition  keys -> owner rank of the link  (o = top bits of hash64(key) * world)
+//   links      this rank's links: A restricted to the owned keys -> valid, unique links, max link,
+//              and one record (node << 32 | A(i,j)) per link and side, grouped by the node's owner rank
+//   nodes      records of one side -> row sums A1 / row nnz |A|_0 1 of the owned nodes (PAPER.md:185,
+//              :187; the column mirrors for destination records, :173) -> unique, max packets, max fan
+// With world = 1 nothing is exchanged: nsg_trace_stats runs links -> nodes(src) -> nodes(dst).
+#pragma once
+#include "nsg.h"
+#include "nsg_common.cuh"
+#include "nsg_global.cuh"
+
+namespace nsg {
+
+constexpr int TT = 512;          // threads per CTA of the trace kernels
+constexpr int TRACE_MAX_WORLD = 1024;
+
+// owner rank of a link / of a node (independent of the table slots, which use the low bits)
+__device__ __forceinline__ u32 link_owner(u64 key, u32 world) {
+  return __umulhi((u32)(hash64(key) >> 32), world);  // floor(h * world / 2^32) < world
+}
+__device__ __forceinline__ u32 node_owner(u32 node, u32 world) {
+  return __umulhi(hash32(node ^ 0x5BD1E995u), world);
+}
+
+// Slot range [lo, hi) of CTA b when `total` slots are split into gridDim.x contiguous ranges.
+__device__ __forceinline__ void cta_range(u64 total, u64& lo, u64& hi) {
+  const u64 per = (total + gridDim.x - 1) / gridDim.x;
+  lo = min(total, (u64)blockIdx.x * per);
+  hi = min(total, lo + per);
+}
+
+__device__ __forceinline__ u64 load_key(const u64* keys, const u32* src, const u32* dst, u64 i) {
+  return keys ? keys[i] : (((u64)src[i] << 32) | dst[i]);
+}
+
+// ---- partition (world > 1): counts per (CTA, owner), then a scatter into owner-contiguous segments
+__global__ void __launch_bounds__(TT) trace_part_count(const u64* __restrict__ keys, const u32* __restrict__ src,
+                                                       const u32* __restrict__ dst, u64 n, u32 world,
+                                                       u32* __restrict__ ccount) {
+  __shared__ u32 h[TRACE_MAX_WORLD];
+  for (u32 o = threadIdx.x; o < world; o += TT) h[o] = 0;
+  __syncthreads();
+  u64 lo, hi;
+  cta_range(n, lo, hi);
+  for (u64 i = lo + threadIdx.x; i < hi; i += TT) atomicAdd(&h[link_owner(load_key(keys, src, dst, i), world)], 1u);
+  __syncthreads();
+  for (u32 o = threadIdx.x; o < world; o += TT) ccount[(u64)blockIdx.x * world + o] = h[o];
+}
+
+// Exclusive offsets in (owner-major, CTA-minor) order for `sides` independent count tables
+// ccount[b][side][o] -> coff[b][side][o]; totals[side][o].  One CTA, thread o per owner.
+__global__ void __launch_bounds__(TRACE_MAX_WORLD) trace_scan(const u32* __restrict__ ccount, u32 grid, u32 sides,
+                                                              u32 world, u64* __restrict__ coff, u64* __restrict__ totals) {
+  __shared__ u64 tot[TRACE_MAX_WORLD];
+  const u32 o = threadIdx.x;
+  for (u32 sd = 0; sd < sides; ++sd) {
+    u64 t = 0;
+    if (o < world)
+      for (u32 b = 0; b < grid; ++b) t += ccount[((u64)b * sides + sd) * world + o];
+    if (o < TRACE_MAX_WORLD) tot[o] = o < world ? t : 0;
+    __syncthreads();
+    if (o == 0) {  // world <= 1024: a serial scan of the owner totals
+      u64 run = 0;
+      for (u32 q = 0; q < world; ++q) { const u64 v = tot[q]; tot[q] = run; run += v; }
+    }
+    __syncthreads();
+    if (o < world) {
+      u64 run = tot[o];
+      for (u32 b = 0; b < grid; ++b) {
+        const u64 idx = ((u64)b * sides + sd) * world + o;
+        coff[idx] = run;
+        run += ccount[idx];
+      }
+      totals[(u64)sd * world + o] = t;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(TT) trace_part_scatter(const u64* __restrict__ keys, const u32* __restrict__ src,
+                                                         const u32* __restrict__ dst, u64 n, u32 world,
+                                                         const u64* __restrict__ coff, u64* __restrict__ out) {
+  // per owner: the CTA's u64 base (from the scan) and a 32-bit local cursor (a CTA range has < 2^32 rows)
+  __shared__ u64 base[TRACE_MAX_WORLD];
+  __shared__ u32 cur[TRACE_MAX_WORLD];
+  for (u32 o = threadIdx.x; o < world; o += TT) { base[o] = coff[(u64)blockIdx.x * world + o]; cur[o] = 0; }
+  __syncthreads();
+  u64 lo, hi;
+  cta_range(n, lo, hi);
+  for (u64 i = lo + threadIdx.x; i < hi; i += TT) {
+    const u64 k = load_key(keys, src, dst, i);
+    const u32 o = link_owner(k, world);
+    out[base[o] + atomicAdd(&cur[o], 1u)] = k;
+  }
+}
+
+// ---- links: A restricted to this rank's keys in a global table, then records per side and owner
+__global__ void __launch_bounds__(TT) trace_link_insert(const u64* __restrict__ keys, const u32* __restrict__ src,
+                                                        const u32* __restrict__ dst, u64 n, u64* __restrict__ lkey,
+                                                        u32* __restrict__ lcnt, u64 LC, u32* __restrict__ esc) {
+  for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < n; i += (u64)gridDim.x * TT) {
+    const u64 k = load_key(keys, src, dst, i);
+    if (k == EMPTY64) atomicAdd(esc, 1u);  // the key ~0 is kept outside the table (reading R6)
+    else glob_link_insert(lkey, lcnt, LC, k, 1u);
+  }
+}
+
+// Per CTA slot range: link statistics (valid = sum of counts, unique links, max link; PAPER.md:180, :181,
+// :183) into acc[0..2] and the record counts per (side, owner) into ccount[b][2][world].  CTA 0 also
+// accounts the escaped key ~0 (esc[0] packets).
+__global__ void __launch_bounds__(TT) trace_link_count(const u64* __restrict__ lkey, const u32* __restrict__ lcnt,
+                                                       u64 LC, const u32* __restrict__ esc, u32 world,
+                                                       u32* __restrict__ ccount, unsigned long long* __restrict__ acc) {
+  __shared__ u32 h[2][TRACE_MAX_WORLD];
+  __shared__ unsigned long long s_sum, s_links, s_max;
+  for (u32 o = threadIdx.x; o < world; o += TT) { h[0][o] = 0; h[1][o] = 0; }
+  if (threadIdx.x == 0) { s_sum = 0; s_links = 0; s_max = 0; }
+  __syncthreads();
+  u64 lo, hi;
+  cta_range(LC, lo, hi);
+  unsigned long long sm = 0, nl = 0;
+  u32 mx = 0;
+  for (u64 i = lo + threadIdx.x; i < hi; i += TT) {
+    const u64 k = ldcg64(&lkey[i]);
+    if (k != EMPTY64) {
+      const u32 c = ldcg32(&lcnt[i]);
+      sm += c; nl += 1; mx = max(mx, c);
+      atomicAdd(&h[0][node_owner((u32)(k >> 32), world)], 1u);
+      atomicAdd(&h[1][node_owner((u32)k, world)], 1u);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && esc[0]) {
+    const u32 c = esc[0];
+    sm += c; nl += 1; mx = max(mx, c);
+    atomicAdd(&h[0][node_owner(EMPTY32, world)], 1u);
+    atomicAdd(&h[1][node_owner(EMPTY32, world)], 1u);
+  }
+  if (sm) atomicAdd(&s_sum, sm);
+  if (nl) atomicAdd(&s_links, nl);
+  if (mx) atomicMax(&s_max, (unsigned long long)mx);
+  __syncthreads();
+  for (u32 o = threadIdx.x; o < world; o += TT) {
+    ccount[((u64)blockIdx.x * 2 + 0) * world + o] = h[0][o];
+    ccount[((u64)blockIdx.x * 2 + 1) * world + o] = h[1][o];
+  }
+  if (threadIdx.x == 0) {
+    if (s_sum) atomicAdd(&acc[0], s_sum);
+    if (s_links) atomicAdd(&acc[1], s_links);
+    if (s_max) atomicMax(&acc[2], s_max);
+  }
+}
+
+__device__ __forceinline__ u64 link_rec(u32 node, u32 c) { return ((u64)node << 32) | c; }
+
+__global__ void __launch_bounds__(TT) trace_link_emit(const u64* __restrict__ lkey, const u32* __restrict__ lcnt,
+                                                      u64 LC, const u32* __restrict__ esc, u32 world,
+                                                      const u64* __restrict__ coff, u64* __restrict__ rec_src,
+                                                      u64* __restrict__ rec_dst) {
+  __shared__ u64 base[2][TRACE_MAX_WORLD];
+  __shared__ u32 cur[2][TRACE_MAX_WORLD];
+  for (u32 o = threadIdx.x; o < world; o += TT) {
+    base[0][o] = coff[((u64)blockIdx.x * 2 + 0) * world + o];
+    base[1][o] = coff[((u64)blockIdx.x * 2 + 1) * world + o];
+    cur[0][o] = 0;
+    cur[1][o] = 0;
+  }
+  __syncthreads();
+  u64 lo, hi;
+  cta_range(LC, lo, hi);
+  for (u64 i = lo + threadIdx.x; i < hi; i += TT) {
+    const u64 k = ldcg64(&lkey[i]);
+    if (k != EMPTY64) {
+      const u32 c = ldcg32(&lcnt[i]);
+      const u32 s = (u32)(k >> 32), d = (u32)k;
+      const u32 os = node_owner(s, world), od = node_owner(d, world);
+      rec_src[base[0][os] + atomicAdd(&cur[0][os], 1u)] = link_rec(s, c);
+      rec_dst[base[1][od] + atomicAdd(&cur[1][od], 1u)] = link_rec(d, c);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && esc[0]) {
+    const u32 o = node_owner(EMPTY32, world);
+    rec_src[base[0][o] + atomicAdd(&cur[0][o], 1u)] = link_rec(EMPTY32, esc[0]);
+    rec_dst[base[1][o] + atomicAdd(&cur[1][o], 1u)] = link_rec(EMPTY32, esc[0]);
+  }
+}
+
+// ---- nodes: merge the records of one side; unique nodes, max packets (:186), max fan (:188)
+__global__ void __launch_bounds__(TT) trace_node_insert(const u64* __restrict__ rec, u64 m, u32* __restrict__ nkey,
+                                                        u32* __restrict__ nP, u32* __restrict__ nF, u64 NC,
+                                                        u32* __restrict__ esc) {
+  for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < m; i += (u64)gridDim.x * TT) {
+    const u64 r = rec[i];
+    glob_node_upsert(nkey, nP, nF, NC, &esc[0], &esc[1], (u32)(r >> 32), (u32)r, 1u);
+  }
+}
+
+// the same, with the record count read from device memory (single-rank trace: no host sync)
+__global__ void __launch_bounds__(TT) trace_node_insert_dev(const u64* __restrict__ rec, const u64* __restrict__ m_dev,
+                                                            u32* __restrict__ nkey, u32* __restrict__ nP,
+                                                            u32* __restrict__ nF, u64 NC, u32* __restrict__ esc) {
+  const u64 m = *m_dev;
+  for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < m; i += (u64)gridDim.x * TT) {
+    const u64 r = rec[i];
+    glob_node_upsert(nkey, nP, nF, NC, &esc[0], &esc[1], (u32)(r >> 32), (u32)r, 1u);
+  }
+}
+
+__global__ void __launch_bounds__(TT) trace_node_scan(const u32* __restrict__ nkey, const u32* __restrict__ nP,
+                                                      const u32* __restrict__ nF, u64 NC, const u32* __restrict__ esc,
+                                                      unsigned long long* __restrict__ acc) {
+  __shared__ unsigned long long s_n, s_p, s_f;
+  if (threadIdx.x == 0) { s_n = 0; s_p = 0; s_f = 0; }
+  __syncthreads();
+  unsigned long long nn = 0;
+  u32 mp = 0, mf = 0;
+  for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < NC; i += (u64)gridDim.x * TT) {
+    if (ldcg32(&nkey[i]) != EMPTY32) { nn += 1; mp = max(mp, ldcg32(&nP[i])); mf = max(mf, ldcg32(&nF[i])); }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && esc[1]) { nn += 1; mp = max(mp, esc[0]); mf = max(mf, esc[1]); }
+  if (nn) atomicAdd(&s_n, nn);
+  if (mp) atomicMax(&s_p, (unsigned long long)mp);
+  if (mf) atomicMax(&s_f, (unsigned long long)mf);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_n) atomicAdd(&acc[0], s_n);
+    if (s_p) atomicMax(&acc[1], s_p);
+    if (s_f) atomicMax(&acc[2], s_f);
+  }
+}
+
+// out[9] (north_star order) from the link partial [valid, links, max link] and the two node partials
+__global__ void trace_finish(const unsigned long long* __restrict__ lacc, const unsigned long long* __restrict__ sacc,
+                             const unsigned long long* __restrict__ dacc, u64* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    out[NSG_VALID_PACKETS] = lacc[0];
+    out[NSG_UNIQUE_LINKS] = lacc[1];
+    out[NSG_MAX_LINK_PACKETS] = lacc[2];
+    out[NSG_UNIQUE_SOURCES] = sacc[0];
+    out[NSG_MAX_SOURCE_PACKETS] = sacc[1];
+    out[NSG_MAX_SOURCE_FANOUT] = sacc[2];
+    out[NSG_UNIQUE_DESTINATIONS] = dacc[0];
+    out[NSG_MAX_DESTINATION_PACKETS] = dacc[1];
+    out[NSG_MAX_DESTINATION_FANIN] = dacc[2];
+  }
+}
+
+}  // namespace nsg

@@ -1,4 +1,5 @@
-"""Window-sharded multi-GPU driver.
+"""Multi-GPU drivers: window-sharded per-window statistics and the whole-trace
+statistics with key-hash all-to-all exchanges.
 
 Windows are independent units (Table 2 is evaluated per traffic matrix A_t, line 173), so
 rank r of R owns the contiguous window block [floor(r*Nw/R), floor((r+1)*Nw/R)) and computes it
@@ -63,3 +64,86 @@ def distributed_window_stats(keys_local: torch.Tensor, n_windows: int, window: i
 
     local = window_stats_packed(keys_local, window, workspace=workspace)
     return gather_window_stats(local, n_windows, group)
+
+
+
+# ---------------------------------------------------------------------------------------------------
+# Whole trace: A = sum over t of A_t over every rank's packets.  Links and nodes are
+# hash-partitioned over the ranks, so the only data-path collectives are the all-to-all exchanges of the
+# keys and of the link records; every aggregation step runs in libnsg's kernels (nsg_trace_*).
+# ---------------------------------------------------------------------------------------------------
+def _trace_partition(keys, world, ws):
+    from .api import trace_partition
+
+    return trace_partition(keys, world, ws)
+
+
+def _trace_links(keys, world, ws):
+    from .api import trace_links
+
+    return trace_links(keys, world, ws)
+
+
+def _trace_nodes(records, ws):
+    from .api import trace_nodes
+
+    return trace_nodes(records, ws)
+
+
+def _trace_workspace(key_cap, rec_cap, world, device):
+    from .api import TraceWorkspace
+
+    return TraceWorkspace(key_cap, rec_cap, world, device)
+
+
+def _exchange(send: torch.Tensor, counts: torch.Tensor, group=None) -> torch.Tensor:
+    """All-to-all of the owner-grouped `send` (segment o -> rank o, lengths `counts`): returns what every
+    rank sent here, in rank order.  NCCL moves device tensors directly; gloo stages them through host memory."""
+    world = dist.get_world_size(group)
+    home = send.device
+    gloo = dist.get_backend(group) == "gloo"
+    c = counts.cpu() if gloo else counts
+    rc = torch.empty_like(c)
+    dist.all_to_all_single(rc, c.contiguous(), group=group)
+    ins, outs = counts.cpu().tolist(), rc.cpu().tolist()
+    src = send[: sum(ins)]
+    if gloo:
+        src = src.cpu()
+    recv = torch.empty(sum(outs), dtype=send.dtype, device=src.device)
+    if world == 1:
+        recv.copy_(src)
+    else:
+        dist.all_to_all_single(recv, src.contiguous(), output_split_sizes=outs, input_split_sizes=ins, group=group)
+    return recv.to(home)
+
+
+def distributed_trace_stats(keys_local: torch.Tensor, group=None) -> torch.Tensor:
+    """The nine statistics of the whole trace held across the ranks (this rank's packets: packed int64 keys
+    on its GPU).  Steps: partition by link owner -> all-to-all -> links -> all-to-all of the source and of the
+    destination records -> nodes per side -> sum / max over ranks.  Returns int64 [9] on every rank (on the
+    keys' device), north_star column order."""
+    world = dist.get_world_size(group)
+    device = keys_local.device
+    n = keys_local.numel()
+    ws = _trace_workspace(max(n, 1), 1, world, device)
+    send, counts = _trace_partition(keys_local, world, ws)
+    mine = _exchange(send, counts, group)
+    m = mine.numel()
+    ws = _trace_workspace(max(m, 1), 1, world, device)
+    link_stats, rs, rd, rc = _trace_links(mine, world, ws)
+    rec_s = _exchange(rs, rc[0], group)
+    rec_d = _exchange(rd, rc[1], group)
+    ws = _trace_workspace(1, max(rec_s.numel(), rec_d.numel(), 1), 1, device)
+    ns = _trace_nodes(rec_s, ws)
+    nd = _trace_nodes(rec_d, ws)
+    # sums: valid, unique links, unique sources, unique destinations; maxes: the rest
+    sums = torch.stack([link_stats[0], link_stats[1], ns[0], nd[0]])
+    maxes = torch.stack([link_stats[2], ns[1], ns[2], nd[1], nd[2]])
+    if world > 1:
+        gloo = dist.get_backend(group) == "gloo"
+        sums_c, maxes_c = (sums.cpu(), maxes.cpu()) if gloo else (sums, maxes)
+        dist.all_reduce(sums_c, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(maxes_c, op=dist.ReduceOp.MAX, group=group)
+        sums, maxes = sums_c.to(device), maxes_c.to(device)
+    out = torch.stack([sums[0], sums[1], maxes[0], sums[2], maxes[1], maxes[2], sums[3], maxes[3], maxes[4]])
+    return out

@@ -76,3 +76,81 @@ def test_gather_matches_single_process(n):
     want = oracle.window_stats_sort(keys=keys, window=W).astype(np.int64)
     for r in range(world):
         assert np.array_equal(results[r], want)
+
+
+# ---------------------------------------------------------------------------------------------------
+# Whole-trace driver: the exchange / merge logic of distributed_trace_stats, with the
+# three kernel steps replaced by numpy stand-ins that keep their contracts (test doubles: the product
+# steps are the CUDA kernels, exercised by tests/test_gpu_trace.py).  The stand-ins use their own owner
+# functions; the driver never computes owners itself.
+# ---------------------------------------------------------------------------------------------------
+def _owner64(k, world):
+    return ((k.astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15)) >> np.uint64(40)) % np.uint64(world)
+
+
+def _fake_partition(keys, world, ws):
+    k = keys.numpy().view(np.uint64)
+    o = _owner64(k, world)
+    order = np.argsort(o, kind="stable")
+    counts = np.bincount(o.astype(np.int64), minlength=world)
+    return torch.from_numpy(k[order].view(np.int64).copy()), torch.from_numpy(counts.astype(np.int64))
+
+
+def _fake_links(keys, world, ws):
+    k = keys.numpy().view(np.uint64)
+    u, c = np.unique(k, return_counts=True)
+    stats = torch.tensor([int(c.sum()), u.size, int(c.max()) if c.size else 0], dtype=torch.int64)
+    recs, counts = [], []
+    for node in (u >> np.uint64(32), u & np.uint64(0xFFFFFFFF)):
+        r = (node << np.uint64(32)) | c.astype(np.uint64)
+        o = _owner64(node + np.uint64(7), world)
+        order = np.argsort(o, kind="stable")
+        recs.append(torch.from_numpy(r[order].view(np.int64).copy()))
+        counts.append(np.bincount(o.astype(np.int64), minlength=world))
+    return stats, recs[0], recs[1], torch.from_numpy(np.stack(counts).astype(np.int64))
+
+
+def _fake_nodes(records, ws):
+    r = records.numpy().view(np.uint64)
+    if r.size == 0:
+        return torch.zeros(3, dtype=torch.int64)
+    node, c = r >> np.uint64(32), r & np.uint64(0xFFFFFFFF)
+    u, inv = np.unique(node, return_inverse=True)
+    P = np.bincount(inv, weights=c.astype(np.float64)).astype(np.int64)
+    F = np.bincount(inv)
+    return torch.tensor([u.size, int(P.max()), int(F.max())], dtype=torch.int64)
+
+
+def _trace_worker(rank, world, port, n, q):
+    import paper_2509_03653_b200.distributed as D
+
+    D._trace_partition, D._trace_links, D._trace_nodes = _fake_partition, _fake_links, _fake_nodes
+    D._trace_workspace = lambda *a: None
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p0, p1 = (n * rank) // world, (n * (rank + 1)) // world
+        keys = gen.generate_host(gen.Dist("zipf", 1.1, 1 << 12), 5, p0, p1 - p0, packed=True)
+        out = D.distributed_trace_stats(torch.from_numpy(keys.view(np.int64)))
+        q.put((rank, out.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 50_000), (3, 20_001), (2, 1)])
+def test_trace_driver_matches_whole_trace_oracle(world, n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_trace_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    keys = gen.generate_host(gen.Dist("zipf", 1.1, 1 << 12), 5, 0, n, packed=True)
+    want = oracle.window_stats_sort(keys=keys, window=n)[0].astype(np.int64)   # the whole trace: one window
+    for r in range(world):
+        assert results[r].tolist() == want.tolist()
