@@ -16,6 +16,7 @@ Three procedures, each citing PAPER.md (= /root/reference/PAPER.md, arXiv 2509.0
   ``window_distributions_dense`` is its dense O0 counterpart (dense.py).
 * ``window_stats_weighted`` — O1w, O1 on weighted rows (src, dst, n_packets): the paper's three-column
   frame (:207; valid packets = sum of n_packets, :180); rows of weight 0 add nothing.
+* ``anonymize`` — the IP anonymisation of PAPER.md:195-203 (unique, keyed permutation, gather; anon.py).
 * ``window_stats_dense`` — O0, the "Matrix notation" column evaluated literally on a dense
   matrix after relabelling the (few) addresses of a tiny window (dense.py).
 
@@ -33,6 +34,7 @@ import threading
 
 import numpy as np
 
+from .anon import anonymize  # noqa: F401
 from .dense import window_distributions_dense, window_stats_dense  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
