@@ -188,6 +188,11 @@ def main():
     ap.add_argument("--workload", default="C2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--once", action="store_true", help="a single untimed call (for ncu)")
+    ap.add_argument("--path", choices=["windows", "trace", "anonymize"], default="windows",
+                    help="windows: per-window statistics (north_star); trace: the whole-trace statistics of each "
+                         "step's packets (nsg_trace_stats; N>1: distributed_trace_stats with all-to-all exchanges, "
+                         "SURVEY §8(f) f4b); anonymize: relabel every address of each step's packets "
+                         "(nsg_anonymize, one shuffle round, SURVEY §8(f) f2)")
     ap.add_argument("--input", choices=["packets", "weighted"], default="packets",
                     help="packets: raw packets (north_star); weighted: rows (src, dst, n_packets) with n_packets "
                          "uniform in [1, 8] (nsg_window_stats_weighted, SURVEY §8(f) f4a); unit = rows/s")
@@ -235,6 +240,13 @@ def main():
     outs = [torch.empty((WINDOWS_PER_STEP, 9), dtype=torch.int64, device=dev) for _ in range(RING)]
     vec = args.outputs == "vectors"
     wtd = args.input == "weighted"
+    trace = args.path == "trace"
+    anon = args.path == "anonymize"
+    if anon and (vec or wtd or world > 1):
+        raise SystemExit("--path anonymize: one GPU, --input packets --outputs stats only")
+    if trace and (vec or wtd):
+        raise SystemExit("--path trace supports --input packets --outputs stats only")
+    from paper_2509_03653_b200.distributed import distributed_trace_stats
     if wtd and vec:
         raise SystemExit("--input weighted supports --outputs stats only")
     wring = None
@@ -252,6 +264,20 @@ def main():
         return 0
 
     def step(i, evs=None):
+        if anon:  # events around the whole call (bitmap reset + mark + rank prefix + relabel)
+            if evs:
+                evs[0].record()
+            r = nsg.anonymize(ring[i % RING], seed=i, rounds=1)
+            if evs:
+                evs[1].record()
+            return r
+        if trace:  # events around the whole call (table resets + the trace kernels [+ exchanges])
+            if evs:
+                evs[0].record()
+            r = nsg.trace_stats(ring[i % RING]) if world == 1 else distributed_trace_stats(ring[i % RING])
+            if evs:
+                evs[1].record()
+            return r
         if vec:  # events around the whole call (workspace reset + persistent kernel + overflow check)
             if evs:
                 evs[0].record()
@@ -321,6 +347,23 @@ def main():
             for k, t in vhost.items():
                 t.copy_(r[k], non_blocking=True)
         d2h_bytes = WINDOWS_PER_STEP * 9 * 8 + sum(t.numel() * t.element_size() for t in vhost.values())
+    elif anon:  # H2D of the packets, the call, D2H of the relabelled src/dst and N
+        ahost = torch.empty((2, n), dtype=torch.int32, pin_memory=True)
+
+        def e2e_once():
+            keys_dev.copy_(host, non_blocking=True)
+            a, b, _ = nsg.anonymize(keys_dev, seed=1, rounds=1)
+            ahost[0].copy_(a, non_blocking=True)
+            ahost[1].copy_(b, non_blocking=True)
+        d2h_bytes = 8 * n + 8
+    elif trace:  # H2D of the packets, the whole-trace call, D2H of the nine statistics
+        tout_host = torch.empty(9, dtype=torch.int64, pin_memory=True)
+
+        def e2e_once():
+            keys_dev.copy_(host, non_blocking=True)
+            r = nsg.trace_stats(keys_dev) if world == 1 else distributed_trace_stats(keys_dev)
+            tout_host.copy_(r, non_blocking=True)
+        d2h_bytes = 9 * 8
     elif wtd:  # H2D of the rows (keys + n_packets), the call, D2H of the statistics
         whost = wring[0].cpu().pin_memory()
         wdev = torch.empty(n, dtype=torch.int32, device=dev)
@@ -362,24 +405,32 @@ def main():
             alg_bytes += 12 * cnt + 32 * WINDOWS_PER_STEP
         achieved = alg_bytes / (k_avg / 1e3) / 1e9
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
+        if anon:  # the relabelled src/dst are written: 8 B/packet more
+            alg_bytes += n * 8
+        if world == 1 and not args.no_cpu_baseline and not (trace or anon):
             cpu = cpu_baseline(dist_, seed)
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "metric": METRIC, "value": value, "unit": "rows/s" if wtd else UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": desc + f"; {WINDOWS_PER_STEP} windows x 2^17 packets per GPU per step (C2 batch)"
                        + ("; outputs: stats + link/source/destination vectors + IP sets" if vec else "")
-                       + ("; weighted rows (src, dst, n_packets ~ U[1,8]), unit rows/s" if wtd else ""),
+                       + ("; weighted rows (src, dst, n_packets ~ U[1,8]), unit rows/s" if wtd else "")
+                       + ("; WHOLE-TRACE statistics of each step's packets (all ranks' packets together)"
+                          if trace else "")
+                       + ("; ANONYMISATION of each step's packets (unique, 1 Feistel shuffle round, gather); "
+                          "8 B/packet written" if anon else ""),
                        "window": WINDOW, "packets_per_gpu_per_step": n, "parallelism": f"windows sharded dp{world}",
                        "l2": f"inputs larger than L2: ring of {RING} x {n * 8 >> 20} MiB batches per GPU, no flush",
                        "input": "device-resident packed u64 keys (src<<32|dst)"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * (12 if wtd else 8),
+            "e2e": {"value": e2e_value, "unit": "rows/s" if wtd else UNIT, "h2d_bytes_per_step": n * (12 if wtd else 8),
                     "d2h_bytes_per_step": d2h_bytes, "steps": e2e_steps},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic_per_launch(args.workload + ("-vectors" if vec else "-weighted" if wtd else "")), "peak_source": peak_src,
-                         "kernel": "nsg::fast_kernel" + (" (+ reset and overflow-check launches: events around "
-                                                          "the whole call)" if (vec or wtd) else ""),
+                         "traffic": traffic_per_launch(args.workload + ("-vectors" if vec else "-weighted" if wtd else "-trace" if trace else "-anonymize" if anon else "")), "peak_source": peak_src,
+                         "kernel": ("nsg::anon_* (512 MiB bitmap; events around the whole call)" if anon else
+                                    "nsg::trace_* (HBM tables; events around the whole call)" if trace else
+                                    "nsg::fast_kernel" + (" (+ reset and overflow-check launches: events around "
+                                                          "the whole call)" if (vec or wtd) else "")),
                          "kernel_ms_avg": k_avg,
                          "algorithmic_bytes_per_launch": alg_bytes},
             "cpu_baseline": cpu,

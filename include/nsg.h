@@ -226,6 +226,22 @@ size_t nsg_trace_stats_workspace_bytes(uint64_t n_packets);
 nsg_status nsg_trace_stats(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
                            uint64_t* out, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- IP address anonymisation ------------------------------
+ * For the whole input: U = the distinct addresses of src and dst in ascending order, N = |U| (PAPER.md:199,
+ * "the number of unique value of src and dest ids"); rank(a) = index of a in U; pi = a keyed pseudo-random
+ * permutation of [0, N) standing for the paper's shuffle of 0..N-1 (reading R15:
+ * per round k < rounds a 4-round Feistel network on the smallest even-bit domain >= N, keyed by
+ * splitmix64(seed + k), cycle-walked into [0, N); rounds = 0 is the identity, i.e. labels = ranks); then
+ * the gather: src_out[p] = pi(rank(src_p)), dst_out[p] = pi(rank(dst_p)).  Every Table 2
+ * quantity of the relabelled stream equals the original's (the paper's anonymisation argument).
+ *   src_out, dst_out  device u32[n_packets]; n_unique device u64[1] (N).  Input as nsg_window_stats_ex.
+ *   workspace         device, 256 B aligned, nsg_anonymize_workspace_bytes() (a 2^32-bit bitmap + prefixes).
+ * Asynchronous on `stream`; errors as nsg_window_stats_ex. */
+size_t nsg_anonymize_workspace_bytes(void);
+nsg_status nsg_anonymize(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
+                         uint64_t seed, uint32_t rounds, uint32_t* src_out, uint32_t* dst_out, uint64_t* n_unique,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
 /* Diagnostics of the last call that used `workspace` (device memory; read it after the stream has
  * completed the call): byte offset inside the workspace of a u32[4] =
  *   {windows the fast path handed to the L2 path because an SMEM table would overflow,

@@ -20,6 +20,7 @@ from .api import (  # noqa: F401
     STAT_NAMES,
     TraceWorkspace,
     Workspace,
+    anonymize,
     last_launches,
     num_windows,
     trace_links,

@@ -13,7 +13,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.path.join(_PKG, "libnsg.so")
 SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("nsg.cu", "nsg_common.cuh", "nsg_fast.cuh", "nsg_global.cuh",
-                                                   "nsg_trace.cuh")]
+                                                   "nsg_trace.cuh", "nsg_anon.cuh")]
 HEADER = os.path.join(ROOT, "include", "nsg.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
@@ -35,6 +35,8 @@ EXPORTS = (
     "nsg_trace_nodes",
     "nsg_trace_stats_workspace_bytes",
     "nsg_trace_stats",
+    "nsg_anonymize_workspace_bytes",
+    "nsg_anonymize",
     "nsg_diag_offset",
     "nsg_last_launches",
     "nsg_status_string",
@@ -114,6 +116,10 @@ def load() -> ctypes.CDLL:
     lib.nsg_trace_stats_workspace_bytes.argtypes = [u64]
     lib.nsg_trace_stats.restype = ctypes.c_int
     lib.nsg_trace_stats.argtypes = [vp, vp, vp, u64, vp, vp, sz, vp]
+    lib.nsg_anonymize_workspace_bytes.restype = sz
+    lib.nsg_anonymize_workspace_bytes.argtypes = []
+    lib.nsg_anonymize.restype = ctypes.c_int
+    lib.nsg_anonymize.argtypes = [vp, vp, vp, u64, u64, u32, vp, vp, vp, vp, sz, vp]
     lib.nsg_diag_offset.restype = sz
     lib.nsg_diag_offset.argtypes = []
     lib.nsg_last_launches.restype = ctypes.c_uint

@@ -446,3 +446,30 @@ def trace_nodes(records: torch.Tensor, workspace: TraceWorkspace, stream=None) -
     if rc != 0:
         raise NsgError(rc, "nsg_trace_nodes")
     return stats
+
+
+
+# ---------------------------------------------------------------------------------------------------
+# IP address anonymisation
+# ---------------------------------------------------------------------------------------------------
+_anon_ws: dict = {}
+
+
+def anonymize(keys: Optional[torch.Tensor] = None, *, src=None, dst=None, seed: int = 0, rounds: int = 1,
+              stream=None):
+    """Relabel every address by pi(rank(address)) (nsg_anonymize): rank = index among the distinct addresses
+    of src and dst (ascending), pi = the keyed permutation of DESIGN.md R15 (`rounds` Feistel rounds; 0 = the
+    ranks themselves).  Returns (src_out int32 [n], dst_out int32 [n], n_unique int64 [1]) on the device."""
+    n, device = _rows(keys, src, dst)
+    so = torch.empty(n, dtype=torch.int32, device=device)
+    do = torch.empty(n, dtype=torch.int32, device=device)
+    nu = torch.zeros(1, dtype=torch.int64, device=device)
+    ws = _anon_ws.get(device.index)
+    if ws is None:
+        ws = _anon_ws[device.index] = _Scratch(_lib.nsg_anonymize_workspace_bytes(), device)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_anonymize(_p(src), _p(dst), _p(keys), n, int(seed) & (2 ** 64 - 1), int(rounds), so.data_ptr(),
+                            do.data_ptr(), nu.data_ptr(), ws.ptr, ws.nbytes, ctypes.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise NsgError(rc, "nsg_anonymize")
+    return so, do, nu

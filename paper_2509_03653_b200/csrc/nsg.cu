@@ -11,6 +11,7 @@
 //                    SMEM hash tables, exchange through L2-resident scratch).
 //   nsg_global.cuh — any window <= 2^31 and the fast path's overflow hand-off: one CTA per window
 //                    with global-memory hash tables.
+//   nsg_anon.cuh   — IP address anonymisation (bitmap unique + rank, keyed permutation, gather).
 //   nsg_trace.cuh  — the whole-trace path (A = sum of the A_t): HBM-resident tables filled by every SM,
 //                    in steps a multi-GPU driver interleaves with all-to-all exchanges.
 // This file holds the C ABI: argument checks, workspace layout, launches.
@@ -21,6 +22,7 @@
 #include "nsg_fast.cuh"
 #include "nsg_global.cuh"
 #include "nsg_trace.cuh"
+#include "nsg_anon.cuh"
 
 #include <cstdio>
 #include <cstring>
@@ -644,6 +646,44 @@ nsg_status nsg_trace_stats(const uint32_t* src, const uint32_t* dst, const uint6
                                        reinterpret_cast<unsigned long long*>(part + 4),
                                        reinterpret_cast<unsigned long long*>(part + 8), reinterpret_cast<nsg::u64*>(out));
   nsg::g_last_launches += 1;
+  return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
+}
+
+size_t nsg_anonymize_workspace_bytes(void) {
+  return nsg::ANON_WORDS * 4 + nsg::ANON_BLOCKS * 4 + nsg::ANON_SCAN_CTAS * 4;
+}
+
+nsg_status nsg_anonymize(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
+                         uint64_t seed, uint32_t rounds, uint32_t* src_out, uint32_t* dst_out, uint64_t* n_unique,
+                         void* workspace, size_t workspace_bytes, void* stream) {
+  nsg::g_last_launches = 0;
+  if (!n_unique || (reinterpret_cast<uintptr_t>(n_unique) & 7)) return NSG_ERR_INVALID_ARGUMENT;
+  if (n_packets && !nsg::input_ok(src, dst, reinterpret_cast<const nsg::u64*>(keys))) return NSG_ERR_INVALID_ARGUMENT;
+  if (n_packets && (!src_out || !dst_out || (reinterpret_cast<uintptr_t>(src_out) & 3) ||
+                    (reinterpret_cast<uintptr_t>(dst_out) & 3)))
+    return NSG_ERR_INVALID_ARGUMENT;
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & 255)) return NSG_ERR_INVALID_ARGUMENT;
+  if (workspace_bytes < nsg_anonymize_workspace_bytes()) return NSG_ERR_WORKSPACE_TOO_SMALL;
+  nsg::DevInfo d;
+  const nsg_status st = nsg::dev_info(d);
+  if (st != NSG_OK) return st;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  unsigned char* base = reinterpret_cast<unsigned char*>(workspace);
+  nsg::u32* bitmap = reinterpret_cast<nsg::u32*>(base);
+  nsg::u32* bpre = reinterpret_cast<nsg::u32*>(base + nsg::ANON_WORDS * 4);
+  nsg::u32* ctot = bpre + nsg::ANON_BLOCKS;
+  nsg::u64* nu = reinterpret_cast<nsg::u64*>(n_unique);
+  const nsg::u64* k = reinterpret_cast<const nsg::u64*>(keys);
+  if (cudaMemsetAsync(bitmap, 0, nsg::ANON_WORDS * 4, s) != cudaSuccess) return NSG_ERR_CUDA;
+  const unsigned grid = (unsigned)(d.sms * (2048 / nsg::AT));
+  if (n_packets) nsg::anon_mark_kernel<<<grid, nsg::AT, 0, s>>>(k, src, dst, n_packets, bitmap);
+  nsg::anon_block_count<<<nsg::ANON_SCAN_CTAS, nsg::AT, 0, s>>>(bitmap, bpre, ctot);
+  nsg::anon_scan_totals<<<1, 1024, 0, s>>>(ctot, nu);
+  nsg::anon_block_prefix<<<nsg::ANON_SCAN_CTAS, nsg::AT, 0, s>>>(bpre, ctot);
+  if (n_packets)
+    nsg::anon_relabel_kernel<<<grid, nsg::AT, 0, s>>>(k, src, dst, n_packets, bitmap, bpre, nu, seed, rounds,
+                                                      src_out, dst_out);
+  nsg::g_last_launches = n_packets ? 5 : 3;
   return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }
 

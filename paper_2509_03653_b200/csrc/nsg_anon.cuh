@@ -1,0 +1,186 @@
+// nsg_anon.cuh — IP address anonymisation.
+//
+// The paper: "Given an array of length N, we generate the sequence array with the values 0,1,..,N-1,
+// followed by the use of the Python shuffle operation ... The shuffled array is then used to assign new
+// values to the original source and destination IP addresses using gather instructions.  The size N ...
+// [is] the number of unique value of src and dest ids"; several shuffle rounds may be
+// applied.  This path computes, for the whole input:
+//   U      = the distinct addresses of src and dst, in ascending order; N = |U|       ("unique")
+//   rank(a)= the index of address a in U
+//   pi     = a keyed pseudo-random permutation of [0, N) (reading R15: a 4-round Feistel network
+//            on the smallest even-bit domain >= N with cycle walking, one network per shuffle round, in
+//            place of the host shuffle; it is deterministic and needs no table, cf. the deterministic
+//            HashGraph permutation the paper cites)
+//   src'_p = pi(rank(src_p)), dst'_p = pi(rank(dst_p))                                 ("gather")
+// U is never materialised: membership is a 2^32-bit bitmap (512 MiB) in the workspace and rank(a) is the
+// number of set bits below a (a per-1024-bit-block exclusive prefix plus in-block popcounts).
+#pragma once
+#include "nsg.h"
+#include "nsg_common.cuh"
+
+namespace nsg {
+
+constexpr int AT = 512;                          // threads per CTA
+constexpr u64 ANON_WORDS = 1ull << 27;           // u32 words of the 2^32-bit bitmap
+constexpr u64 ANON_BLOCKS = ANON_WORDS / 32;     // 1024-bit blocks (2^22)
+constexpr u32 ANON_SCAN_PER_CTA = 4096;          // blocks per CTA in the prefix scan
+constexpr u32 ANON_SCAN_CTAS = (u32)(ANON_BLOCKS / ANON_SCAN_PER_CTA);  // 1024
+
+__device__ __forceinline__ u64 anon_mix(u64 z) {  // splitmix64
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// One keyed Feistel permutation of [0, N) (N >= 1): 4 rounds on 2h-bit values (2^(2h) >= N, h >= 1),
+// round function f_j(R) = low h bits of splitmix64(key ^ (j << 56) ^ R), cycle-walked into [0, N).
+__device__ __forceinline__ u64 anon_feistel(u64 x, u64 N, u64 key) {
+  u32 bits = 64 - __clzll((long long)(N - 1));  // ceil(log2 N) for N >= 2; 0 for N = 1
+  if (bits < 2) bits = 2;
+  const u32 h = (bits + 1) >> 1;
+  const u64 mask = (1ull << h) - 1;
+  do {
+    u64 L = x >> h, R = x & mask;
+#pragma unroll
+    for (u32 j = 0; j < 4; ++j) {
+      const u64 t = L ^ (anon_mix(key ^ ((u64)j << 56) ^ R) & mask);
+      L = R;
+      R = t;
+    }
+    x = (L << h) | R;
+  } while (x >= N);
+  return x;
+}
+
+__device__ __forceinline__ u64 anon_perm(u64 r, u64 N, u64 seed, u32 rounds) {
+  for (u32 k = 0; k < rounds; ++k) r = anon_feistel(r, N, anon_mix(seed + k));
+  return r;
+}
+
+__device__ __forceinline__ void anon_mark(u32* bitmap, u32 a) {
+  u32* w = &bitmap[a >> 5];
+  const u32 bit = 1u << (a & 31);
+  if (!(ldcg32(w) & bit)) atomicOr(w, bit);  // read first: repeated addresses cost no atomic
+}
+
+__global__ void __launch_bounds__(AT) anon_mark_kernel(const u64* __restrict__ keys, const u32* __restrict__ src,
+                                                       const u32* __restrict__ dst, u64 n, u32* __restrict__ bitmap) {
+  for (u64 i = (u64)blockIdx.x * AT + threadIdx.x; i < n; i += (u64)gridDim.x * AT) {
+    const u32 s = keys ? (u32)(keys[i] >> 32) : src[i];
+    const u32 d = keys ? (u32)keys[i] : dst[i];
+    anon_mark(bitmap, s);
+    anon_mark(bitmap, d);
+  }
+}
+
+// Set bits per 1024-bit block, then the exclusive prefix over blocks: per-CTA totals, a one-CTA scan of
+// the totals (N = their sum), per-CTA downsweep.
+__global__ void __launch_bounds__(AT) anon_block_count(const u32* __restrict__ bitmap, u32* __restrict__ bcnt,
+                                                       u32* __restrict__ ctot) {
+  __shared__ u32 red[AT / 32];
+  const u64 b0 = (u64)blockIdx.x * ANON_SCAN_PER_CTA;
+  u32 mine = 0;
+  for (u32 j = threadIdx.x; j < ANON_SCAN_PER_CTA; j += AT) {
+    const uint4* p = reinterpret_cast<const uint4*>(bitmap + (b0 + j) * 32);
+    u32 c = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint4 v = __ldcs(p + q);
+      c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
+    }
+    bcnt[b0 + j] = c;
+    mine += c;
+  }
+  mine = warp_sum(mine);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mine;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    u32 v = threadIdx.x < AT / 32 ? red[threadIdx.x] : 0u;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) ctot[blockIdx.x] = v;
+  }
+}
+
+__global__ void __launch_bounds__(1024) anon_scan_totals(u32* __restrict__ ctot, u64* __restrict__ n_unique) {
+  __shared__ u32 wsum[32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const u32 v = ctot[t];  // ANON_SCAN_CTAS == 1024 == blockDim.x
+  u32 x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    u32 s = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    wsum[lane] = s;
+  }
+  __syncthreads();
+  const u32 incl = x + (wid ? wsum[wid - 1] : 0u);
+  ctot[t] = incl - v;  // exclusive
+  if (t == 1023) *n_unique = (u64)(incl - v) + v;  // the exclusive prefix fits 32 bits even when N = 2^32
+}
+
+__global__ void __launch_bounds__(AT) anon_block_prefix(u32* __restrict__ bcnt, const u32* __restrict__ ctot) {
+  // in-CTA exclusive scan of this CTA's 4096 block counts (8 per thread), offset by the CTA prefix
+  __shared__ u32 wsum[AT / 32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  constexpr int PER = ANON_SCAN_PER_CTA / AT;
+  u32* b = bcnt + (u64)blockIdx.x * ANON_SCAN_PER_CTA + t * PER;
+  u32 v[PER], s = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) { v[q] = b[q]; s += v[q]; }
+  u32 x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    u32 w = lane < AT / 32 ? wsum[lane] : 0u;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < AT / 32) wsum[lane] = w;
+  }
+  __syncthreads();
+  u32 run = ctot[blockIdx.x] + (x - s) + (wid ? wsum[wid - 1] : 0u);
+#pragma unroll
+  for (int q = 0; q < PER; ++q) { b[q] = run; run += v[q]; }
+}
+
+// rank(a) = set bits of the bitmap below a
+__device__ __forceinline__ u64 anon_rank(const u32* __restrict__ bitmap, const u32* __restrict__ bpre, u32 a) {
+  const u32 blk = a >> 10, word = a >> 5;
+  u64 r = bpre[blk];
+  for (u32 w = blk << 5; w < word; ++w) r += __popc(ldcg32(&bitmap[w]));
+  return r + __popc(ldcg32(&bitmap[word]) & ((1u << (a & 31)) - 1u));
+}
+
+__global__ void __launch_bounds__(AT) anon_relabel_kernel(const u64* __restrict__ keys, const u32* __restrict__ src,
+                                                          const u32* __restrict__ dst, u64 n,
+                                                          const u32* __restrict__ bitmap, const u32* __restrict__ bpre,
+                                                          const u64* __restrict__ n_unique, u64 seed, u32 rounds,
+                                                          u32* __restrict__ src_out, u32* __restrict__ dst_out) {
+  const u64 N = *n_unique;
+  for (u64 i = (u64)blockIdx.x * AT + threadIdx.x; i < n; i += (u64)gridDim.x * AT) {
+    const u32 s = keys ? (u32)(keys[i] >> 32) : src[i];
+    const u32 d = keys ? (u32)keys[i] : dst[i];
+    src_out[i] = (u32)anon_perm(anon_rank(bitmap, bpre, s), N, seed, rounds);
+    dst_out[i] = (u32)anon_perm(anon_rank(bitmap, bpre, d), N, seed, rounds);
+  }
+}
+
+}  // namespace nsg
