@@ -13,7 +13,8 @@
 //            HashGraph permutation the paper cites)
 //   src'_p = pi(rank(src_p)), dst'_p = pi(rank(dst_p))                                 ("gather")
 // U is never materialised: membership is a 2^32-bit bitmap (512 MiB) in the workspace and rank(a) is the
-// number of set bits below a (a per-1024-bit-block exclusive prefix plus in-block popcounts).
+// number of set bits below a: an exclusive prefix per 128-bit group (128 MiB) plus the popcounts inside
+// a's group (one 128-bit load).
 #pragma once
 #include "nsg.h"
 #include "nsg_common.cuh"
@@ -22,8 +23,8 @@ namespace nsg {
 
 constexpr int AT = 512;                          // threads per CTA
 constexpr u64 ANON_WORDS = 1ull << 27;           // u32 words of the 2^32-bit bitmap
-constexpr u64 ANON_BLOCKS = ANON_WORDS / 32;     // 1024-bit blocks (2^22)
-constexpr u32 ANON_SCAN_PER_CTA = 4096;          // blocks per CTA in the prefix scan
+constexpr u64 ANON_BLOCKS = ANON_WORDS / 4;      // 128-bit groups (2^25)
+constexpr u32 ANON_SCAN_PER_CTA = 32768;         // groups per CTA in the prefix scan
 constexpr u32 ANON_SCAN_CTAS = (u32)(ANON_BLOCKS / ANON_SCAN_PER_CTA);  // 1024
 
 __device__ __forceinline__ u64 anon_mix(u64 z) {  // splitmix64
@@ -74,21 +75,17 @@ __global__ void __launch_bounds__(AT) anon_mark_kernel(const u64* __restrict__ k
   }
 }
 
-// Set bits per 1024-bit block, then the exclusive prefix over blocks: per-CTA totals, a one-CTA scan of
+// Set bits per 128-bit group, then the exclusive prefix over groups: per-CTA totals, a one-CTA scan of
 // the totals (N = their sum), per-CTA downsweep.
 __global__ void __launch_bounds__(AT) anon_block_count(const u32* __restrict__ bitmap, u32* __restrict__ bcnt,
                                                        u32* __restrict__ ctot) {
   __shared__ u32 red[AT / 32];
   const u64 b0 = (u64)blockIdx.x * ANON_SCAN_PER_CTA;
+  const uint4* p = reinterpret_cast<const uint4*>(bitmap);
   u32 mine = 0;
   for (u32 j = threadIdx.x; j < ANON_SCAN_PER_CTA; j += AT) {
-    const uint4* p = reinterpret_cast<const uint4*>(bitmap + (b0 + j) * 32);
-    u32 c = 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint4 v = __ldcs(p + q);
-      c += __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-    }
+    const uint4 v = __ldcg(p + b0 + j);  // kept in L2 for the relabel kernel
+    const u32 c = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
     bcnt[b0 + j] = c;
     mine += c;
   }
@@ -130,14 +127,16 @@ __global__ void __launch_bounds__(1024) anon_scan_totals(u32* __restrict__ ctot,
 }
 
 __global__ void __launch_bounds__(AT) anon_block_prefix(u32* __restrict__ bcnt, const u32* __restrict__ ctot) {
-  // in-CTA exclusive scan of this CTA's 4096 block counts (8 per thread), offset by the CTA prefix
+  // in-CTA exclusive scan of this CTA's group counts (PER contiguous per thread), offset by the CTA prefix
   __shared__ u32 wsum[AT / 32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   constexpr int PER = ANON_SCAN_PER_CTA / AT;
   u32* b = bcnt + (u64)blockIdx.x * ANON_SCAN_PER_CTA + t * PER;
-  u32 v[PER], s = 0;
-#pragma unroll
-  for (int q = 0; q < PER; ++q) { v[q] = b[q]; s += v[q]; }
+  u32 s = 0;
+  for (int q = 0; q < PER; q += 4) {
+    const uint4 v = *reinterpret_cast<const uint4*>(b + q);
+    s += v.x + v.y + v.z + v.w;
+  }
   u32 x = s;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -157,16 +156,27 @@ __global__ void __launch_bounds__(AT) anon_block_prefix(u32* __restrict__ bcnt, 
   }
   __syncthreads();
   u32 run = ctot[blockIdx.x] + (x - s) + (wid ? wsum[wid - 1] : 0u);
-#pragma unroll
-  for (int q = 0; q < PER; ++q) { b[q] = run; run += v[q]; }
+  for (int q = 0; q < PER; q += 4) {
+    uint4 v = *reinterpret_cast<const uint4*>(b + q);
+    uint4 o;
+    o.x = run; run += v.x;
+    o.y = run; run += v.y;
+    o.z = run; run += v.z;
+    o.w = run; run += v.w;
+    *reinterpret_cast<uint4*>(b + q) = o;
+  }
 }
 
-// rank(a) = set bits of the bitmap below a
+// rank(a) = set bits of the bitmap below a: the group prefix + the bits of a's group below a
 __device__ __forceinline__ u64 anon_rank(const u32* __restrict__ bitmap, const u32* __restrict__ bpre, u32 a) {
-  const u32 blk = a >> 10, word = a >> 5;
-  u64 r = bpre[blk];
-  for (u32 w = blk << 5; w < word; ++w) r += __popc(ldcg32(&bitmap[w]));
-  return r + __popc(ldcg32(&bitmap[word]) & ((1u << (a & 31)) - 1u));
+  const uint4 g = __ldcg(reinterpret_cast<const uint4*>(bitmap) + (a >> 7));
+  const u32 q = (a >> 5) & 3u, below = (1u << (a & 31)) - 1u;
+  u32 r = bpre[a >> 7];
+  r += q > 0 ? __popc(g.x) : __popc(g.x & below);
+  if (q >= 1) r += q > 1 ? __popc(g.y) : __popc(g.y & below);
+  if (q >= 2) r += q > 2 ? __popc(g.z) : __popc(g.z & below);
+  if (q == 3) r += __popc(g.w & below);
+  return r;
 }
 
 __global__ void __launch_bounds__(AT) anon_relabel_kernel(const u64* __restrict__ keys, const u32* __restrict__ src,
