@@ -100,14 +100,33 @@ __global__ void __launch_bounds__(TT) trace_part_scatter(const u64* __restrict__
 }
 
 // ---- links: A restricted to this rank's keys in a global table, then records per side and owner
+// Each CTA first aggregates in a direct-mapped SMEM cache (slot = top bits of an independent multiplicative
+// mix of the key): a packet whose key holds (or claims) its cache slot costs one SMEM atomic, so hot
+// links (Zipf) do not serialise on one global counter; the rest go to the global table at once, and the
+// cache is flushed (one global upsert per cached key) at the end.  Every packet is counted exactly once.
+constexpr int TCACHE = 4096;
 __global__ void __launch_bounds__(TT) trace_link_insert(const u64* __restrict__ keys, const u32* __restrict__ src,
                                                         const u32* __restrict__ dst, u64 n, u64* __restrict__ lkey,
                                                         u32* __restrict__ lcnt, u64 LC, u32* __restrict__ esc) {
+  __shared__ u64 ck[TCACHE];
+  __shared__ u32 cc[TCACHE];
+  for (int i = threadIdx.x; i < TCACHE; i += TT) { ck[i] = EMPTY64; cc[i] = 0; }
+  __syncthreads();
   for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < n; i += (u64)gridDim.x * TT) {
     const u64 k = load_key(keys, src, dst, i);
-    if (k == EMPTY64) atomicAdd(esc, 1u);  // the key ~0 is kept outside the table (reading R6)
+    if (k == EMPTY64) { atomicAdd(esc, 1u); continue; }  // the key ~0 is kept outside the table (reading R6)
+    const u32 cs = (u32)((k * 0x9E3779B97F4A7C15ull) >> 52);  // an independent mix: owner and table use hash64
+    u64 cur = ck[cs];
+    if (cur == EMPTY64) {
+      cur = atomicCAS(reinterpret_cast<unsigned long long*>(&ck[cs]), EMPTY64, k);
+      if (cur == EMPTY64) cur = k;
+    }
+    if (cur == k) atomicAdd(&cc[cs], 1u);
     else glob_link_insert(lkey, lcnt, LC, k, 1u);
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < TCACHE; i += TT)
+    if (ck[i] != EMPTY64) glob_link_insert(lkey, lcnt, LC, ck[i], cc[i]);
 }
 
 // Per CTA slot range: link statistics (valid = sum of counts, unique links, max link; PAPER.md:180, :181,
@@ -190,24 +209,45 @@ __global__ void __launch_bounds__(TT) trace_link_emit(const u64* __restrict__ lk
 }
 
 // ---- nodes: merge the records of one side; unique nodes, max packets (:186), max fan (:188)
+// Records of a node are merged in a per-CTA SMEM cache first, as trace_link_insert does for links (hot
+// sources / destinations would otherwise serialise on one global counter).
+__device__ __forceinline__ void node_records(const u64* __restrict__ rec, u64 m, u32* __restrict__ nkey,
+                                             u32* __restrict__ nP, u32* __restrict__ nF, u64 NC, u32* __restrict__ esc,
+                                             u32* ck, u32* cp, u32* cf) {
+  for (int i = threadIdx.x; i < TCACHE; i += TT) { ck[i] = EMPTY32; cp[i] = 0; cf[i] = 0; }
+  __syncthreads();
+  for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < m; i += (u64)gridDim.x * TT) {
+    const u64 r = rec[i];
+    const u32 node = (u32)(r >> 32), c = (u32)r;
+    if (node == EMPTY32) { atomicAdd(&esc[0], c); atomicAdd(&esc[1], 1u); continue; }
+    const u32 cs = (node * 0x9E3779B1u) >> (32 - 12);  // independent of the owner / table hashes (hash32)
+    u32 cur = ck[cs];
+    if (cur == EMPTY32) {
+      cur = atomicCAS(&ck[cs], EMPTY32, node);
+      if (cur == EMPTY32) cur = node;
+    }
+    if (cur == node) { atomicAdd(&cp[cs], c); atomicAdd(&cf[cs], 1u); }
+    else glob_node_upsert(nkey, nP, nF, NC, &esc[0], &esc[1], node, c, 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < TCACHE; i += TT)
+    if (ck[i] != EMPTY32) glob_node_upsert(nkey, nP, nF, NC, &esc[0], &esc[1], ck[i], cp[i], cf[i]);
+}
+static_assert(TCACHE == 4096, "node cache slot uses 12 hash bits");
+
 __global__ void __launch_bounds__(TT) trace_node_insert(const u64* __restrict__ rec, u64 m, u32* __restrict__ nkey,
                                                         u32* __restrict__ nP, u32* __restrict__ nF, u64 NC,
                                                         u32* __restrict__ esc) {
-  for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < m; i += (u64)gridDim.x * TT) {
-    const u64 r = rec[i];
-    glob_node_upsert(nkey, nP, nF, NC, &esc[0], &esc[1], (u32)(r >> 32), (u32)r, 1u);
-  }
+  __shared__ u32 ck[TCACHE], cp[TCACHE], cf[TCACHE];
+  node_records(rec, m, nkey, nP, nF, NC, esc, ck, cp, cf);
 }
 
 // the same, with the record count read from device memory (single-rank trace: no host sync)
 __global__ void __launch_bounds__(TT) trace_node_insert_dev(const u64* __restrict__ rec, const u64* __restrict__ m_dev,
                                                             u32* __restrict__ nkey, u32* __restrict__ nP,
                                                             u32* __restrict__ nF, u64 NC, u32* __restrict__ esc) {
-  const u64 m = *m_dev;
-  for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < m; i += (u64)gridDim.x * TT) {
-    const u64 r = rec[i];
-    glob_node_upsert(nkey, nP, nF, NC, &esc[0], &esc[1], (u32)(r >> 32), (u32)r, 1u);
-  }
+  __shared__ u32 ck[TCACHE], cp[TCACHE], cf[TCACHE];
+  node_records(rec, *m_dev, nkey, nP, nF, NC, esc, ck, cp, cf);
 }
 
 __global__ void __launch_bounds__(TT) trace_node_scan(const u32* __restrict__ nkey, const u32* __restrict__ nP,
