@@ -363,7 +363,7 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
 struct TLayout {
   u64 LC, NC;
   u32 grid, world;
-  size_t o_acc, o_ccount, o_coff, o_lkey, o_lcnt, o_nkey, o_nP, o_nF, total;
+  size_t o_acc, o_ccount, o_coff, o_lt, o_nt, total;
 };
 
 static TLayout trace_layout(u64 key_cap, u64 rec_cap, u32 world, int sms) {
@@ -377,11 +377,8 @@ static TLayout trace_layout(u64 key_cap, u64 rec_cap, u32 world, int sms) {
   T.o_acc = o; o = align256(o + 64 * sizeof(u64));  // u32 esc[0] (link key ~0), esc[2..3] (node ~0 P, F)
   T.o_ccount = o; o = align256(o + (size_t)T.grid * 2 * world * sizeof(u32));
   T.o_coff = o; o = align256(o + (size_t)T.grid * 2 * world * sizeof(u64));
-  T.o_lkey = o; o = align256(o + (size_t)T.LC * sizeof(u64));
-  T.o_lcnt = o; o = align256(o + (size_t)T.LC * sizeof(u32));
-  T.o_nkey = o; o = align256(o + (size_t)T.NC * sizeof(u32));
-  T.o_nP = o; o = align256(o + (size_t)T.NC * sizeof(u32));
-  T.o_nF = o; o = align256(o + (size_t)T.NC * sizeof(u32));
+  T.o_lt = o; o = align256(o + (size_t)T.LC * sizeof(LSlot));
+  T.o_nt = o; o = align256(o + (size_t)T.NC * sizeof(NSlot));
   T.total = o;
   return T;
 }
@@ -418,37 +415,33 @@ static nsg_status trace_links_impl(const u32* src, const u32* dst, const u64* ke
                                    u64* rec_src, u64* rec_dst, u64* rec_counts, TraceCall& c) {
   const TLayout& T = c.T;
   u32* esc = reinterpret_cast<u32*>(c.base + T.o_acc);
-  u64* lkey = reinterpret_cast<u64*>(c.base + T.o_lkey);
-  u32* lcnt = reinterpret_cast<u32*>(c.base + T.o_lcnt);
+  LSlot* lt = reinterpret_cast<LSlot*>(c.base + T.o_lt);
   u32* ccount = reinterpret_cast<u32*>(c.base + T.o_ccount);
   u64* coff = reinterpret_cast<u64*>(c.base + T.o_coff);
-  if (cudaMemsetAsync(esc, 0, 16, c.s) != cudaSuccess || cudaMemsetAsync(lkey, 0xFF, T.LC * 8, c.s) != cudaSuccess ||
-      cudaMemsetAsync(lcnt, 0, T.LC * 4, c.s) != cudaSuccess || cudaMemsetAsync(link_stats, 0, 24, c.s) != cudaSuccess)
+  if (cudaMemsetAsync(esc, 0, 16, c.s) != cudaSuccess || cudaMemsetAsync(link_stats, 0, 24, c.s) != cudaSuccess)
     return NSG_ERR_CUDA;
+  trace_fill<<<T.grid, TT, 0, c.s>>>(lt, T.LC, nullptr, 0);
   if (n) {
-    trace_link_insert<<<T.grid, TT, 0, c.s>>>(keys, src, dst, n, lkey, lcnt, T.LC, esc);
+    trace_link_insert<<<T.grid, TT, 0, c.s>>>(keys, src, dst, n, lt, T.LC, esc);
     g_last_launches++;
   }
-  trace_link_count<<<T.grid, TT, 0, c.s>>>(lkey, lcnt, T.LC, esc, world, ccount,
-                                           reinterpret_cast<unsigned long long*>(link_stats));
+  trace_link_count<<<T.grid, TT, 0, c.s>>>(lt, T.LC, esc, world, ccount, reinterpret_cast<unsigned long long*>(link_stats));
   trace_scan<<<1, TRACE_MAX_WORLD, 0, c.s>>>(ccount, T.grid, 2, world, coff, rec_counts);
-  trace_link_emit<<<T.grid, TT, 0, c.s>>>(lkey, lcnt, T.LC, esc, world, coff, rec_src, rec_dst);
-  g_last_launches += 3;
+  trace_link_emit<<<T.grid, TT, 0, c.s>>>(lt, T.LC, esc, world, coff, rec_src, rec_dst);
+  g_last_launches += 4;
   return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }
 
 static nsg_status trace_nodes_counted(const u64* rec, const u64* m_dev, u64* node_stats, TraceCall& c) {
   const TLayout& T = c.T;
   u32* esc = reinterpret_cast<u32*>(c.base + T.o_acc) + 2;
-  u32* nkey = reinterpret_cast<u32*>(c.base + T.o_nkey);
-  u32* nP = reinterpret_cast<u32*>(c.base + T.o_nP);
-  u32* nF = reinterpret_cast<u32*>(c.base + T.o_nF);
-  if (cudaMemsetAsync(esc, 0, 8, c.s) != cudaSuccess || cudaMemsetAsync(nkey, 0xFF, T.NC * 4, c.s) != cudaSuccess ||
-      cudaMemsetAsync(nP, 0, T.NC * 4, c.s) != cudaSuccess || cudaMemsetAsync(nF, 0, T.NC * 4, c.s) != cudaSuccess ||
-      cudaMemsetAsync(node_stats, 0, 24, c.s) != cudaSuccess)
+  NSlot* nt = reinterpret_cast<NSlot*>(c.base + T.o_nt);
+  if (cudaMemsetAsync(esc, 0, 8, c.s) != cudaSuccess || cudaMemsetAsync(node_stats, 0, 24, c.s) != cudaSuccess)
     return NSG_ERR_CUDA;
-  trace_node_insert_dev<<<T.grid, TT, 0, c.s>>>(rec, m_dev, nkey, nP, nF, T.NC, esc);
-  trace_node_scan<<<T.grid, TT, 0, c.s>>>(nkey, nP, nF, T.NC, esc, reinterpret_cast<unsigned long long*>(node_stats));
+  trace_fill<<<T.grid, TT, 0, c.s>>>(nullptr, 0, nt, T.NC);
+  g_last_launches++;
+  trace_node_insert_dev<<<T.grid, TT, 0, c.s>>>(rec, m_dev, nt, T.NC, esc);
+  trace_node_scan<<<T.grid, TT, 0, c.s>>>(nt, T.NC, esc, reinterpret_cast<unsigned long long*>(node_stats));
   g_last_launches += 2;
   return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }
@@ -456,18 +449,16 @@ static nsg_status trace_nodes_counted(const u64* rec, const u64* m_dev, u64* nod
 static nsg_status trace_nodes_impl(const u64* rec, u64 m, u64* node_stats, TraceCall& c) {
   const TLayout& T = c.T;
   u32* esc = reinterpret_cast<u32*>(c.base + T.o_acc) + 2;
-  u32* nkey = reinterpret_cast<u32*>(c.base + T.o_nkey);
-  u32* nP = reinterpret_cast<u32*>(c.base + T.o_nP);
-  u32* nF = reinterpret_cast<u32*>(c.base + T.o_nF);
-  if (cudaMemsetAsync(esc, 0, 8, c.s) != cudaSuccess || cudaMemsetAsync(nkey, 0xFF, T.NC * 4, c.s) != cudaSuccess ||
-      cudaMemsetAsync(nP, 0, T.NC * 4, c.s) != cudaSuccess || cudaMemsetAsync(nF, 0, T.NC * 4, c.s) != cudaSuccess ||
-      cudaMemsetAsync(node_stats, 0, 24, c.s) != cudaSuccess)
+  NSlot* nt = reinterpret_cast<NSlot*>(c.base + T.o_nt);
+  if (cudaMemsetAsync(esc, 0, 8, c.s) != cudaSuccess || cudaMemsetAsync(node_stats, 0, 24, c.s) != cudaSuccess)
     return NSG_ERR_CUDA;
+  trace_fill<<<T.grid, TT, 0, c.s>>>(nullptr, 0, nt, T.NC);
+  g_last_launches++;
   if (m) {
-    trace_node_insert<<<T.grid, TT, 0, c.s>>>(rec, m, nkey, nP, nF, T.NC, esc);
+    trace_node_insert<<<T.grid, TT, 0, c.s>>>(rec, m, nt, T.NC, esc);
     g_last_launches++;
   }
-  trace_node_scan<<<T.grid, TT, 0, c.s>>>(nkey, nP, nF, T.NC, esc, reinterpret_cast<unsigned long long*>(node_stats));
+  trace_node_scan<<<T.grid, TT, 0, c.s>>>(nt, T.NC, esc, reinterpret_cast<unsigned long long*>(node_stats));
   g_last_launches++;
   return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }

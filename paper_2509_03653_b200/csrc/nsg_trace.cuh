@@ -38,6 +38,45 @@ __device__ __forceinline__ u64 load_key(const u64* keys, const u32* src, const u
   return keys ? keys[i] : (((u64)src[i] << 32) | dst[i]);
 }
 
+// HBM tables with one 16-byte slot per entry (key and counters in the same 32-byte sector: one DRAM
+// access per probe instead of one per array)
+struct __align__(16) LSlot { u64 key; u32 cnt; u32 pad; };
+struct __align__(16) NSlot { u32 key, P, F, pad; };
+
+__global__ void __launch_bounds__(TT) trace_fill(LSlot* __restrict__ lt, u64 LC, NSlot* __restrict__ nt, u64 NC) {
+  for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < LC; i += (u64)gridDim.x * TT)
+    reinterpret_cast<ulonglong2*>(lt)[i] = make_ulonglong2(EMPTY64, 0ull);
+  for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < NC; i += (u64)gridDim.x * TT)
+    reinterpret_cast<uint4*>(nt)[i] = make_uint4(EMPTY32, 0u, 0u, 0u);
+}
+
+__device__ __forceinline__ void tl_insert(LSlot* t, u64 LC, u64 key, u32 add) {
+  u64 slot = hash64(key) & (LC - 1);
+  for (;;) {
+    u64 k = ldcg64(&t[slot].key);
+    if (k == EMPTY64) {
+      const u64 old = atomicCAS(reinterpret_cast<unsigned long long*>(&t[slot].key), EMPTY64, key);
+      k = (old == EMPTY64) ? key : old;
+    }
+    if (k == key) { atomicAdd(&t[slot].cnt, add); return; }
+    slot = (slot + 1) & (LC - 1);  // >= 2x the keys' slots: never full
+  }
+}
+
+__device__ __forceinline__ void tn_upsert(NSlot* t, u64 NC, u32* esc, u32 node, u32 p, u32 f) {
+  if (node == EMPTY32) { atomicAdd(&esc[0], p); atomicAdd(&esc[1], f); return; }
+  u64 slot = ((u64)hash32(node) * 0x9E3779B97F4A7C15ull >> 11) & (NC - 1);
+  for (;;) {
+    u32 k = ldcg32(&t[slot].key);
+    if (k == EMPTY32) {
+      const u32 old = atomicCAS(&t[slot].key, EMPTY32, node);
+      k = (old == EMPTY32) ? node : old;
+    }
+    if (k == node) { atomicAdd(&t[slot].P, p); atomicAdd(&t[slot].F, f); return; }
+    slot = (slot + 1) & (NC - 1);
+  }
+}
+
 // ---- partition (world > 1): counts per (CTA, owner), then a scatter into owner-contiguous segments
 __global__ void __launch_bounds__(TT) trace_part_count(const u64* __restrict__ keys, const u32* __restrict__ src,
                                                        const u32* __restrict__ dst, u64 n, u32 world,
@@ -106,8 +145,8 @@ __global__ void __launch_bounds__(TT) trace_part_scatter(const u64* __restrict__
 // cache is flushed (one global upsert per cached key) at the end.  Every packet is counted exactly once.
 constexpr int TCACHE = 4096;
 __global__ void __launch_bounds__(TT) trace_link_insert(const u64* __restrict__ keys, const u32* __restrict__ src,
-                                                        const u32* __restrict__ dst, u64 n, u64* __restrict__ lkey,
-                                                        u32* __restrict__ lcnt, u64 LC, u32* __restrict__ esc) {
+                                                        const u32* __restrict__ dst, u64 n, LSlot* __restrict__ lt,
+                                                        u64 LC, u32* __restrict__ esc) {
   __shared__ u64 ck[TCACHE];
   __shared__ u32 cc[TCACHE];
   for (int i = threadIdx.x; i < TCACHE; i += TT) { ck[i] = EMPTY64; cc[i] = 0; }
@@ -122,18 +161,18 @@ __global__ void __launch_bounds__(TT) trace_link_insert(const u64* __restrict__ 
       if (cur == EMPTY64) cur = k;
     }
     if (cur == k) atomicAdd(&cc[cs], 1u);
-    else glob_link_insert(lkey, lcnt, LC, k, 1u);
+    else tl_insert(lt, LC, k, 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < TCACHE; i += TT)
-    if (ck[i] != EMPTY64) glob_link_insert(lkey, lcnt, LC, ck[i], cc[i]);
+    if (ck[i] != EMPTY64) tl_insert(lt, LC, ck[i], cc[i]);
 }
 
 // Per CTA slot range: link statistics (valid = sum of counts, unique links, max link; PAPER.md:180, :181,
 // :183) into acc[0..2] and the record counts per (side, owner) into ccount[b][2][world].  CTA 0 also
 // accounts the escaped key ~0 (esc[0] packets).
-__global__ void __launch_bounds__(TT) trace_link_count(const u64* __restrict__ lkey, const u32* __restrict__ lcnt,
-                                                       u64 LC, const u32* __restrict__ esc, u32 world,
+__global__ void __launch_bounds__(TT) trace_link_count(const LSlot* __restrict__ lt, u64 LC,
+                                                       const u32* __restrict__ esc, u32 world,
                                                        u32* __restrict__ ccount, unsigned long long* __restrict__ acc) {
   __shared__ u32 h[2][TRACE_MAX_WORLD];
   __shared__ unsigned long long s_sum, s_links, s_max;
@@ -145,9 +184,10 @@ __global__ void __launch_bounds__(TT) trace_link_count(const u64* __restrict__ l
   unsigned long long sm = 0, nl = 0;
   u32 mx = 0;
   for (u64 i = lo + threadIdx.x; i < hi; i += TT) {
-    const u64 k = ldcg64(&lkey[i]);
+    const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(lt) + i);
+    const u64 k = e.x;
     if (k != EMPTY64) {
-      const u32 c = ldcg32(&lcnt[i]);
+      const u32 c = (u32)e.y;
       sm += c; nl += 1; mx = max(mx, c);
       atomicAdd(&h[0][node_owner((u32)(k >> 32), world)], 1u);
       atomicAdd(&h[1][node_owner((u32)k, world)], 1u);
@@ -176,8 +216,8 @@ __global__ void __launch_bounds__(TT) trace_link_count(const u64* __restrict__ l
 
 __device__ __forceinline__ u64 link_rec(u32 node, u32 c) { return ((u64)node << 32) | c; }
 
-__global__ void __launch_bounds__(TT) trace_link_emit(const u64* __restrict__ lkey, const u32* __restrict__ lcnt,
-                                                      u64 LC, const u32* __restrict__ esc, u32 world,
+__global__ void __launch_bounds__(TT) trace_link_emit(const LSlot* __restrict__ lt, u64 LC,
+                                                      const u32* __restrict__ esc, u32 world,
                                                       const u64* __restrict__ coff, u64* __restrict__ rec_src,
                                                       u64* __restrict__ rec_dst) {
   __shared__ u64 base[2][TRACE_MAX_WORLD];
@@ -192,9 +232,10 @@ __global__ void __launch_bounds__(TT) trace_link_emit(const u64* __restrict__ lk
   u64 lo, hi;
   cta_range(LC, lo, hi);
   for (u64 i = lo + threadIdx.x; i < hi; i += TT) {
-    const u64 k = ldcg64(&lkey[i]);
+    const ulonglong2 e = __ldcg(reinterpret_cast<const ulonglong2*>(lt) + i);
+    const u64 k = e.x;
     if (k != EMPTY64) {
-      const u32 c = ldcg32(&lcnt[i]);
+      const u32 c = (u32)e.y;
       const u32 s = (u32)(k >> 32), d = (u32)k;
       const u32 os = node_owner(s, world), od = node_owner(d, world);
       rec_src[base[0][os] + atomicAdd(&cur[0][os], 1u)] = link_rec(s, c);
@@ -211,9 +252,8 @@ __global__ void __launch_bounds__(TT) trace_link_emit(const u64* __restrict__ lk
 // ---- nodes: merge the records of one side; unique nodes, max packets (:186), max fan (:188)
 // Records of a node are merged in a per-CTA SMEM cache first, as trace_link_insert does for links (hot
 // sources / destinations would otherwise serialise on one global counter).
-__device__ __forceinline__ void node_records(const u64* __restrict__ rec, u64 m, u32* __restrict__ nkey,
-                                             u32* __restrict__ nP, u32* __restrict__ nF, u64 NC, u32* __restrict__ esc,
-                                             u32* ck, u32* cp, u32* cf) {
+__device__ __forceinline__ void node_records(const u64* __restrict__ rec, u64 m, NSlot* __restrict__ nt, u64 NC,
+                                             u32* __restrict__ esc, u32* ck, u32* cp, u32* cf) {
   for (int i = threadIdx.x; i < TCACHE; i += TT) { ck[i] = EMPTY32; cp[i] = 0; cf[i] = 0; }
   __syncthreads();
   for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < m; i += (u64)gridDim.x * TT) {
@@ -227,31 +267,28 @@ __device__ __forceinline__ void node_records(const u64* __restrict__ rec, u64 m,
       if (cur == EMPTY32) cur = node;
     }
     if (cur == node) { atomicAdd(&cp[cs], c); atomicAdd(&cf[cs], 1u); }
-    else glob_node_upsert(nkey, nP, nF, NC, &esc[0], &esc[1], node, c, 1u);
+    else tn_upsert(nt, NC, esc, node, c, 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < TCACHE; i += TT)
-    if (ck[i] != EMPTY32) glob_node_upsert(nkey, nP, nF, NC, &esc[0], &esc[1], ck[i], cp[i], cf[i]);
+    if (ck[i] != EMPTY32) tn_upsert(nt, NC, esc, ck[i], cp[i], cf[i]);
 }
 static_assert(TCACHE == 4096, "node cache slot uses 12 hash bits");
 
-__global__ void __launch_bounds__(TT) trace_node_insert(const u64* __restrict__ rec, u64 m, u32* __restrict__ nkey,
-                                                        u32* __restrict__ nP, u32* __restrict__ nF, u64 NC,
-                                                        u32* __restrict__ esc) {
+__global__ void __launch_bounds__(TT) trace_node_insert(const u64* __restrict__ rec, u64 m, NSlot* __restrict__ nt,
+                                                        u64 NC, u32* __restrict__ esc) {
   __shared__ u32 ck[TCACHE], cp[TCACHE], cf[TCACHE];
-  node_records(rec, m, nkey, nP, nF, NC, esc, ck, cp, cf);
+  node_records(rec, m, nt, NC, esc, ck, cp, cf);
 }
 
 // the same, with the record count read from device memory (single-rank trace: no host sync)
 __global__ void __launch_bounds__(TT) trace_node_insert_dev(const u64* __restrict__ rec, const u64* __restrict__ m_dev,
-                                                            u32* __restrict__ nkey, u32* __restrict__ nP,
-                                                            u32* __restrict__ nF, u64 NC, u32* __restrict__ esc) {
+                                                            NSlot* __restrict__ nt, u64 NC, u32* __restrict__ esc) {
   __shared__ u32 ck[TCACHE], cp[TCACHE], cf[TCACHE];
-  node_records(rec, *m_dev, nkey, nP, nF, NC, esc, ck, cp, cf);
+  node_records(rec, *m_dev, nt, NC, esc, ck, cp, cf);
 }
 
-__global__ void __launch_bounds__(TT) trace_node_scan(const u32* __restrict__ nkey, const u32* __restrict__ nP,
-                                                      const u32* __restrict__ nF, u64 NC, const u32* __restrict__ esc,
+__global__ void __launch_bounds__(TT) trace_node_scan(const NSlot* __restrict__ nt, u64 NC, const u32* __restrict__ esc,
                                                       unsigned long long* __restrict__ acc) {
   __shared__ unsigned long long s_n, s_p, s_f;
   if (threadIdx.x == 0) { s_n = 0; s_p = 0; s_f = 0; }
@@ -259,7 +296,8 @@ __global__ void __launch_bounds__(TT) trace_node_scan(const u32* __restrict__ nk
   unsigned long long nn = 0;
   u32 mp = 0, mf = 0;
   for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < NC; i += (u64)gridDim.x * TT) {
-    if (ldcg32(&nkey[i]) != EMPTY32) { nn += 1; mp = max(mp, ldcg32(&nP[i])); mf = max(mf, ldcg32(&nF[i])); }
+    const uint4 e = __ldcg(reinterpret_cast<const uint4*>(nt) + i);
+    if (e.x != EMPTY32) { nn += 1; mp = max(mp, e.y); mf = max(mf, e.z); }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && esc[1]) { nn += 1; mp = max(mp, esc[0]); mf = max(mf, esc[1]); }
   if (nn) atomicAdd(&s_n, nn);
