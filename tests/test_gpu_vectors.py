@@ -144,3 +144,18 @@ def test_stats_unchanged_by_vectors(nsg, cuda_device):
     a = nsg.window_stats_packed(kd, W).cpu()
     b = nsg.window_vectors(kd, W)["stats"].cpu()
     assert torch.equal(a, b)
+
+
+def test_shared_address_pool(nsg, cuda_device):
+    """Sources and destinations drawn from one Zipf-weighted pool of addresses, so most addresses are on both
+    sides (the generated workloads use disjoint pools): exercises the S0 -> S1 list hand-off of |S n D|."""
+    rng = np.random.default_rng(17)
+    pool = rng.choice(2 ** 32, size=20_000, replace=False).astype(np.uint64)
+    p = 1.0 / np.arange(1, pool.size + 1) ** 1.1
+    p /= p.sum()
+    n = 3 * W + 999
+    keys = (pool[rng.choice(pool.size, n, p=p)] << np.uint64(32)) | pool[rng.choice(pool.size, n, p=p)]
+    want = oracle.window_distributions(keys=keys, window=W)
+    assert int(want["ip_sets"][:, 3].min()) > 1000
+    for flags in (0, 1):
+        assert_vectors(gpu_vectors(nsg, keys, W, cuda_device, flags=flags), keys, W)
