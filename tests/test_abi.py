@@ -158,3 +158,47 @@ def test_vectors_argument_validation_without_gpu():
     # input / window errors are still checked first
     assert f(None, None, None, 10, 4, 8, ctypes.byref(ok), 256, 1 << 20, None, 0) == 1
     assert f(None, None, 8, 10, 0, 8, ctypes.byref(ok), 256, 1 << 20, None, 0) == 1
+
+
+def test_next_row_entry_points_validate_without_gpu():
+    """Argument errors of the weighted / trace / anonymisation entry points are reported before any device
+    work (so they are testable here, without a GPU)."""
+    lib = ctypes.CDLL(LIB)
+    vp, u64, u32, sz = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_size_t
+    w = lib.nsg_window_stats_weighted
+    w.restype, w.argtypes = ctypes.c_int, [vp, vp, vp, vp, u64, u64, vp, vp, sz, vp, u32]
+    assert w(None, None, 8, None, 10, 4, 8, 256, 1 << 20, None, 0) == 1      # NULL n_packets
+    assert w(None, None, 8, 6, 10, 4, 8, 256, 1 << 20, None, 0) == 1         # misaligned n_packets
+    assert w(None, None, None, 8, 10, 4, 8, 256, 1 << 20, None, 0) == 1      # no rows
+    assert w(None, None, 8, 8, 0, 4, None, None, 0, None, 0) == 0           # n == 0: nothing to do
+    tw = lib.nsg_trace_workspace_bytes
+    tw.restype, tw.argtypes = sz, [u64, u64, u32]
+    assert tw(100, 100, 0) == 0 and tw(100, 100, 1025) == 0 and tw(100, 100, 8) > 0
+    assert tw(1 << 20, 1 << 20, 1) > tw(1 << 10, 1 << 10, 1)
+    tl = lib.nsg_trace_links
+    tl.restype, tl.argtypes = ctypes.c_int, [vp, vp, vp, u64, u32, vp, vp, vp, vp, vp, sz, u64, u64, vp]
+    assert tl(None, None, 8, 11, 1, 8, 8, 8, 8, 256, 1 << 20, 10, 10, None) == 1   # n > key_capacity
+    assert tl(None, None, 8, 10, 1, None, 8, 8, 8, 256, 1 << 20, 10, 10, None) == 1  # NULL link_stats
+    assert tl(None, None, 8, 10, 1, 8, 8, 8, 12, 256, 1 << 20, 10, 10, None) == 1    # misaligned rec_counts
+    tn = lib.nsg_trace_nodes
+    tn.restype, tn.argtypes = ctypes.c_int, [vp, u64, vp, vp, sz, u64, u64, vp]
+    assert tn(8, 11, 8, 256, 1 << 20, 10, 10, None) == 1                            # m > record_capacity
+    assert tn(None, 5, 8, 256, 1 << 20, 10, 10, None) == 1                          # NULL records
+    tp = lib.nsg_trace_partition
+    tp.restype, tp.argtypes = ctypes.c_int, [vp, vp, vp, u64, u32, vp, vp, vp, sz, u64, u64, vp]
+    assert tp(None, None, 8, 10, 2, None, 8, 256, 1 << 20, 10, 10, None) == 1       # NULL send_keys
+    ts = lib.nsg_trace_stats
+    ts.restype, ts.argtypes = ctypes.c_int, [vp, vp, vp, u64, vp, vp, sz, vp]
+    tsw = lib.nsg_trace_stats_workspace_bytes
+    tsw.restype, tsw.argtypes = sz, [u64]
+    assert ts(None, None, None, 0, None, None, 0, None) == 0                        # n == 0
+    assert ts(None, None, 8, 10, None, 256, 1 << 30, None) == 1                     # NULL out
+    assert ts(None, None, 8, 10, 8, 256, tsw(10) - 1, None) == 3                    # workspace too small
+    an = lib.nsg_anonymize
+    an.restype, an.argtypes = ctypes.c_int, [vp, vp, vp, u64, u64, u32, vp, vp, vp, vp, sz, vp]
+    aw = lib.nsg_anonymize_workspace_bytes
+    aw.restype, aw.argtypes = sz, []
+    assert aw() >= (1 << 29)                                                        # the 2^32-bit bitmap
+    assert an(None, None, 8, 10, 0, 1, 8, 8, None, 256, aw(), None) == 1            # NULL n_unique
+    assert an(None, None, 8, 10, 0, 1, None, 8, 8, 256, aw(), None) == 1            # NULL src_out
+    assert an(None, None, 8, 10, 0, 1, 8, 8, 8, 256, aw() - 1, None) == 3           # workspace too small
