@@ -111,7 +111,7 @@ def test_force_global_and_zero_windows(nsg, cuda_device):
     wt[3000:6000] = 0  # a window of zero-weight rows only: an all-zero A_t
     want = oracle.window_stats_weighted(keys=keys, weights=wt, window=3000)
     assert want[1].tolist() == [0] * 9
-    for flags in (0, 1):
+    for flags in (0, 1, 2):  # fast path, FORCE_GLOBAL, INJECT_OVERFLOW (odd windows handed to the L2 path)
         assert run_w(nsg, keys, wt, 3000, cuda_device, flags=flags).tolist() == want.tolist()
 
 
