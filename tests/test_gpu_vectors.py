@@ -156,6 +156,6 @@ def test_shared_address_pool(nsg, cuda_device):
     n = 3 * W + 999
     keys = (pool[rng.choice(pool.size, n, p=p)] << np.uint64(32)) | pool[rng.choice(pool.size, n, p=p)]
     want = oracle.window_distributions(keys=keys, window=W)
-    assert int(want["ip_sets"][:, 3].min()) > 1000
+    assert int(want["ip_sets"][:-1, 3].min()) > 1000   # full windows share most addresses
     for flags in (0, 1):
         assert_vectors(gpu_vectors(nsg, keys, W, cuda_device, flags=flags), keys, W)
