@@ -641,7 +641,8 @@ nsg_status nsg_trace_stats(const uint32_t* src, const uint32_t* dst, const uint6
 }
 
 size_t nsg_anonymize_workspace_bytes(void) {
-  return nsg::ANON_WORDS * 4 + nsg::ANON_BLOCKS * 4 + nsg::ANON_SCAN_CTAS * 4;
+  return nsg::ANON_WORDS * 4 + nsg::ANON_BLOCKS * 4 + nsg::ANON_SCAN_CTAS * 4 + nsg::ANON_TABLE_SLOTS * 8 +
+         nsg::ANON_TABLE_MAX * 4;
 }
 
 nsg_status nsg_anonymize(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
@@ -663,6 +664,8 @@ nsg_status nsg_anonymize(const uint32_t* src, const uint32_t* dst, const uint64_
   nsg::u32* bitmap = reinterpret_cast<nsg::u32*>(base);
   nsg::u32* bpre = reinterpret_cast<nsg::u32*>(base + nsg::ANON_WORDS * 4);
   nsg::u32* ctot = bpre + nsg::ANON_BLOCKS;
+  nsg::u64* table = reinterpret_cast<nsg::u64*>(ctot + nsg::ANON_SCAN_CTAS);  // 8 B aligned: offsets are multiples of 4 KiB
+  nsg::u32* U = reinterpret_cast<nsg::u32*>(table + nsg::ANON_TABLE_SLOTS);
   nsg::u64* nu = reinterpret_cast<nsg::u64*>(n_unique);
   const nsg::u64* k = reinterpret_cast<const nsg::u64*>(keys);
   if (cudaMemsetAsync(bitmap, 0, nsg::ANON_WORDS * 4, s) != cudaSuccess) return NSG_ERR_CUDA;
@@ -671,10 +674,14 @@ nsg_status nsg_anonymize(const uint32_t* src, const uint32_t* dst, const uint64_
   nsg::anon_block_count<<<nsg::ANON_SCAN_CTAS, nsg::AT, 0, s>>>(bitmap, bpre, ctot);
   nsg::anon_scan_totals<<<1, 1024, 0, s>>>(ctot, nu);
   nsg::anon_block_prefix<<<nsg::ANON_SCAN_CTAS, nsg::AT, 0, s>>>(bpre, ctot);
-  if (n_packets)
-    nsg::anon_relabel_kernel<<<grid, nsg::AT, 0, s>>>(k, src, dst, n_packets, bitmap, bpre, nu, seed, rounds,
+  if (n_packets) {
+    nsg::anon_table_fill<<<grid, nsg::AT, 0, s>>>(table, nu);
+    nsg::anon_enumerate<<<grid, nsg::AT, 0, s>>>(bitmap, bpre, nu, U);
+    nsg::anon_table_label<<<grid, nsg::AT, 0, s>>>(U, nu, seed, rounds, table);
+    nsg::anon_relabel_kernel<<<grid, nsg::AT, 0, s>>>(k, src, dst, n_packets, bitmap, bpre, table, nu, seed, rounds,
                                                       src_out, dst_out);
-  nsg::g_last_launches = n_packets ? 5 : 3;
+  }
+  nsg::g_last_launches = n_packets ? 8 : 3;
   return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }
 

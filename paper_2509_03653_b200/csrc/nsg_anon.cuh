@@ -14,7 +14,10 @@
 //   src'_p = pi(rank(src_p)), dst'_p = pi(rank(dst_p))                                 ("gather")
 // U is never materialised: membership is a 2^32-bit bitmap (512 MiB) in the workspace and rank(a) is the
 // number of set bits below a: an exclusive prefix per 128-bit group (128 MiB) plus the popcounts inside
-// a's group (one 128-bit load).
+// a's group (one 128-bit load).  When N <= ANON_TABLE_MAX the labels pi(rank(a)) are computed once per
+// distinct address (a scan of the bitmap) into an address -> label hash table of next_pow2(2N) slots,
+// small enough to stay in L2, and the gather is one table probe per address; otherwise every address
+// is ranked and permuted directly.
 #pragma once
 #include "nsg.h"
 #include "nsg_common.cuh"
@@ -26,6 +29,9 @@ constexpr u64 ANON_WORDS = 1ull << 27;           // u32 words of the 2^32-bit bi
 constexpr u64 ANON_BLOCKS = ANON_WORDS / 4;      // 128-bit groups (2^25)
 constexpr u32 ANON_SCAN_PER_CTA = 32768;         // groups per CTA in the prefix scan
 constexpr u32 ANON_SCAN_CTAS = (u32)(ANON_BLOCKS / ANON_SCAN_PER_CTA);  // 1024
+constexpr u64 ANON_TABLE_SLOTS = 1ull << 24;     // label table capacity (u64 slots: address << 32 | label)
+constexpr u64 ANON_TABLE_MAX = ANON_TABLE_SLOTS / 2;  // largest N served by the table (load <= 1/2)
+// workspace: bitmap | group prefix | CTA totals | label table | U (the distinct addresses in rank order)
 
 __device__ __forceinline__ u64 anon_mix(u64 z) {  // splitmix64
   z += 0x9E3779B97F4A7C15ull;
@@ -179,17 +185,88 @@ __device__ __forceinline__ u64 anon_rank(const u32* __restrict__ bitmap, const u
   return r;
 }
 
+// ---- label table (N <= ANON_TABLE_MAX): slot = entry (address << 32 | label), EMPTY64 = free.  A real
+// entry never equals EMPTY64 because labels are < N <= 2^23.
+__device__ __forceinline__ u64 anon_table_cap(u64 N) {
+  u64 c = 1;
+  while (c < 2 * N) c <<= 1;
+  return c;
+}
+__device__ __forceinline__ u64 anon_slot(u32 a, u64 cap) { return ((u64)hash32(a) * 0x9E3779B97F4A7C15ull >> 17) & (cap - 1); }
+
+__global__ void __launch_bounds__(AT) anon_table_fill(u64* __restrict__ table, const u64* __restrict__ n_unique) {
+  const u64 N = *n_unique;
+  if (N > ANON_TABLE_MAX) return;
+  const u64 cap = anon_table_cap(N);
+  for (u64 i = (u64)blockIdx.x * AT + threadIdx.x; i < cap; i += (u64)gridDim.x * AT) table[i] = EMPTY64;
+}
+
+// Enumerate the distinct addresses in ascending order, U[rank] = a (one thread per 128-bit group of the
+// bitmap, the granularity of the rank prefix; the work per set bit is one store), then label them densely
+// (anon_table_label: full warps for the permutation arithmetic).
+__global__ void __launch_bounds__(AT) anon_enumerate(const u32* __restrict__ bitmap, const u32* __restrict__ bpre,
+                                                     const u64* __restrict__ n_unique, u32* __restrict__ U) {
+  if (*n_unique > ANON_TABLE_MAX) return;
+  const uint4* g4 = reinterpret_cast<const uint4*>(bitmap);
+  for (u64 gi = (u64)blockIdx.x * AT + threadIdx.x; gi < ANON_BLOCKS; gi += (u64)gridDim.x * AT) {
+    const uint4 g = __ldcs(g4 + gi);
+    if ((g.x | g.y | g.z | g.w) == 0) continue;
+    u32 r = bpre[gi];
+    const u32 wv[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      u32 bits = wv[q];
+      while (bits) {
+        const u32 b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        U[r++] = (u32)(gi * 128 + q * 32 + b);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(AT) anon_table_label(const u32* __restrict__ U, const u64* __restrict__ n_unique,
+                                                       u64 seed, u32 rounds, u64* __restrict__ table) {
+  const u64 N = *n_unique;
+  if (N > ANON_TABLE_MAX) return;
+  const u64 cap = anon_table_cap(N);
+  for (u64 r = (u64)blockIdx.x * AT + threadIdx.x; r < N; r += (u64)gridDim.x * AT) {
+    const u32 a = U[r];
+    const u64 e = ((u64)a << 32) | (u32)anon_perm(r, N, seed, rounds);
+    u64 slot = anon_slot(a, cap);
+    while (atomicCAS(reinterpret_cast<unsigned long long*>(&table[slot]), EMPTY64, e) != EMPTY64)
+      slot = (slot + 1) & (cap - 1);  // each address is inserted once: a taken slot holds another address
+  }
+}
+
+__device__ __forceinline__ u32 anon_lookup(const u64* __restrict__ table, u64 cap, u32 a) {
+  u64 slot = anon_slot(a, cap);
+  for (;;) {
+    const u64 e = __ldcg(reinterpret_cast<const unsigned long long*>(&table[slot]));
+    if ((u32)(e >> 32) == a && e != EMPTY64) return (u32)e;
+    slot = (slot + 1) & (cap - 1);  // every looked-up address is present
+  }
+}
+
 __global__ void __launch_bounds__(AT) anon_relabel_kernel(const u64* __restrict__ keys, const u32* __restrict__ src,
                                                           const u32* __restrict__ dst, u64 n,
                                                           const u32* __restrict__ bitmap, const u32* __restrict__ bpre,
+                                                          const u64* __restrict__ table,
                                                           const u64* __restrict__ n_unique, u64 seed, u32 rounds,
                                                           u32* __restrict__ src_out, u32* __restrict__ dst_out) {
   const u64 N = *n_unique;
+  const bool tab = N <= ANON_TABLE_MAX;
+  const u64 cap = tab ? anon_table_cap(N) : 0;
   for (u64 i = (u64)blockIdx.x * AT + threadIdx.x; i < n; i += (u64)gridDim.x * AT) {
     const u32 s = keys ? (u32)(keys[i] >> 32) : src[i];
     const u32 d = keys ? (u32)keys[i] : dst[i];
-    src_out[i] = (u32)anon_perm(anon_rank(bitmap, bpre, s), N, seed, rounds);
-    dst_out[i] = (u32)anon_perm(anon_rank(bitmap, bpre, d), N, seed, rounds);
+    if (tab) {
+      src_out[i] = anon_lookup(table, cap, s);
+      dst_out[i] = anon_lookup(table, cap, d);
+    } else {
+      src_out[i] = (u32)anon_perm(anon_rank(bitmap, bpre, s), N, seed, rounds);
+      dst_out[i] = (u32)anon_perm(anon_rank(bitmap, bpre, d), N, seed, rounds);
+    }
   }
 }
 

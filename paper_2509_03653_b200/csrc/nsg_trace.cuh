@@ -92,33 +92,55 @@ __global__ void __launch_bounds__(TT) trace_part_count(const u64* __restrict__ k
 }
 
 // Exclusive offsets in (owner-major, CTA-minor) order for `sides` independent count tables
-// ccount[b][side][o] -> coff[b][side][o]; totals[side][o].  One CTA, thread o per owner.
+// ccount[b][side][o] -> coff[b][side][o]; totals[side][o].  One CTA of 1024 threads scans the world*grid
+// counts of each side in chunks of 1024 (element e = o * grid + b).
 __global__ void __launch_bounds__(TRACE_MAX_WORLD) trace_scan(const u32* __restrict__ ccount, u32 grid, u32 sides,
                                                               u32 world, u64* __restrict__ coff, u64* __restrict__ totals) {
-  __shared__ u64 tot[TRACE_MAX_WORLD];
-  const u32 o = threadIdx.x;
+  __shared__ u64 wsum[32];
+  __shared__ u64 carry;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const u64 ne = (u64)world * grid;
   for (u32 sd = 0; sd < sides; ++sd) {
-    u64 t = 0;
-    if (o < world)
-      for (u32 b = 0; b < grid; ++b) t += ccount[((u64)b * sides + sd) * world + o];
-    if (o < TRACE_MAX_WORLD) tot[o] = o < world ? t : 0;
+    if (t == 0) carry = 0;
     __syncthreads();
-    if (o == 0) {  // world <= 1024: a serial scan of the owner totals
-      u64 run = 0;
-      for (u32 q = 0; q < world; ++q) { const u64 v = tot[q]; tot[q] = run; run += v; }
-    }
-    __syncthreads();
-    if (o < world) {
-      u64 run = tot[o];
-      for (u32 b = 0; b < grid; ++b) {
-        const u64 idx = ((u64)b * sides + sd) * world + o;
-        coff[idx] = run;
-        run += ccount[idx];
+    for (u64 e0 = 0; e0 < ne; e0 += TRACE_MAX_WORLD) {
+      const u64 e = e0 + t;
+      const u32 o = (u32)(e / grid), b = (u32)(e - (u64)o * grid);
+      const u64 idx = ((u64)b * sides + sd) * world + o;
+      const u64 v = e < ne ? ccount[idx] : 0;
+      u64 x = v;
+#pragma unroll
+      for (int k = 1; k < 32; k <<= 1) {
+        const u64 y = __shfl_up_sync(0xffffffffu, x, k);
+        if (lane >= k) x += y;
       }
-      totals[(u64)sd * world + o] = t;
+      if (lane == 31) wsum[wid] = x;
+      __syncthreads();
+      if (wid == 0) {
+        u64 w = wsum[lane];
+#pragma unroll
+        for (int k = 1; k < 32; k <<= 1) {
+          const u64 y = __shfl_up_sync(0xffffffffu, w, k);
+          if (lane >= k) w += y;
+        }
+        wsum[lane] = w;
+      }
+      __syncthreads();
+      const u64 incl = x + (wid ? wsum[wid - 1] : 0ull) + carry;
+      if (e < ne) coff[idx] = incl - v;
+      __syncthreads();
+      if (t == TRACE_MAX_WORLD - 1) carry = incl;
+      __syncthreads();
     }
-    __syncthreads();
   }
+  // totals per (side, owner): the difference of consecutive owner starts
+  for (u32 sd = 0; sd < sides; ++sd)
+    for (u32 o = t; o < world; o += TRACE_MAX_WORLD) {
+      const u64 first = coff[((u64)0 * sides + sd) * world + o];
+      const u64 lastb = (u64)(grid - 1);
+      const u64 li = (lastb * sides + sd) * world + o;
+      totals[(u64)sd * world + o] = coff[li] + ccount[li] - first;
+    }
 }
 
 __global__ void __launch_bounds__(TT) trace_part_scatter(const u64* __restrict__ keys, const u32* __restrict__ src,

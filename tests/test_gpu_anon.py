@@ -32,7 +32,8 @@ def gpu_anon(nsg, keys, device, layout="packed", **kw):
 
 
 @pytest.mark.parametrize("dist,n", [(gen.Dist("zipf", 1.1, 1 << 20), 1 << 23), (gen.Dist("heavy"), 1 << 20),
-                                    (gen.Dist("uniform"), 1 << 20), (gen.Dist("zipf", 1.5, 1 << 6), 1000), (None, 1)])
+                                    (gen.Dist("uniform"), 1 << 20), (gen.Dist("zipf", 1.5, 1 << 6), 1000), (None, 1),
+                                    (gen.Dist("uniform"), 1 << 23)])  # the last: N > 2^23, direct ranks (no label table)
 @pytest.mark.parametrize("seed,rounds", [(0, 0), (7, 1), (2 ** 64 - 1, 3)])
 def test_anonymize_matches_oracle(nsg, cuda_device, dist, n, seed, rounds):
     keys = np.array([0x0A0000010A000002], np.uint64) if dist is None else gen.generate_host(dist, 91, 0, n, packed=True)
