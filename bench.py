@@ -193,6 +193,9 @@ def main():
                          "step's packets (nsg_trace_stats; N>1: distributed_trace_stats with all-to-all exchanges, "
                          "SURVEY §8(f) f4b); anonymize: relabel every address of each step's packets "
                          "(nsg_anonymize, one shuffle round, SURVEY §8(f) f2)")
+    ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
+                    help="--path trace at N>1: NCCL all-to-all exchanges, or the fused partition/emission kernels "
+                         "storing into the owners' CUDA-IPC-mapped buffers (peer memory over NVLink)")
     ap.add_argument("--input", choices=["packets", "weighted"], default="packets",
                     help="packets: raw packets (north_star); weighted: rows (src, dst, n_packets) with n_packets "
                          "uniform in [1, 8] (nsg_window_stats_weighted, SURVEY §8(f) f4a); unit = rows/s")
@@ -274,7 +277,8 @@ def main():
         if trace:  # events around the whole call (table resets + the trace kernels [+ exchanges])
             if evs:
                 evs[0].record()
-            r = nsg.trace_stats(ring[i % RING]) if world == 1 else distributed_trace_stats(ring[i % RING])
+            r = nsg.trace_stats(ring[i % RING]) if world == 1 else \
+                distributed_trace_stats(ring[i % RING], transport=args.transport)
             if evs:
                 evs[1].record()
             return r
@@ -361,7 +365,7 @@ def main():
 
         def e2e_once():
             keys_dev.copy_(host, non_blocking=True)
-            r = nsg.trace_stats(keys_dev) if world == 1 else distributed_trace_stats(keys_dev)
+            r = nsg.trace_stats(keys_dev) if world == 1 else distributed_trace_stats(keys_dev, transport=args.transport)
             tout_host.copy_(r, non_blocking=True)
         d2h_bytes = 9 * 8
     elif wtd:  # H2D of the rows (keys + n_packets), the call, D2H of the statistics

@@ -220,6 +220,45 @@ nsg_status nsg_trace_links(const uint32_t* src, const uint32_t* dst, const uint6
 nsg_status nsg_trace_nodes(const uint64_t* records, uint64_t m, uint64_t* node_stats, void* workspace,
                            size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity, void* stream);
 
+/* ---- Fused exchange over peer memory (one process per GPU, CUDA IPC) --------------------------------
+ * The all-to-all steps above can skip the collective: the scatter kernels store every key / record
+ * straight into the owner rank's receive buffer through a peer mapping (NVLink P2P on a multi-GPU node),
+ * so the transfer overlaps the partition / emission tile by tile.  The driver (distributed.py) all-gathers
+ * the per-owner counts first to place each rank's segment, and synchronises (stream + barrier) before an
+ * owner reads its buffer.
+ *   nsg_ipc_alloc   cudaMalloc `bytes` and export it: *dev_ptr, handle_out = nsg_ipc_handle_bytes() host
+ *                   bytes to send to the peers; nsg_ipc_free releases it.  (The only entry points that
+ *                   allocate device memory: the receive buffers must be IPC-exportable allocations.)
+ *   nsg_ipc_open    map a peer's buffer from its handle (same node; the same GPU works too); nsg_ipc_close.
+ *   nsg_trace_owner_counts     counts u64[world] (device): keys per link owner (as nsg_trace_partition).
+ *   nsg_trace_partition_peers  scatter the keys: owner o's segment to peers[o] + peer_base[o] (peers: device
+ *                              array of `world` device pointers valid in this process; peer_base: device
+ *                              u64[world], in elements).
+ *   nsg_trace_links_count      nsg_trace_links without the emission: link_stats u64[3], rec_counts
+ *                              u64[2][world]; the table stays in the workspace for ...
+ *   nsg_trace_links_emit_peers the records of the table left by nsg_trace_links_count (same workspace and
+ *                              capacities, nothing in between on it), side s's owner-o segment to
+ *                              peers_s[o] + base_s[o]. */
+size_t nsg_ipc_handle_bytes(void);
+nsg_status nsg_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out);
+nsg_status nsg_ipc_open(const void* handle, void** dev_ptr);
+nsg_status nsg_ipc_close(void* dev_ptr);
+nsg_status nsg_ipc_free(void* dev_ptr);
+nsg_status nsg_trace_owner_counts(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n,
+                                  uint32_t world, uint64_t* counts, void* workspace, size_t workspace_bytes,
+                                  uint64_t key_capacity, uint64_t record_capacity, void* stream);
+nsg_status nsg_trace_partition_peers(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n,
+                                     uint32_t world, uint64_t* const* peers, const uint64_t* peer_base,
+                                     void* workspace, size_t workspace_bytes, uint64_t key_capacity,
+                                     uint64_t record_capacity, void* stream);
+nsg_status nsg_trace_links_count(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n,
+                                 uint32_t world, uint64_t* link_stats, uint64_t* rec_counts, void* workspace,
+                                 size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity, void* stream);
+nsg_status nsg_trace_links_emit_peers(uint32_t world, uint64_t* const* peers_src, uint64_t* const* peers_dst,
+                                      const uint64_t* base_src, const uint64_t* base_dst, void* workspace,
+                                      size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity,
+                                      void* stream);
+
 /* One GPU: the nine whole-trace statistics into out u64[9] (device), north_star column order; the steps
  * above with world = 1 and no host synchronisation.  Workspace: nsg_trace_stats_workspace_bytes(n). */
 size_t nsg_trace_stats_workspace_bytes(uint64_t n_packets);

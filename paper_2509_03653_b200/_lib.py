@@ -35,6 +35,15 @@ EXPORTS = (
     "nsg_trace_nodes",
     "nsg_trace_stats_workspace_bytes",
     "nsg_trace_stats",
+    "nsg_ipc_handle_bytes",
+    "nsg_ipc_alloc",
+    "nsg_ipc_open",
+    "nsg_ipc_close",
+    "nsg_ipc_free",
+    "nsg_trace_owner_counts",
+    "nsg_trace_partition_peers",
+    "nsg_trace_links_count",
+    "nsg_trace_links_emit_peers",
     "nsg_anonymize_workspace_bytes",
     "nsg_anonymize",
     "nsg_diag_offset",
@@ -120,6 +129,24 @@ def load() -> ctypes.CDLL:
     lib.nsg_anonymize_workspace_bytes.argtypes = []
     lib.nsg_anonymize.restype = ctypes.c_int
     lib.nsg_anonymize.argtypes = [vp, vp, vp, u64, u64, u32, vp, vp, vp, vp, sz, vp]
+    lib.nsg_ipc_handle_bytes.restype = sz
+    lib.nsg_ipc_handle_bytes.argtypes = []
+    lib.nsg_ipc_alloc.restype = ctypes.c_int
+    lib.nsg_ipc_alloc.argtypes = [sz, ctypes.POINTER(vp), vp]
+    lib.nsg_ipc_open.restype = ctypes.c_int
+    lib.nsg_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
+    lib.nsg_ipc_close.restype = ctypes.c_int
+    lib.nsg_ipc_close.argtypes = [vp]
+    lib.nsg_ipc_free.restype = ctypes.c_int
+    lib.nsg_ipc_free.argtypes = [vp]
+    lib.nsg_trace_owner_counts.restype = ctypes.c_int
+    lib.nsg_trace_owner_counts.argtypes = [vp, vp, vp, u64, u32, vp, vp, sz, u64, u64, vp]
+    lib.nsg_trace_partition_peers.restype = ctypes.c_int
+    lib.nsg_trace_partition_peers.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp, sz, u64, u64, vp]
+    lib.nsg_trace_links_count.restype = ctypes.c_int
+    lib.nsg_trace_links_count.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp, sz, u64, u64, vp]
+    lib.nsg_trace_links_emit_peers.restype = ctypes.c_int
+    lib.nsg_trace_links_emit_peers.argtypes = [u32, vp, vp, vp, vp, vp, sz, u64, u64, vp]
     lib.nsg_diag_offset.restype = sz
     lib.nsg_diag_offset.argtypes = []
     lib.nsg_last_launches.restype = ctypes.c_uint

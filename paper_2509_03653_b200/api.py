@@ -473,3 +473,101 @@ def anonymize(keys: Optional[torch.Tensor] = None, *, src=None, dst=None, seed: 
     if rc != 0:
         raise NsgError(rc, "nsg_anonymize")
     return so, do, nu
+
+
+
+# ---------------------------------------------------------------------------------------------------
+# Fused exchange over peer memory (include/nsg.h "Fused exchange"): IPC-exported receive buffers
+# ---------------------------------------------------------------------------------------------------
+class _DevArray:
+    """A raw device allocation seen by torch through __cuda_array_interface__ (no copy)."""
+
+    def __init__(self, ptr: int, n: int, device):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i8", "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+        self.device = device
+
+
+def ipc_handle_bytes() -> int:
+    return int(_lib.nsg_ipc_handle_bytes())
+
+
+def ipc_alloc(capacity: int, device):
+    """An IPC-exportable device buffer of `capacity` int64 elements: (pointer, handle bytes, tensor view)."""
+    ptr = ctypes.c_void_p()
+    handle = (ctypes.c_char * ipc_handle_bytes())()
+    with torch.cuda.device(device):
+        rc = _lib.nsg_ipc_alloc(max(1, int(capacity)) * 8, ctypes.byref(ptr), handle)
+    if rc != 0:
+        raise NsgError(rc, "nsg_ipc_alloc")
+    view = torch.as_tensor(_DevArray(ptr.value, max(1, int(capacity)), device), device=device)
+    return ptr.value, bytes(handle), view
+
+
+def ipc_open(handle: bytes, device) -> int:
+    ptr = ctypes.c_void_p()
+    with torch.cuda.device(device):
+        rc = _lib.nsg_ipc_open(handle, ctypes.byref(ptr))
+    if rc != 0:
+        raise NsgError(rc, "nsg_ipc_open")
+    return ptr.value
+
+
+def ipc_close(ptr: int) -> None:
+    _lib.nsg_ipc_close(ctypes.c_void_p(ptr))
+
+
+def ipc_free(ptr: int) -> None:
+    _lib.nsg_ipc_free(ctypes.c_void_p(ptr))
+
+
+def trace_owner_counts(keys: torch.Tensor, world: int, workspace: TraceWorkspace, stream=None) -> torch.Tensor:
+    """Keys per link owner rank: int64 [world] on the device (nsg_trace_owner_counts)."""
+    n, device = _rows(keys, None, None)
+    counts = torch.zeros(world, dtype=torch.int64, device=device)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_trace_owner_counts(None, None, keys.data_ptr() if n else None, n, int(world), counts.data_ptr(),
+                                     workspace.ptr, workspace.nbytes, workspace.key_capacity,
+                                     workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise NsgError(rc, "nsg_trace_owner_counts")
+    return counts
+
+
+def trace_partition_peers(keys: torch.Tensor, world: int, peer_ptrs: torch.Tensor, peer_base: torch.Tensor,
+                          workspace: TraceWorkspace, stream=None) -> None:
+    """Scatter the keys straight into the owners' receive buffers (nsg_trace_partition_peers)."""
+    n, device = _rows(keys, None, None)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_trace_partition_peers(None, None, keys.data_ptr() if n else None, n, int(world), peer_ptrs.data_ptr(),
+                                        peer_base.data_ptr(), workspace.ptr, workspace.nbytes, workspace.key_capacity,
+                                        workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise NsgError(rc, "nsg_trace_partition_peers")
+
+
+def trace_links_count(keys: torch.Tensor, world: int, workspace: TraceWorkspace, stream=None):
+    """The owned links' statistics (int64 [3]) and record counts per side and owner (int64 [2, world]); the
+    table stays in `workspace` for trace_links_emit_peers."""
+    n, device = _rows(keys, None, None)
+    stats = torch.zeros(3, dtype=torch.int64, device=device)
+    rc_ = torch.zeros((2, world), dtype=torch.int64, device=device)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_trace_links_count(None, None, keys.data_ptr() if n else None, n, int(world), stats.data_ptr(),
+                                    rc_.data_ptr(), workspace.ptr, workspace.nbytes, workspace.key_capacity,
+                                    workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise NsgError(rc, "nsg_trace_links_count")
+    return stats, rc_
+
+
+def trace_links_emit_peers(world: int, ptrs_src: torch.Tensor, ptrs_dst: torch.Tensor, base_src: torch.Tensor,
+                           base_dst: torch.Tensor, workspace: TraceWorkspace, stream=None) -> None:
+    """Emit the records of the table left by trace_links_count straight into the owners' buffers."""
+    device = ptrs_src.device
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_trace_links_emit_peers(int(world), ptrs_src.data_ptr(), ptrs_dst.data_ptr(), base_src.data_ptr(),
+                                         base_dst.data_ptr(), workspace.ptr, workspace.nbytes, workspace.key_capacity,
+                                         workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise NsgError(rc, "nsg_trace_links_emit_peers")

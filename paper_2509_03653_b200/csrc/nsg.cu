@@ -427,7 +427,8 @@ static nsg_status trace_links_impl(const u32* src, const u32* dst, const u64* ke
   }
   trace_link_count<<<T.grid, TT, 0, c.s>>>(lt, T.LC, esc, world, ccount, reinterpret_cast<unsigned long long*>(link_stats));
   trace_scan<<<1, TRACE_MAX_WORLD, 0, c.s>>>(ccount, T.grid, 2, world, coff, rec_counts);
-  trace_link_emit<<<T.grid, TT, 0, c.s>>>(lt, T.LC, esc, world, coff, rec_src, rec_dst);
+  trace_link_emit<<<T.grid, TT, 0, c.s>>>(lt, T.LC, esc, world, coff, rec_src, rec_dst, nullptr, nullptr, nullptr,
+                                          nullptr);
   g_last_launches += 4;
   return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }
@@ -574,7 +575,7 @@ nsg_status nsg_trace_partition(const uint32_t* src, const uint32_t* dst, const u
   nsg::trace_scan<<<1, nsg::TRACE_MAX_WORLD, 0, c.s>>>(ccount, c.T.grid, 1, world, coff,
                                                         reinterpret_cast<nsg::u64*>(send_counts));
   nsg::trace_part_scatter<<<c.T.grid, nsg::TT, 0, c.s>>>(k, src, dst, n, world, coff,
-                                                         reinterpret_cast<nsg::u64*>(send_keys));
+                                                         reinterpret_cast<nsg::u64*>(send_keys), nullptr, nullptr);
   nsg::g_last_launches = 3;
   return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }
@@ -606,6 +607,131 @@ nsg_status nsg_trace_nodes(const uint64_t* records, uint64_t m, uint64_t* node_s
   nsg_status st = nsg::trace_begin(workspace, workspace_bytes, key_capacity, record_capacity, 1, stream, c);
   if (st != NSG_OK) return st;
   return nsg::trace_nodes_impl(reinterpret_cast<const nsg::u64*>(records), m, reinterpret_cast<nsg::u64*>(node_stats), c);
+}
+
+// ---- fused exchange over peer memory (CUDA IPC): the scatters write straight into the owners' buffers
+size_t nsg_ipc_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+nsg_status nsg_ipc_alloc(size_t bytes, void** dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out || bytes == 0) return NSG_ERR_INVALID_ARGUMENT;
+  nsg::DevInfo d;
+  const nsg_status st = nsg::dev_info(d);
+  if (st != NSG_OK) return st;
+  if (cudaMalloc(dev_ptr, bytes) != cudaSuccess) return NSG_ERR_CUDA;
+  if (cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle_out), *dev_ptr) != cudaSuccess) {
+    cudaFree(*dev_ptr);
+    *dev_ptr = nullptr;
+    return NSG_ERR_CUDA;
+  }
+  return NSG_OK;
+}
+
+nsg_status nsg_ipc_open(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return NSG_ERR_INVALID_ARGUMENT;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
+}
+
+nsg_status nsg_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return NSG_ERR_INVALID_ARGUMENT;
+  return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
+}
+
+nsg_status nsg_ipc_free(void* dev_ptr) {
+  if (!dev_ptr) return NSG_ERR_INVALID_ARGUMENT;
+  return cudaFree(dev_ptr) == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
+}
+
+nsg_status nsg_trace_owner_counts(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n,
+                                  uint32_t world, uint64_t* counts, void* workspace, size_t workspace_bytes,
+                                  uint64_t key_capacity, uint64_t record_capacity, void* stream) {
+  nsg::g_last_launches = 0;
+  if (n && !nsg::input_ok(src, dst, reinterpret_cast<const nsg::u64*>(keys))) return NSG_ERR_INVALID_ARGUMENT;
+  if (!counts || (reinterpret_cast<uintptr_t>(counts) & 7)) return NSG_ERR_INVALID_ARGUMENT;
+  nsg::TraceCall c;
+  nsg_status st = nsg::trace_begin(workspace, workspace_bytes, key_capacity, record_capacity, world, stream, c);
+  if (st != NSG_OK) return st;
+  nsg::u32* ccount = reinterpret_cast<nsg::u32*>(c.base + c.T.o_ccount);
+  nsg::u64* coff = reinterpret_cast<nsg::u64*>(c.base + c.T.o_coff);
+  nsg::trace_part_count<<<c.T.grid, nsg::TT, 0, c.s>>>(reinterpret_cast<const nsg::u64*>(keys), src, dst, n, world, ccount);
+  nsg::trace_scan<<<1, nsg::TRACE_MAX_WORLD, 0, c.s>>>(ccount, c.T.grid, 1, world, coff, reinterpret_cast<nsg::u64*>(counts));
+  nsg::g_last_launches = 2;
+  return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
+}
+
+nsg_status nsg_trace_partition_peers(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n,
+                                     uint32_t world, uint64_t* const* peers, const uint64_t* peer_base,
+                                     void* workspace, size_t workspace_bytes, uint64_t key_capacity,
+                                     uint64_t record_capacity, void* stream) {
+  nsg::g_last_launches = 0;
+  if (n && !nsg::input_ok(src, dst, reinterpret_cast<const nsg::u64*>(keys))) return NSG_ERR_INVALID_ARGUMENT;
+  if (!peers || !peer_base || (reinterpret_cast<uintptr_t>(peers) & 7) || (reinterpret_cast<uintptr_t>(peer_base) & 7))
+    return NSG_ERR_INVALID_ARGUMENT;
+  nsg::TraceCall c;
+  nsg_status st = nsg::trace_begin(workspace, workspace_bytes, key_capacity, record_capacity, world, stream, c);
+  if (st != NSG_OK) return st;
+  nsg::u32* ccount = reinterpret_cast<nsg::u32*>(c.base + c.T.o_ccount);
+  nsg::u64* coff = reinterpret_cast<nsg::u64*>(c.base + c.T.o_coff);
+  const nsg::u64* k = reinterpret_cast<const nsg::u64*>(keys);
+  nsg::trace_part_count<<<c.T.grid, nsg::TT, 0, c.s>>>(k, src, dst, n, world, ccount);
+  nsg::trace_scan<<<1, nsg::TRACE_MAX_WORLD, 0, c.s>>>(ccount, c.T.grid, 1, world, coff, nullptr);
+  nsg::trace_part_scatter<<<c.T.grid, nsg::TT, 0, c.s>>>(k, src, dst, n, world, coff, nullptr,
+                                                         reinterpret_cast<nsg::u64* const*>(peers),
+                                                         reinterpret_cast<const nsg::u64*>(peer_base));
+  nsg::g_last_launches = 3;
+  return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
+}
+
+nsg_status nsg_trace_links_count(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n,
+                                 uint32_t world, uint64_t* link_stats, uint64_t* rec_counts, void* workspace,
+                                 size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity, void* stream) {
+  nsg::g_last_launches = 0;
+  if (n > key_capacity) return NSG_ERR_INVALID_ARGUMENT;
+  if (n && !nsg::input_ok(src, dst, reinterpret_cast<const nsg::u64*>(keys))) return NSG_ERR_INVALID_ARGUMENT;
+  if (!link_stats || !rec_counts || (reinterpret_cast<uintptr_t>(link_stats) & 7) ||
+      (reinterpret_cast<uintptr_t>(rec_counts) & 7))
+    return NSG_ERR_INVALID_ARGUMENT;
+  nsg::TraceCall c;
+  nsg_status st = nsg::trace_begin(workspace, workspace_bytes, key_capacity, record_capacity, world, stream, c);
+  if (st != NSG_OK) return st;
+  const nsg::TLayout& T = c.T;
+  nsg::u32* esc = reinterpret_cast<nsg::u32*>(c.base + T.o_acc);
+  nsg::LSlot* lt = reinterpret_cast<nsg::LSlot*>(c.base + T.o_lt);
+  nsg::u32* ccount = reinterpret_cast<nsg::u32*>(c.base + T.o_ccount);
+  nsg::u64* coff = reinterpret_cast<nsg::u64*>(c.base + T.o_coff);
+  if (cudaMemsetAsync(esc, 0, 16, c.s) != cudaSuccess || cudaMemsetAsync(link_stats, 0, 24, c.s) != cudaSuccess)
+    return NSG_ERR_CUDA;
+  nsg::trace_fill<<<T.grid, nsg::TT, 0, c.s>>>(lt, T.LC, nullptr, 0);
+  if (n)
+    nsg::trace_link_insert<<<T.grid, nsg::TT, 0, c.s>>>(reinterpret_cast<const nsg::u64*>(keys), src, dst, n, lt, T.LC, esc);
+  nsg::trace_link_count<<<T.grid, nsg::TT, 0, c.s>>>(lt, T.LC, esc, world, ccount,
+                                                     reinterpret_cast<unsigned long long*>(link_stats));
+  nsg::trace_scan<<<1, nsg::TRACE_MAX_WORLD, 0, c.s>>>(ccount, T.grid, 2, world, coff,
+                                                       reinterpret_cast<nsg::u64*>(rec_counts));
+  nsg::g_last_launches = n ? 4 : 3;
+  return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
+}
+
+nsg_status nsg_trace_links_emit_peers(uint32_t world, uint64_t* const* peers_src, uint64_t* const* peers_dst,
+                                      const uint64_t* base_src, const uint64_t* base_dst, void* workspace,
+                                      size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity,
+                                      void* stream) {
+  nsg::g_last_launches = 0;
+  const void* p8[] = {peers_src, peers_dst, base_src, base_dst};
+  for (const void* p : p8)
+    if (!p || (reinterpret_cast<uintptr_t>(p) & 7)) return NSG_ERR_INVALID_ARGUMENT;
+  nsg::TraceCall c;
+  nsg_status st = nsg::trace_begin(workspace, workspace_bytes, key_capacity, record_capacity, world, stream, c);
+  if (st != NSG_OK) return st;
+  const nsg::TLayout& T = c.T;
+  nsg::trace_link_emit<<<T.grid, nsg::TT, 0, c.s>>>(
+      reinterpret_cast<const nsg::LSlot*>(c.base + T.o_lt), T.LC, reinterpret_cast<const nsg::u32*>(c.base + T.o_acc),
+      world, reinterpret_cast<const nsg::u64*>(c.base + T.o_coff), nullptr, nullptr,
+      reinterpret_cast<nsg::u64* const*>(peers_src), reinterpret_cast<nsg::u64* const*>(peers_dst),
+      reinterpret_cast<const nsg::u64*>(base_src), reinterpret_cast<const nsg::u64*>(base_dst));
+  nsg::g_last_launches = 1;
+  return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }
 
 nsg_status nsg_trace_stats(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,

