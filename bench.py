@@ -194,8 +194,9 @@ def main():
                          "SURVEY §8(f) f4b); anonymize: relabel every address of each step's packets "
                          "(nsg_anonymize, one shuffle round, SURVEY §8(f) f2)")
     ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
-                    help="--path trace at N>1: NCCL all-to-all exchanges, or the fused partition/emission kernels "
-                         "storing into the owners' CUDA-IPC-mapped buffers (peer memory over NVLink)")
+                    help="N>1: NCCL collectives, or the kernels storing straight into the other ranks' "
+                         "CUDA-IPC-mapped buffers over peer memory (windows: result rows from the epilogue; "
+                         "trace: the partition / record emission)")
     ap.add_argument("--input", choices=["packets", "weighted"], default="packets",
                     help="packets: raw packets (north_star); weighted: rows (src, dst, n_packets) with n_packets "
                          "uniform in [1, 8] (nsg_window_stats_weighted, SURVEY §8(f) f4a); unit = rows/s")
@@ -243,6 +244,11 @@ def main():
     outs = [torch.empty((WINDOWS_PER_STEP, 9), dtype=torch.int64, device=dev) for _ in range(RING)]
     vec = args.outputs == "vectors"
     wtd = args.input == "weighted"
+    p2p_tab = None
+    if world > 1 and args.transport == "p2p":  # the result gather done by the kernels' epilogues (peer memory)
+        from paper_2509_03653_b200.distributed import PeerBuffers
+
+        p2p_tab = PeerBuffers(WINDOWS_PER_STEP * world * 9, None, dev)
     trace = args.path == "trace"
     anon = args.path == "anonymize"
     if anon and (vec or wtd or world > 1):
@@ -294,6 +300,10 @@ def main():
             r = nsg.window_stats_weighted(ring[i % RING], wring[i % RING], WINDOW, out=outs[i % RING], workspace=ws)
             if evs:
                 evs[1].record()
+        elif world > 1 and args.transport == "p2p":  # rows stored into every rank's IPC-mapped table
+            r = nsg.window_stats_mirrored(ring[i % RING], p2p_tab.ptrs, rank * WINDOWS_PER_STEP, WINDOW,
+                                          out=outs[i % RING], workspace=ws)
+            return r
         else:
             r = nsg.window_stats_packed(ring[i % RING], WINDOW, out=outs[i % RING], workspace=ws, kernel_events=evs)
         if world > 1:
@@ -319,6 +329,9 @@ def main():
     start.record()
     for i in range(args.steps):
         step(i, kev[i])
+    if p2p_tab is not None:  # every rank's rows are in every table before the clock stops
+        torch.cuda.synchronize(dev)
+        tdist.barrier()
     end.record()
     torch.cuda.synchronize(dev)
     wall = time.perf_counter() - wall0

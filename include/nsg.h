@@ -135,6 +135,17 @@ nsg_status nsg_window_stats_from_host(const uint64_t* keys_host, uint64_t n_pack
                                       uint64_t* keys_dev, uint64_t* out, uint64_t* out_host, void* workspace,
                                       size_t workspace_bytes, void* stream, void* copy_stream, uint32_t chunk_windows);
 
+/* nsg_window_stats_ex whose result rows are also stored, by the kernels' epilogues, into n_mirrors >= 1
+ * further tables: row w goes to mirrors[j] + (mirror_row0 + w) * NSG_NUM_STATS for every j.  mirrors is a
+ * device array of device pointers (8 B aligned) valid in this process — in the multi-GPU driver
+ * (distributed.py, transport "p2p") the CUDA-IPC-mapped result tables of every rank, so the all-gather of
+ * the 72 B/window results is done by the stores themselves over peer memory instead of a collective.
+ * Rows of windows recomputed by the L2 path are rewritten there later in stream order. */
+nsg_status nsg_window_stats_mirrored(const uint32_t* src, const uint32_t* dst, const uint64_t* keys,
+                                     uint64_t n_packets, uint64_t window, uint64_t* out, void* workspace,
+                                     size_t workspace_bytes, void* stream, uint32_t flags, uint64_t* const* mirrors,
+                                     uint32_t n_mirrors, uint64_t mirror_row0);
+
 /* Weighted rows: the paper's three-column frame src, dst, n_packets
  * (PAPER.md:207).  Row p adds its weight n_packets[p] to A_t(src_p, dst_p), so valid packets is the sum
  * of n_packets and a link is a nonzero of A_t: a row of weight 0 adds

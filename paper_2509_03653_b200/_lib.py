@@ -29,6 +29,7 @@ EXPORTS = (
     "nsg_window_stats_from_host",
     "nsg_window_vectors",
     "nsg_window_stats_weighted",
+    "nsg_window_stats_mirrored",
     "nsg_trace_workspace_bytes",
     "nsg_trace_partition",
     "nsg_trace_links",
@@ -147,6 +148,8 @@ def load() -> ctypes.CDLL:
     lib.nsg_trace_links_count.argtypes = [vp, vp, vp, u64, u32, vp, vp, vp, sz, u64, u64, vp]
     lib.nsg_trace_links_emit_peers.restype = ctypes.c_int
     lib.nsg_trace_links_emit_peers.argtypes = [u32, vp, vp, vp, vp, vp, sz, u64, u64, vp]
+    lib.nsg_window_stats_mirrored.restype = ctypes.c_int
+    lib.nsg_window_stats_mirrored.argtypes = [vp, vp, vp, u64, u64, vp, vp, sz, vp, u32, vp, u32, u64]
     lib.nsg_diag_offset.restype = sz
     lib.nsg_diag_offset.argtypes = []
     lib.nsg_last_launches.restype = ctypes.c_uint

@@ -571,3 +571,27 @@ def trace_links_emit_peers(world: int, ptrs_src: torch.Tensor, ptrs_dst: torch.T
                                          workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
     if rc != 0:
         raise NsgError(rc, "nsg_trace_links_emit_peers")
+
+
+
+def window_stats_mirrored(keys: torch.Tensor, mirrors: torch.Tensor, row0: int, window: int = DEFAULT_WINDOW, *,
+                          out=None, workspace: Optional[Workspace] = None, stream=None, flags: int = 0) -> torch.Tensor:
+    """window_stats_packed whose rows are also stored by the kernels into every table of `mirrors` (device
+    int64 [k] of device pointers, e.g. the IPC-mapped result tables of every rank) at row row0 + w
+    (nsg_window_stats_mirrored).  Returns the local int64 [n_windows, 9] result."""
+    _check(keys, "keys", _U64_TYPES)
+    n, device = keys.numel(), keys.device
+    window = int(window)
+    nw = num_windows(n, window)
+    if out is None:
+        out = torch.empty((nw, NUM_STATS), dtype=torch.int64, device=device)
+    if n == 0:
+        return out
+    ws = _workspace(n, window, device, workspace)
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    rc = _lib.nsg_window_stats_mirrored(None, None, keys.data_ptr(), n, window, out.data_ptr(), ws.ptr, ws.nbytes,
+                                        ctypes.c_void_p(s.cuda_stream), int(flags), mirrors.data_ptr(),
+                                        mirrors.numel(), int(row0))
+    if rc != 0:
+        raise NsgError(rc, "nsg_window_stats_mirrored")
+    return out

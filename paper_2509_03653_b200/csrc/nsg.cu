@@ -186,7 +186,8 @@ static WriteValue32Fn write_value32() {
 
 static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u64 W, u64* out, void* ws,
                       size_t ws_bytes, void* stream, u32 flags, void* ev_before = nullptr, void* ev_after = nullptr,
-                      const StreamIn* sin = nullptr, const nsg_vectors* vec = nullptr, const u32* wgt = nullptr) {
+                      const StreamIn* sin = nullptr, const nsg_vectors* vec = nullptr, const u32* wgt = nullptr,
+                      u64* const* mirror = nullptr, u32 n_mirror = 0, u64 mirror_row0 = 0) {
   g_last_launches = 0;
   if (W == 0 || W > NSG_MAX_WINDOW) return NSG_ERR_INVALID_ARGUMENT;
   if (n == 0) return NSG_OK;
@@ -196,6 +197,7 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
   if ((reinterpret_cast<uintptr_t>(ws) & 255) || (reinterpret_cast<uintptr_t>(out) & 7)) return NSG_ERR_INVALID_ARGUMENT;
   if (keys && (reinterpret_cast<uintptr_t>(keys) & 7)) return NSG_ERR_INVALID_ARGUMENT;
   if (wgt && (reinterpret_cast<uintptr_t>(wgt) & 3)) return NSG_ERR_INVALID_ARGUMENT;
+  if (n_mirror && (!mirror || (reinterpret_cast<uintptr_t>(mirror) & 7))) return NSG_ERR_INVALID_ARGUMENT;
   nsg_vectors V;
   memset(&V, 0, sizeof(V));
   if (vec) {
@@ -263,6 +265,7 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
   gg.v_node[1] = V.dst_node; gg.v_pk[1] = V.dst_packets; gg.v_fan[1] = V.dst_fanin;
   gg.v_ipsets = reinterpret_cast<u64*>(V.ip_sets);
   gg.wgt = wgt;
+  gg.mirror = mirror; gg.n_mirror = n_mirror; gg.mirror_row0 = mirror_row0;
 
   const bool use_fast = L.fast && !(flags & NSG_FLAG_FORCE_GLOBAL);
   if (use_fast) {
@@ -292,6 +295,7 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
     g.s0list = reinterpret_cast<u32*>(base + L.o_s0list);
     g.wgt = wgt;
     g.wscr = reinterpret_cast<u32*>(base + L.o_wscr);
+    g.mirror = mirror; g.n_mirror = n_mirror; g.mirror_row0 = mirror_row0;
     {  // ticket regions (see Geo): breakpoints where an item class enters or leaves the schedule
       u64 pts[8] = {0, (u64)LAG_L, (u64)LAG_S, (u64)LAG_F, L.nw, L.nw + LAG_L, L.nw + LAG_S, L.nw + LAG_F};
       std::sort(pts, pts + 8);
@@ -537,6 +541,16 @@ nsg_status nsg_window_vectors(const uint32_t* src, const uint32_t* dst, const ui
   return nsg::run(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_packets, window,
                   reinterpret_cast<nsg::u64*>(out), workspace, workspace_bytes, stream, flags, nullptr, nullptr,
                   nullptr, vectors);
+}
+
+nsg_status nsg_window_stats_mirrored(const uint32_t* src, const uint32_t* dst, const uint64_t* keys,
+                                     uint64_t n_packets, uint64_t window, uint64_t* out, void* workspace,
+                                     size_t workspace_bytes, void* stream, uint32_t flags, uint64_t* const* mirrors,
+                                     uint32_t n_mirrors, uint64_t mirror_row0) {
+  if (n_mirrors == 0 || !mirrors) return NSG_ERR_INVALID_ARGUMENT;
+  return nsg::run(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_packets, window, reinterpret_cast<nsg::u64*>(out),
+                  workspace, workspace_bytes, stream, flags, nullptr, nullptr, nullptr, nullptr, nullptr,
+                  reinterpret_cast<nsg::u64* const*>(mirrors), n_mirrors, mirror_row0);
 }
 
 nsg_status nsg_window_stats_weighted(const uint32_t* src, const uint32_t* dst, const uint64_t* keys,

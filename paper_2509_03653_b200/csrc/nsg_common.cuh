@@ -86,4 +86,11 @@ __device__ __forceinline__ u32 warp_append(bool want, u32* ctr) {
   return base + (u32)__popc(mask & ((1u << lane) - 1u));
 }
 
+// One result row (nine u64, column order of include/nsg.h: valid, links, max link, sources, max source
+// packets, max fan-out, destinations, max destination packets, max fan-in).
+__device__ __forceinline__ void store_row(u64* o, const u64* row) {
+#pragma unroll
+  for (int j = 0; j < 9; ++j) o[j] = row[j];
+}
+
 }  // namespace nsg

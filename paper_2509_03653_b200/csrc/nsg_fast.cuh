@@ -118,6 +118,11 @@ struct Geo {
   u32* s0win;   // [R][B2]         w+1 once side item S0(w, sb) has published its list (release)
   // Weighted rows (nsg_window_stats_weighted): n_packets per row, or NULL.
   const u32* wgt;
+  // Result mirrors (nsg_window_stats_mirrored): every row is also stored at mirror[j] + (row0 + w) * 9,
+  // e.g. the IPC-mapped result tables of every rank (the multi-GPU gather done by the epilogue itself).
+  u64* const* mirror;
+  u32 n_mirror;
+  u64 mirror_row0;
   u32* wscr;    // [R][cp*CH]      the weights, laid out like kscr
 };
 
@@ -881,16 +886,9 @@ __device__ void item_finalize(const Geo& g, u64 w, SmemMisc& m, u64* __restrict_
       r[9] += m.wtmp[9 * NWARP + i];
     }
     const u64 wlen = min(g.W, g.n - w * g.W);
-    u64* o = out + w * NSG_NUM_STATS;
-    o[NSG_VALID_PACKETS] = r[1];
-    o[NSG_UNIQUE_LINKS] = r[0];
-    o[NSG_MAX_LINK_PACKETS] = r[4];
-    o[NSG_UNIQUE_SOURCES] = r[2];
-    o[NSG_MAX_SOURCE_PACKETS] = r[5];
-    o[NSG_MAX_SOURCE_FANOUT] = r[6];
-    o[NSG_UNIQUE_DESTINATIONS] = r[3];
-    o[NSG_MAX_DESTINATION_PACKETS] = r[7];
-    o[NSG_MAX_DESTINATION_FANIN] = r[8];
+    const u64 row[NSG_NUM_STATS] = {r[1], r[0], r[4], r[2], r[5], r[6], r[3], r[7], r[8]};  // north_star order
+    store_row(out + w * NSG_NUM_STATS, row);
+    for (u32 j = 0; j < g.n_mirror; ++j) store_row(g.mirror[j] + (g.mirror_row0 + w) * NSG_NUM_STATS, row);
     if (g.v_ipsets) {  // |S u D|, |S \ D|, |D \ S|, |S n D|
       u64* ip = g.v_ipsets + w * 4;
       ip[0] = (u64)r[2] + r[3] - r[9]; ip[1] = r[2] - r[9]; ip[2] = r[3] - r[9]; ip[3] = r[9];

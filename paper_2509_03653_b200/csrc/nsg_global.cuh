@@ -26,6 +26,9 @@ struct GGeo {
   u32* v_node[2]; u32* v_pk[2]; u32* v_fan[2];
   u64* v_ipsets;
   const u32* wgt;  // weighted rows: n_packets per row (NULL: raw packets, weight 1)
+  u64* const* mirror;  // result mirrors (as Geo)
+  u32 n_mirror;
+  u64 mirror_row0;
 };
 
 __device__ __forceinline__ void glob_link_insert(u64* lkey, u32* lcnt, u64 LC, u64 key, u32 add) {
@@ -181,16 +184,9 @@ global_kernel(GGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, 
         for (int j = 0; j < 4; ++j) r[j] += red[j * (GT / 32) + i];
         for (int j = 4; j < 9; ++j) r[j] = max(r[j], red[j * (GT / 32) + i]);
       }
-      u64* o = out + w * NSG_NUM_STATS;
-      o[NSG_VALID_PACKETS] = r[1];
-      o[NSG_UNIQUE_LINKS] = r[0];
-      o[NSG_MAX_LINK_PACKETS] = r[4];
-      o[NSG_UNIQUE_SOURCES] = r[2];
-      o[NSG_MAX_SOURCE_PACKETS] = r[5];
-      o[NSG_MAX_SOURCE_FANOUT] = r[6];
-      o[NSG_UNIQUE_DESTINATIONS] = r[3];
-      o[NSG_MAX_DESTINATION_PACKETS] = r[7];
-      o[NSG_MAX_DESTINATION_FANIN] = r[8];
+      const u64 row[NSG_NUM_STATS] = {r[1], r[0], r[4], r[2], r[5], r[6], r[3], r[7], r[8]};  // north_star order
+      store_row(out + w * NSG_NUM_STATS, row);
+      for (u32 j = 0; j < g.n_mirror; ++j) store_row(g.mirror[j] + (g.mirror_row0 + w) * NSG_NUM_STATS, row);
       // self-check: the counts sum to the window's packets (sum of n_packets for weighted rows, which the
       // 32-bit counters support up to 2^32 - 1 per window: beyond that the window is reported in diag[2])
       if (wtot >= (1ull << 32)) atomicAdd(&g.diag[2], 1u);

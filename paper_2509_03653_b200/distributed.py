@@ -56,14 +56,35 @@ def gather_window_stats(local: torch.Tensor, n_windows: int, group=None) -> torc
     return torch.cat(pieces, dim=0).to(home)
 
 
-def distributed_window_stats(keys_local: torch.Tensor, n_windows: int, window: int, group=None,
-                             workspace=None) -> torch.Tensor:
-    """Per-rank CUDA computation of its window block (packed keys of exactly those windows) and the
-    NCCL gather of the [n_windows, 9] result onto every rank."""
-    from .api import window_stats_packed
+_result_tables: dict = {}
 
-    local = window_stats_packed(keys_local, window, workspace=workspace)
-    return gather_window_stats(local, n_windows, group)
+
+def distributed_window_stats(keys_local: torch.Tensor, n_windows: int, window: int, group=None,
+                             workspace=None, transport: str = "nccl") -> torch.Tensor:
+    """Per-rank CUDA computation of its window block (packed keys of exactly those windows) and the gather of
+    the [n_windows, 9] result onto every rank.  transport="nccl": all_gather_into_tensor; "p2p": the kernels'
+    epilogues store every row into every rank's CUDA-IPC-mapped result table (nsg_window_stats_mirrored), then
+    a stream sync + barrier; the tables are kept across calls."""
+    if transport == "nccl":
+        from .api import window_stats_packed
+
+        local = window_stats_packed(keys_local, window, workspace=workspace)
+        return gather_window_stats(local, n_windows, group)
+    if transport != "p2p":
+        raise ValueError("transport must be 'nccl' or 'p2p'")
+    from .api import window_stats_mirrored
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    device = keys_local.device
+    key = (id(group), n_windows, device.index)
+    tab = _result_tables.get(key)
+    if tab is None:
+        tab = _result_tables[key] = PeerBuffers(n_windows * NUM_STATS, group, device)
+    w0, w1 = window_block(n_windows, rank, world)
+    window_stats_mirrored(keys_local, tab.ptrs, w0, window, workspace=workspace)
+    torch.cuda.synchronize(device)
+    dist.barrier(group=group)  # every rank's rows are in every table
+    return tab.local[: n_windows * NUM_STATS].view(n_windows, NUM_STATS).clone()
 
 
 
