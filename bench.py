@@ -301,8 +301,12 @@ def main():
             if evs:
                 evs[1].record()
         elif world > 1 and args.transport == "p2p":  # rows stored into every rank's IPC-mapped table
+            if evs:  # events around the whole call (workspace reset + persistent kernel + overflow check)
+                evs[0].record()
             r = nsg.window_stats_mirrored(ring[i % RING], p2p_tab.ptrs, rank * WINDOWS_PER_STEP, WINDOW,
                                           out=outs[i % RING], workspace=ws)
+            if evs:
+                evs[1].record()
             return r
         else:
             r = nsg.window_stats_packed(ring[i % RING], WINDOW, out=outs[i % RING], workspace=ws, kernel_events=evs)

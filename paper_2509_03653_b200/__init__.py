@@ -24,12 +24,17 @@ from .api import (  # noqa: F401
     last_launches,
     num_windows,
     trace_links,
+    trace_links_count,
+    trace_links_emit_peers,
     trace_nodes,
+    trace_owner_counts,
     trace_partition,
+    trace_partition_peers,
     trace_stats,
     version,
     window_stats,
     window_stats_from_host,
+    window_stats_mirrored,
     window_stats_packed,
     window_stats_weighted,
     window_vectors,

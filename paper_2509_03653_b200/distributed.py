@@ -194,6 +194,21 @@ class PeerBuffers:
         self.opened = []
 
 
+_trace_buffers: dict = {}
+
+
+def _peer_buffers(name: str, capacity: int, group, device) -> "PeerBuffers":
+    """Receive buffers kept across calls, re-created (collectively: every rank computes the same capacity
+    from the same gathered counts) only when a call needs more than they hold."""
+    key = (id(group), name, device.index)
+    b = _trace_buffers.get(key)
+    if b is None or b.capacity < max(1, capacity):
+        if b is not None:
+            b.close()
+        b = _trace_buffers[key] = PeerBuffers(max(capacity, 1) * 5 // 4 + 1024, group, device)
+    return b
+
+
 def _trace_stats_p2p(keys_local: torch.Tensor, group=None) -> torch.Tensor:
     """distributed_trace_stats with the fused exchange: the partition and emission kernels store straight
     into the owners' receive buffers over peer memory, so no all-to-all collective moves the data."""
@@ -205,8 +220,8 @@ def _trace_stats_p2p(keys_local: torch.Tensor, group=None) -> torch.Tensor:
     ws = _trace_workspace(max(n, 1), 1, world, device)
     counts = trace_owner_counts(keys_local, world, ws)
     recv, base, cap = segment_plan(_all_gather_rows(counts, group), rank)
-    kbuf = PeerBuffers(cap, group, device)
-    dist.barrier(group=group)
+    kbuf = _peer_buffers("keys", cap, group, device)
+    dist.barrier(group=group)  # the previous call's readers are done with the buffers
     trace_partition_peers(keys_local, world, kbuf.ptrs, base.to(device), ws)
     torch.cuda.synchronize(device)
     dist.barrier(group=group)  # every sender's stores into this rank's buffer are complete
@@ -215,7 +230,7 @@ def _trace_stats_p2p(keys_local: torch.Tensor, group=None) -> torch.Tensor:
     link_stats, rc = trace_links_count(mine, world, ws)
     R = _all_gather_rows(rc, group)  # [world, 2, world]
     plans = [segment_plan(R[:, s, :], rank) for s in (0, 1)]
-    rbufs = [PeerBuffers(p[2], group, device) for p in plans]
+    rbufs = [_peer_buffers(f"records{s}", plans[s][2], group, device) for s in (0, 1)]
     dist.barrier(group=group)
     trace_links_emit_peers(world, rbufs[0].ptrs, rbufs[1].ptrs, plans[0][1].to(device), plans[1][1].to(device), ws)
     torch.cuda.synchronize(device)
@@ -223,8 +238,6 @@ def _trace_stats_p2p(keys_local: torch.Tensor, group=None) -> torch.Tensor:
     wsn = _trace_workspace(1, max(plans[0][0], plans[1][0], 1), 1, device)
     ns = _trace_nodes(rbufs[0].local[:plans[0][0]], wsn)
     nd = _trace_nodes(rbufs[1].local[:plans[1][0]], wsn)
-    for b in (kbuf, *rbufs):
-        b.close()
     return _trace_combine(link_stats, ns, nd, group)
 
 
