@@ -275,18 +275,33 @@ def main():
         torch.cuda.synchronize(dev)
         return 0
 
-    # Plain per-window statistics at N=1: batches alternate over `nstreams` streams (double-buffered
-    # workspaces); each call is still one whole pass of the hot path over its batch.
-    nstreams = max(1, args.streams) if (world == 1 and not (anon or trace or vec or wtd)) else 1
+    # Plain per-window statistics: batches alternate over `nstreams` streams (double-buffered workspaces);
+    # each call is still one whole pass of the hot path over its batch.  At N>1 the result gathers stay on
+    # one stream of their own, in step order (one communicator is never driven from two streams at once).
+    nstreams = max(1, args.streams) if not (anon or trace or vec or wtd) else 1
     wss = [ws] + [nsg.Workspace(n, WINDOW, dev) for _ in range(nstreams - 1)]
     streams = [torch.cuda.current_stream(dev)] + [torch.cuda.Stream(dev) for _ in range(nstreams - 1)]
+    gstream = torch.cuda.Stream(dev) if (nstreams > 1 and world > 1) else None
 
     def step(i, evs=None):
         if nstreams > 1:
             s_i = streams[i % nstreams]
             with torch.cuda.stream(s_i):
-                return nsg.window_stats_packed(ring[i % RING], WINDOW, out=outs[i % RING], workspace=wss[i % nstreams],
-                                               stream=s_i, kernel_events=evs)
+                if world > 1 and args.transport == "p2p":
+                    if evs:
+                        evs[0].record()
+                    r = nsg.window_stats_mirrored(ring[i % RING], p2p_tab.ptrs, rank * WINDOWS_PER_STEP, WINDOW,
+                                                  out=outs[i % RING], workspace=wss[i % nstreams])
+                    if evs:
+                        evs[1].record()
+                    return r
+                r = nsg.window_stats_packed(ring[i % RING], WINDOW, out=outs[i % RING], workspace=wss[i % nstreams],
+                                            stream=s_i, kernel_events=evs)
+            if gstream is not None:
+                gstream.wait_stream(s_i)
+                with torch.cuda.stream(gstream):
+                    gather_window_stats(r, WINDOWS_PER_STEP * world)
+            return r
         if anon:  # events around the whole call (bitmap reset + mark + rank prefix + relabel)
             if evs:
                 evs[0].record()
@@ -349,7 +364,7 @@ def main():
         s_.wait_event(start)
     for i in range(args.steps):
         step(i, kev[i])
-    for s_ in streams[1:]:
+    for s_ in streams[1:] + ([gstream] if gstream is not None else []):
         streams[0].wait_stream(s_)
     if p2p_tab is not None:  # every rank's rows are in every table before the clock stops
         torch.cuda.synchronize(dev)
