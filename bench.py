@@ -484,6 +484,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": "rows/s" if wtd else UNIT, "h2d_bytes_per_step": n * (12 if wtd else 8),
                     "d2h_bytes_per_step": d2h_bytes, "steps": e2e_steps},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "frac_vs_nominal_8000": achieved / 8000.0,
                          "traffic": traffic_per_launch(args.workload + ("-vectors" if vec else "-weighted" if wtd else "-trace" if trace else "-anonymize" if anon else "")), "peak_source": peak_src,
                          "kernel": ("nsg::anon_* (512 MiB bitmap; events around the whole call)" if anon else
                                     "nsg::trace_* (HBM tables; events around the whole call)" if trace else
