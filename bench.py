@@ -278,8 +278,10 @@ def main():
     # Plain per-window statistics: batches alternate over `nstreams` streams (double-buffered workspaces);
     # each call is still one whole pass of the hot path over its batch.  At N>1 the result gathers stay on
     # one stream of their own, in step order (one communicator is never driven from two streams at once).
-    nstreams = max(1, args.streams) if not (anon or trace or vec or wtd) else 1
+    nstreams = max(1, args.streams) if not (anon or trace) and (world == 1 or not (vec or wtd)) else 1
     wss = [ws] + [nsg.Workspace(n, WINDOW, dev) for _ in range(nstreams - 1)]
+    vbufs = [vbuf] + ([nsg.window_vectors(ring[0], WINDOW, out=outs[1], workspace=wss[1]) for _ in range(nstreams - 1)]
+                      if vec else [None] * (nstreams - 1))
     streams = [torch.cuda.current_stream(dev)] + [torch.cuda.Stream(dev) for _ in range(nstreams - 1)]
     gstream = torch.cuda.Stream(dev) if (nstreams > 1 and world > 1) else None
 
@@ -287,6 +289,18 @@ def main():
         if nstreams > 1:
             s_i = streams[i % nstreams]
             with torch.cuda.stream(s_i):
+                if vec or wtd:  # events around the whole call (workspace reset + persistent kernel + check)
+                    if evs:
+                        evs[0].record()
+                    if vec:
+                        r = nsg.window_vectors(ring[i % RING], WINDOW, out=outs[i % RING], workspace=wss[i % nstreams],
+                                               buffers=vbufs[i % nstreams], stream=s_i)["stats"]
+                    else:
+                        r = nsg.window_stats_weighted(ring[i % RING], wring[i % RING], WINDOW, out=outs[i % RING],
+                                                      workspace=wss[i % nstreams], stream=s_i)
+                    if evs:
+                        evs[1].record()
+                    return r
                 if world > 1 and args.transport == "p2p":
                     if evs:
                         evs[0].record()
