@@ -5,11 +5,12 @@ Windows are independent units (Table 2 is evaluated per traffic matrix 
 rank r of R owns the contiguous window block [floor(r*Nw/R), floor((r+1)*Nw/R)) and computes it
 with no data-path collective.  The only exchange is the 72 B/window result rows: one
 all_gather_into_tensor of an int64 [max_rows, 9] block per rank (NCCL over NVLink on GPUs, gloo in
-the CPU tests), after which every rank holds the [Nw, 9] table.
+the CPU tests), after which every rank holds the [Nw, 9] table — or, with transport "p2p", the kernels'
+epilogues store every row into every rank's CUDA-IPC-mapped table themselves.  The whole trace
+partitions links and nodes over the ranks and exchanges keys and link records (NCCL all-to-all, or the
+scatter kernels storing into the owners' IPC-mapped buffers).
 """
 from __future__ import annotations
-
-from typing import Optional
 
 import torch
 import torch.distributed as dist
