@@ -19,12 +19,18 @@
  *   Readings of the paper where it is silent or garbled are listed in DESIGN.md ("Readings"): directed
  *   links, self-loops are ordinary entries, every 32-bit address value is a vertex, empty max = 0.
  *
+ * Entry points: the nine statistics per window (nsg_window_stats*, raw packets; _weighted for rows
+ * with n_packets; _mirrored to store the rows into other tables too); the vector-valued rows and the IP
+ * set counts per window (nsg_window_vectors); the whole-trace statistics (nsg_trace_*, one GPU or the
+ * steps of a multi-GPU exchange, with nsg_ipc_* buffers for the peer-memory variant); IP anonymisation
+ * (nsg_anonymize).  SURVEY.md §8 maps them to the paper.
+ *
  * Addresses are IPv4 in host integer order (a.b.c.d <-> a<<24|b<<16|c<<8|d).  The packed form of a
  * packet is the u64 key (src << 32) | dst.
  *
  * Conventions for every entry point:
- *   - Ownership: the caller allocates every buffer; the library never allocates device memory and keeps
- *     no pointer after returning.  Device work is ASYNCHRONOUS on `stream` (a cudaStream_t passed as
+ *   - Ownership: the caller allocates every buffer; the library never allocates device memory (except
+ *     nsg_ipc_alloc, whose purpose is an IPC-exportable buffer) and keeps no pointer after returning.  Device work is ASYNCHRONOUS on `stream` (a cudaStream_t passed as
  *     void*; NULL = legacy default stream): buffers must stay alive and unmodified until the stream
  *     reaches that point.  out[] is only valid once the stream has completed the call.
  *   - Arguments: window >= 1 and window <= NSG_MAX_WINDOW; n_packets == 0 -> NSG_OK with no launch;
