@@ -193,6 +193,9 @@ def main():
                          "step's packets (nsg_trace_stats; N>1: distributed_trace_stats with all-to-all exchanges, "
                          "SURVEY §8(f) f4b); anonymize: relabel every address of each step's packets "
                          "(nsg_anonymize, one shuffle round, SURVEY §8(f) f2)")
+    ap.add_argument("--l2", choices=["cold", "warm"], default="cold",
+                    help="cold: steps cycle through a 1 GiB ring of batches (never L2-resident; the default and the "
+                         "headline); warm: one 64 MiB batch reused every step (L2-resident input, SURVEY §8(d))")
     ap.add_argument("--streams", type=int, default=2,
                     help="default path at N=1: consecutive batches alternate over this many CUDA streams with "
                          "their own workspaces, so a batch's pipeline fill overlaps the previous batch's drain")
@@ -239,8 +242,9 @@ def main():
 
     n = WINDOWS_PER_STEP * WINDOW
     # this rank's ring: batch i of rank r covers packets [((i * world) + r) * n, ...) of the stream
-    ring = torch.empty((RING, n), dtype=torch.int64, device=dev)
-    for i in range(RING):
+    ring_n = RING if args.l2 == "cold" else 1
+    ring = torch.empty((ring_n, n), dtype=torch.int64, device=dev)
+    for i in range(ring_n):
         gen.generate_device(dist_, seed, ((i * world) + rank) * n, n, keys=ring[i])
     torch.cuda.synchronize(dev)
     ws = nsg.Workspace(n, WINDOW, dev)
@@ -265,7 +269,7 @@ def main():
     if wtd:  # n_packets per row, seeded, uniform in [1, 8]
         gw = torch.Generator(device=dev)
         gw.manual_seed(1000 + seed + rank)
-        wring = torch.randint(1, 9, (RING, n), generator=gw, device=dev, dtype=torch.int32)
+        wring = torch.randint(1, 9, (ring_n, n), generator=gw, device=dev, dtype=torch.int32)
     vbuf = nsg.window_vectors(ring[0], WINDOW, out=outs[0], workspace=ws) if vec else None
     if args.once:
         if vec:
@@ -293,10 +297,10 @@ def main():
                     if evs:
                         evs[0].record()
                     if vec:
-                        r = nsg.window_vectors(ring[i % RING], WINDOW, out=outs[i % RING], workspace=wss[i % nstreams],
+                        r = nsg.window_vectors(ring[i % ring_n], WINDOW, out=outs[i % RING], workspace=wss[i % nstreams],
                                                buffers=vbufs[i % nstreams], stream=s_i)["stats"]
                     else:
-                        r = nsg.window_stats_weighted(ring[i % RING], wring[i % RING], WINDOW, out=outs[i % RING],
+                        r = nsg.window_stats_weighted(ring[i % ring_n], wring[i % ring_n], WINDOW, out=outs[i % RING],
                                                       workspace=wss[i % nstreams], stream=s_i)
                     if evs:
                         evs[1].record()
@@ -304,12 +308,12 @@ def main():
                 if world > 1 and args.transport == "p2p":
                     if evs:
                         evs[0].record()
-                    r = nsg.window_stats_mirrored(ring[i % RING], p2p_tab.ptrs, rank * WINDOWS_PER_STEP, WINDOW,
+                    r = nsg.window_stats_mirrored(ring[i % ring_n], p2p_tab.ptrs, rank * WINDOWS_PER_STEP, WINDOW,
                                                   out=outs[i % RING], workspace=wss[i % nstreams])
                     if evs:
                         evs[1].record()
                     return r
-                r = nsg.window_stats_packed(ring[i % RING], WINDOW, out=outs[i % RING], workspace=wss[i % nstreams],
+                r = nsg.window_stats_packed(ring[i % ring_n], WINDOW, out=outs[i % RING], workspace=wss[i % nstreams],
                                             stream=s_i, kernel_events=evs)
             if gstream is not None:
                 gstream.wait_stream(s_i)
@@ -319,40 +323,40 @@ def main():
         if anon:  # events around the whole call (bitmap reset + mark + rank prefix + relabel)
             if evs:
                 evs[0].record()
-            r = nsg.anonymize(ring[i % RING], seed=i, rounds=1)
+            r = nsg.anonymize(ring[i % ring_n], seed=i, rounds=1)
             if evs:
                 evs[1].record()
             return r
         if trace:  # events around the whole call (table resets + the trace kernels [+ exchanges])
             if evs:
                 evs[0].record()
-            r = nsg.trace_stats(ring[i % RING]) if world == 1 else \
-                distributed_trace_stats(ring[i % RING], transport=args.transport)
+            r = nsg.trace_stats(ring[i % ring_n]) if world == 1 else \
+                distributed_trace_stats(ring[i % ring_n], transport=args.transport)
             if evs:
                 evs[1].record()
             return r
         if vec:  # events around the whole call (workspace reset + persistent kernel + overflow check)
             if evs:
                 evs[0].record()
-            r = nsg.window_vectors(ring[i % RING], WINDOW, out=outs[i % RING], workspace=ws, buffers=vbuf)["stats"]
+            r = nsg.window_vectors(ring[i % ring_n], WINDOW, out=outs[i % RING], workspace=ws, buffers=vbuf)["stats"]
             if evs:
                 evs[1].record()
         elif wtd:  # events around the whole call (workspace reset + persistent kernel + overflow check)
             if evs:
                 evs[0].record()
-            r = nsg.window_stats_weighted(ring[i % RING], wring[i % RING], WINDOW, out=outs[i % RING], workspace=ws)
+            r = nsg.window_stats_weighted(ring[i % ring_n], wring[i % ring_n], WINDOW, out=outs[i % RING], workspace=ws)
             if evs:
                 evs[1].record()
         elif world > 1 and args.transport == "p2p":  # rows stored into every rank's IPC-mapped table
             if evs:  # events around the whole call (workspace reset + persistent kernel + overflow check)
                 evs[0].record()
-            r = nsg.window_stats_mirrored(ring[i % RING], p2p_tab.ptrs, rank * WINDOWS_PER_STEP, WINDOW,
+            r = nsg.window_stats_mirrored(ring[i % ring_n], p2p_tab.ptrs, rank * WINDOWS_PER_STEP, WINDOW,
                                           out=outs[i % RING], workspace=ws)
             if evs:
                 evs[1].record()
             return r
         else:
-            r = nsg.window_stats_packed(ring[i % RING], WINDOW, out=outs[i % RING], workspace=ws, kernel_events=evs)
+            r = nsg.window_stats_packed(ring[i % ring_n], WINDOW, out=outs[i % RING], workspace=ws, kernel_events=evs)
         if world > 1:
             gather_window_stats(r, WINDOWS_PER_STEP * world)
         return r
@@ -492,7 +496,8 @@ def main():
                        + ("; ANONYMISATION of each step's packets (unique, 1 Feistel shuffle round, gather); "
                           "8 B/packet written" if anon else ""),
                        "window": WINDOW, "packets_per_gpu_per_step": n, "parallelism": f"windows sharded dp{world}",
-                       "l2": f"inputs larger than L2: ring of {RING} x {n * 8 >> 20} MiB batches per GPU, no flush",
+                       "l2": (f"inputs larger than L2: ring of {RING} x {n * 8 >> 20} MiB batches per GPU, no flush"
+                              if ring_n > 1 else f"L2-warm: one {n * 8 >> 20} MiB batch reused every step"),
                        "input": "device-resident packed u64 keys (src<<32|dst)",
                        "streams": nstreams},
             "e2e": {"value": e2e_value, "unit": "rows/s" if wtd else UNIT, "h2d_bytes_per_step": n * (12 if wtd else 8),
