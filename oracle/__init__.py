@@ -72,7 +72,7 @@ def _load():
                           ctypes.c_void_p, ctypes.c_int]
             f = lib.nsg_oracle_window_distributions
             f.restype = ctypes.c_int
-            f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64] + \
+            f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64] + \
                 [ctypes.c_void_p] * 10 + [ctypes.c_int]
             lib.nsg_oracle_hardware_threads.restype = ctypes.c_uint
             _lib = lib
@@ -131,7 +131,8 @@ def window_stats_sort(src=None, dst=None, window: int = 1 << 17, *, keys=None, t
 IP_SETS = ("union", "src_only", "dst_only", "both")
 
 
-def window_distributions(src=None, dst=None, window: int = 1 << 17, *, keys=None, threads: int = 0) -> dict:
+def window_distributions(src=None, dst=None, window: int = 1 << 17, *, keys=None, weights=None,
+                         threads: int = 0) -> dict:
     """O1d: per window, the nonzeros of A_t and the row/column sums and nnz, each in ascending key
     order, plus the four IP set counts.
 
@@ -140,10 +141,14 @@ def window_distributions(src=None, dst=None, window: int = 1 << 17, *, keys=None
       src_node u32[n], src_packets u64[n], src_fan u64[n]     (counts[w,1] entries per window)
       dst_node u32[n], dst_packets u64[n], dst_fan u64[n]     (counts[w,2] entries per window)
       counts u64[nw, 3] = (links, sources, destinations); ip_sets u64[nw, 4] = IP_SETS order.
+    `weights`: optional u32 [n] n_packets per row (weighted rows as O1w; weight 0 adds nothing).
     """
     s, d = _split(src, dst, keys)
     if s.shape != d.shape:
         raise ValueError("src and dst must have the same length")
+    w8 = None if weights is None else _u32(weights)
+    if w8 is not None and w8.shape != s.shape:
+        raise ValueError("weights must have one entry per row")
     n = int(s.shape[0])
     if window < 1:
         raise ValueError("window must be >= 1")
@@ -157,7 +162,8 @@ def window_distributions(src=None, dst=None, window: int = 1 << 17, *, keys=None
     if n:
         order = ("link_key", "link_packets", "src_node", "src_packets", "src_fan", "dst_node", "dst_packets",
                  "dst_fan", "counts", "ip_sets")
-        rc = _load().nsg_oracle_window_distributions(s.ctypes.data, d.ctypes.data, n, int(window),
+        rc = _load().nsg_oracle_window_distributions(s.ctypes.data, d.ctypes.data,
+                                                     None if w8 is None else w8.ctypes.data, n, int(window),
                                                      *[r[k].ctypes.data for k in order], int(threads))
         if rc != 0:
             raise ValueError(f"nsg_oracle_window_distributions returned {rc}")

@@ -199,10 +199,13 @@ struct DistOut {
   uint64_t* ip_sets;  // [nw][4]
 };
 
-void window_dist(const uint32_t* src, const uint32_t* dst, uint64_t len, uint64_t w, uint64_t window,
-                 const DistOut& o) {
+// wgt: NULL for raw packets (weight 1), else the rows' n_packets (O1w's reading: a row of weight 0 adds
+// nothing, so it creates no link and no node).
+void window_dist(const uint32_t* src, const uint32_t* dst, const uint32_t* wgt, uint64_t len, uint64_t w,
+                 uint64_t window, const DistOut& o) {
   std::map<std::pair<uint32_t, uint32_t>, uint64_t> A;             // A_t(i,j)
-  for (uint64_t p = 0; p < len; ++p) A[{src[p], dst[p]}] += 1;
+  for (uint64_t p = 0; p < len; ++p)
+    if (!wgt || wgt[p] != 0) A[{src[p], dst[p]}] += wgt ? wgt[p] : 1;
   std::map<uint32_t, std::pair<uint64_t, uint64_t>> row, col;       // (sum, nnz) per row / column
   for (const auto& e : A) {
     row[e.first.first].first += e.second;   // (A_t 1)_i
@@ -298,9 +301,9 @@ int nsg_oracle_window_stats_weighted(const uint32_t* src, const uint32_t* dst, c
 }
 
 // Returns 0 on success, 1 on invalid arguments.  Every vector array is host [n] (window w's entries at
-// [w*window, w*window + cnt)); cnt is host [nw][3], ip_sets host [nw][4].
-int nsg_oracle_window_distributions(const uint32_t* src, const uint32_t* dst, uint64_t n, uint64_t window,
-                                    uint64_t* link_key, uint64_t* link_packets, uint32_t* src_node,
+// [w*window, w*window + cnt)); cnt is host [nw][3], ip_sets host [nw][4]; wgt host [n] or NULL (raw packets).
+int nsg_oracle_window_distributions(const uint32_t* src, const uint32_t* dst, const uint32_t* wgt, uint64_t n,
+                                    uint64_t window, uint64_t* link_key, uint64_t* link_packets, uint32_t* src_node,
                                     uint64_t* src_packets, uint64_t* src_fan, uint32_t* dst_node,
                                     uint64_t* dst_packets, uint64_t* dst_fan, uint64_t* cnt, uint64_t* ip_sets,
                                     int n_threads) {
@@ -316,7 +319,7 @@ int nsg_oracle_window_distributions(const uint32_t* src, const uint32_t* dst, ui
   auto worker = [&](unsigned t) {
     for (uint64_t w = t; w < nw; w += T) {
       const uint64_t b = w * window;
-      window_dist(src + b, dst + b, std::min(window, n - b), w, window, o);
+      window_dist(src + b, dst + b, wgt ? wgt + b : nullptr, std::min(window, n - b), w, window, o);
     }
   };
   std::vector<std::thread> pool;

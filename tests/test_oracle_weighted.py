@@ -100,3 +100,42 @@ def test_zero_weight_rows_are_ignored():
     s2[z] = 0xFFFFFFFF - np.arange(z.sum(), dtype=np.uint32)
     d2[z] = 0xFFFF0000 + np.arange(z.sum(), dtype=np.uint32)
     assert oracle.window_stats_weighted(s2, d2, wt, 3000).tolist() == base.tolist()
+
+
+# ---------------------------------------------------------------- weighted distributions (f1 x f4a)
+DKEYS = ("link_key", "link_packets", "src_node", "src_packets", "src_fan", "dst_node", "dst_packets", "dst_fan",
+         "ip_sets")
+
+
+def _dist_windows(r, W):
+    return [oracle.window_slices(r, W, w) for w in range(r["counts"].shape[0])]
+
+
+@pytest.mark.parametrize("dist", [gen.Dist("zipf", 1.1, 1 << 20), gen.Dist("heavy")])
+def test_weighted_distributions_equal_raw(dist):
+    """SPEC.md:142 for the vector-valued rows: the distributions of the per-window aggregated rows (weights =
+    multiplicities, padded with weight-0 rows) equal the raw packets' distributions, window by window."""
+    W = 1 << 14
+    s, d = gen.generate_host(dist, 52, 0, 3 * W)
+    raw = _dist_windows(oracle.window_distributions(s, d, W), W)
+    S, D, C = aggregate_windows(s, d, W, W, np.random.default_rng(2))
+    agg = _dist_windows(oracle.window_distributions(S, D, W, weights=C), W)
+    for a, b in zip(agg, raw):
+        for k in DKEYS:
+            assert np.asarray(a[k]).tolist() == np.asarray(b[k]).tolist(), k
+
+
+def test_weighted_distributions_expansion():
+    rng = np.random.default_rng(9)
+    for _ in range(100):
+        n = int(rng.integers(1, 200))
+        s = rng.integers(0, 30, n).astype(np.uint32)
+        d = rng.integers(0, 30, n).astype(np.uint32)
+        wt = rng.integers(0, 5, n).astype(np.uint32)
+        if wt.sum() == 0:
+            continue
+        a = _dist_windows(oracle.window_distributions(s, d, n, weights=wt), n)[0]
+        b = _dist_windows(oracle.window_distributions(np.repeat(s, wt), np.repeat(d, wt), int(wt.sum())),
+                          int(wt.sum()))[0]
+        for k in DKEYS:
+            assert np.asarray(a[k]).tolist() == np.asarray(b[k]).tolist(), k
