@@ -298,6 +298,13 @@ nsg_status nsg_anonymize(const uint32_t* src, const uint32_t* dst, const uint64_
                          uint64_t seed, uint32_t rounds, uint32_t* src_out, uint32_t* dst_out, uint64_t* n_unique,
                          void* workspace, size_t workspace_bytes, void* stream);
 
+/* nsg_window_vectors on weighted rows (src, dst, n_packets) as nsg_window_stats_weighted: link packets,
+ * source / destination packets are sums of n_packets; rows of weight 0 add nothing. */
+nsg_status nsg_window_vectors_weighted(const uint32_t* src, const uint32_t* dst, const uint64_t* keys,
+                                       const uint32_t* n_packets, uint64_t n_rows, uint64_t window, uint64_t* out,
+                                       const nsg_vectors* vectors, void* workspace, size_t workspace_bytes,
+                                       void* stream, uint32_t flags);
+
 /* Diagnostics of the last call that used `workspace` (device memory; read it after the stream has
  * completed the call): byte offset inside the workspace of a u32[4] =
  *   {windows the fast path handed to the L2 path because an SMEM table would overflow,

@@ -28,6 +28,7 @@ EXPORTS = (
     "nsg_window_stats_timed",
     "nsg_window_stats_from_host",
     "nsg_window_vectors",
+    "nsg_window_vectors_weighted",
     "nsg_window_stats_weighted",
     "nsg_window_stats_mirrored",
     "nsg_trace_workspace_bytes",
@@ -112,6 +113,8 @@ def load() -> ctypes.CDLL:
     lib.nsg_window_stats_from_host.argtypes = [vp, u64, u64, vp, vp, vp, vp, sz, vp, vp, u32]
     lib.nsg_window_vectors.restype = ctypes.c_int
     lib.nsg_window_vectors.argtypes = [vp, vp, vp, u64, u64, vp, ctypes.POINTER(NsgVectors), vp, sz, vp, u32]
+    lib.nsg_window_vectors_weighted.restype = ctypes.c_int
+    lib.nsg_window_vectors_weighted.argtypes = [vp, vp, vp, vp, u64, u64, vp, ctypes.POINTER(NsgVectors), vp, sz, vp, u32]
     lib.nsg_window_stats_weighted.restype = ctypes.c_int
     lib.nsg_window_stats_weighted.argtypes = [vp, vp, vp, vp, u64, u64, vp, vp, sz, vp, u32]
     lib.nsg_trace_workspace_bytes.restype = sz

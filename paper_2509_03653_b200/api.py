@@ -229,7 +229,7 @@ IP_SET_NAMES = ("union", "src_only", "dst_only", "both")
 def window_vectors(keys: Optional[torch.Tensor] = None, window: int = DEFAULT_WINDOW, *, src=None, dst=None,
                    links: bool = True, sources: bool = True, destinations: bool = True, ip_sets: bool = True,
                    out=None, workspace: Optional[Workspace] = None, stream=None, flags: int = 0,
-                   buffers: Optional[dict] = None) -> dict:
+                   buffers: Optional[dict] = None, n_packets: Optional[torch.Tensor] = None) -> dict:
     """The nine statistics plus the vector outputs of nsg_window_vectors.
 
     Input: packed `keys` (device int64/uint64) or SoA `src`, `dst` (device int32/uint32).  Returns a dict of
@@ -240,7 +240,8 @@ def window_vectors(keys: Optional[torch.Tensor] = None, window: int = DEFAULT_WI
     [w*window, w*window + count) with count = stats[w, 1] (links), stats[w, 3] (sources) or stats[w, 6]
     (destinations), in unspecified (hash) order; 32-bit values are the u32 bit patterns.
     `buffers`: optional preallocated output tensors (a dict as returned by an earlier call with the same
-    n and window), reused instead of allocating.
+    n and window), reused instead of allocating.  `n_packets`: optional device int32/uint32 [n] weights of
+    the rows (nsg_window_vectors_weighted; weighted rows as window_stats_weighted).
     """
     if keys is not None:
         if src is not None or dst is not None:
@@ -291,6 +292,17 @@ def window_vectors(keys: Optional[torch.Tensor] = None, window: int = DEFAULT_WI
         return r
     ws = _workspace(n, window, device, workspace)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    if n_packets is not None:
+        _check(n_packets, "n_packets", _U32_TYPES)
+        if n_packets.numel() != n or n_packets.device != device:
+            raise ValueError("n_packets must have one entry per row, on the rows' device")
+        rc = _lib.nsg_window_vectors_weighted(
+            None if src is None else src.data_ptr(), None if dst is None else dst.data_ptr(),
+            None if keys is None else keys.data_ptr(), n_packets.data_ptr(), n, window, out.data_ptr(),
+            ctypes.byref(v), ws.ptr, ws.nbytes, ctypes.c_void_p(s.cuda_stream), int(flags))
+        if rc != 0:
+            raise NsgError(rc, "nsg_window_vectors_weighted")
+        return r
     rc = _lib.nsg_window_vectors(
         None if src is None else src.data_ptr(), None if dst is None else dst.data_ptr(),
         None if keys is None else keys.data_ptr(), n, window, out.data_ptr(), ctypes.byref(v), ws.ptr, ws.nbytes,

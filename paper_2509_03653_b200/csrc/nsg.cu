@@ -825,6 +825,15 @@ nsg_status nsg_anonymize(const uint32_t* src, const uint32_t* dst, const uint64_
   return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }
 
+nsg_status nsg_window_vectors_weighted(const uint32_t* src, const uint32_t* dst, const uint64_t* keys,
+                                       const uint32_t* n_packets, uint64_t n_rows, uint64_t window, uint64_t* out,
+                                       const nsg_vectors* vectors, void* workspace, size_t workspace_bytes,
+                                       void* stream, uint32_t flags) {
+  if (!vectors || (n_rows && !n_packets)) return NSG_ERR_INVALID_ARGUMENT;
+  return nsg::run(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_rows, window, reinterpret_cast<nsg::u64*>(out),
+                  workspace, workspace_bytes, stream, flags, nullptr, nullptr, nullptr, vectors, n_packets);
+}
+
 size_t nsg_diag_offset(void) { return nsg::DIAG_OFFSET; }
 
 unsigned nsg_last_launches(void) { return nsg::g_last_launches; }

@@ -122,3 +122,27 @@ def test_sum_beyond_32_bits_is_reported(nsg, cuda_device):
     assert diag[2] == 1  # window 0 exceeds the 32-bit counters; window 1 is fine
     got = run_w(nsg, keys[2:], wt[2:], 2, cuda_device)
     assert got.tolist() == oracle.window_stats_weighted(keys=keys[2:], weights=wt[2:], window=2).tolist()
+
+
+@pytest.mark.parametrize("flags", [0, 1, 2])
+def test_weighted_vectors(nsg, cuda_device, flags):
+    """nsg_window_vectors_weighted: every vector and the IP sets of weighted rows vs the weighted O1d."""
+    from test_gpu_vectors import window_entries
+
+    n = 2 * W + 3001
+    keys = gen.generate_host(gen.Dist("zipf", 1.1, 1 << 18), 66, 0, n, packed=True)
+    wt = np.random.default_rng(7).integers(0, 6, n).astype(np.uint32)
+    kd = torch.from_numpy(keys.view(np.int64)).to(cuda_device)
+    wd = torch.from_numpy(wt.view(np.int32)).to(cuda_device)
+    r = nsg.window_vectors(kd, W, n_packets=wd, flags=flags)
+    torch.cuda.synchronize(cuda_device)
+    g = {k: (t.cpu().numpy().view(np.uint64) if t.dtype == torch.int64 else t.cpu().numpy().view(np.uint32))
+         for k, t in r.items()}
+    want = oracle.window_distributions(keys=keys, window=W, weights=wt)
+    assert g["stats"].tolist() == oracle.window_stats_weighted(keys=keys, weights=wt, window=W).tolist()
+    assert g["ip_sets"].tolist() == want["ip_sets"].tolist()
+    for w in range(want["counts"].shape[0]):
+        got, exp = window_entries(g, W, w), oracle.window_slices(want, W, w)
+        for f in ("link_key", "link_packets", "src_node", "src_packets", "src_fan", "dst_node", "dst_packets",
+                  "dst_fan"):
+            assert got[f].astype(np.uint64).tolist() == exp[f].astype(np.uint64).tolist(), (w, f)
