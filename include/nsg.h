@@ -305,6 +305,13 @@ nsg_status nsg_window_vectors_weighted(const uint32_t* src, const uint32_t* dst,
                                        const nsg_vectors* vectors, void* workspace, size_t workspace_bytes,
                                        void* stream, uint32_t flags);
 
+/* nsg_trace_stats on weighted rows (src, dst, n_packets; device u32 n_packets[n_rows], 4 B aligned): the
+ * whole-trace statistics with A(i,j) = summed n_packets (as nsg_window_stats_weighted, one window = the
+ * whole input); per-link and per-node sums must stay below 2^32.  Same workspace size as nsg_trace_stats. */
+nsg_status nsg_trace_stats_weighted(const uint32_t* src, const uint32_t* dst, const uint64_t* keys,
+                                    const uint32_t* n_packets, uint64_t n_rows, uint64_t* out, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+
 /* Diagnostics of the last call that used `workspace` (device memory; read it after the stream has
  * completed the call): byte offset inside the workspace of a u32[4] =
  *   {windows the fast path handed to the L2 path because an SMEM table would overflow,

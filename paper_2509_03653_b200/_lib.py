@@ -37,6 +37,7 @@ EXPORTS = (
     "nsg_trace_nodes",
     "nsg_trace_stats_workspace_bytes",
     "nsg_trace_stats",
+    "nsg_trace_stats_weighted",
     "nsg_ipc_handle_bytes",
     "nsg_ipc_alloc",
     "nsg_ipc_open",
@@ -127,6 +128,8 @@ def load() -> ctypes.CDLL:
     lib.nsg_trace_nodes.argtypes = [vp, u64, vp, vp, sz, u64, u64, vp]
     lib.nsg_trace_stats_workspace_bytes.restype = sz
     lib.nsg_trace_stats_workspace_bytes.argtypes = [u64]
+    lib.nsg_trace_stats_weighted.restype = ctypes.c_int
+    lib.nsg_trace_stats_weighted.argtypes = [vp, vp, vp, vp, u64, vp, vp, sz, vp]
     lib.nsg_trace_stats.restype = ctypes.c_int
     lib.nsg_trace_stats.argtypes = [vp, vp, vp, u64, vp, vp, sz, vp]
     lib.nsg_anonymize_workspace_bytes.restype = sz

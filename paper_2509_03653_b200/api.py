@@ -399,9 +399,11 @@ def _p(t):
     return None if t is None else t.data_ptr()
 
 
-def trace_stats(keys: Optional[torch.Tensor] = None, *, src=None, dst=None, out=None, stream=None) -> torch.Tensor:
+def trace_stats(keys: Optional[torch.Tensor] = None, *, src=None, dst=None, out=None, stream=None,
+                n_packets: Optional[torch.Tensor] = None) -> torch.Tensor:
     """The nine statistics of the WHOLE input (A = sum of the A_t; nsg_trace_stats, one GPU).  Returns a
-    device int64 [9] tensor, valid when `stream` completes."""
+    device int64 [9] tensor, valid when `stream` completes.  `n_packets`: optional device int32/uint32 [n]
+    weights of the rows (nsg_trace_stats_weighted)."""
     n, device = _rows(keys, src, dst)
     if out is None:
         out = torch.empty(NUM_STATS, dtype=torch.int64, device=device)
@@ -409,6 +411,15 @@ def trace_stats(keys: Optional[torch.Tensor] = None, *, src=None, dst=None, out=
         return out.zero_()
     ws = _Scratch(_lib.nsg_trace_stats_workspace_bytes(n), device)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    if n_packets is not None:
+        _check(n_packets, "n_packets", _U32_TYPES)
+        if n_packets.numel() != n or n_packets.device != device:
+            raise ValueError("n_packets must have one entry per row, on the rows' device")
+        rc = _lib.nsg_trace_stats_weighted(_p(src), _p(dst), _p(keys), n_packets.data_ptr(), n, out.data_ptr(),
+                                           ws.ptr, ws.nbytes, ctypes.c_void_p(s.cuda_stream))
+        if rc != 0:
+            raise NsgError(rc, "nsg_trace_stats_weighted")
+        return out
     rc = _lib.nsg_trace_stats(_p(src), _p(dst), _p(keys), n, out.data_ptr(), ws.ptr, ws.nbytes,
                               ctypes.c_void_p(s.cuda_stream))
     if rc != 0:

@@ -416,7 +416,8 @@ static bool input_ok(const u32* src, const u32* dst, const u64* keys) {
 }
 
 static nsg_status trace_links_impl(const u32* src, const u32* dst, const u64* keys, u64 n, u32 world, u64* link_stats,
-                                   u64* rec_src, u64* rec_dst, u64* rec_counts, TraceCall& c) {
+                                   u64* rec_src, u64* rec_dst, u64* rec_counts, TraceCall& c,
+                                   const u32* wgt = nullptr) {
   const TLayout& T = c.T;
   u32* esc = reinterpret_cast<u32*>(c.base + T.o_acc);
   LSlot* lt = reinterpret_cast<LSlot*>(c.base + T.o_lt);
@@ -426,7 +427,7 @@ static nsg_status trace_links_impl(const u32* src, const u32* dst, const u64* ke
     return NSG_ERR_CUDA;
   trace_fill<<<T.grid, TT, 0, c.s>>>(lt, T.LC, nullptr, 0);
   if (n) {
-    trace_link_insert<<<T.grid, TT, 0, c.s>>>(keys, src, dst, n, lt, T.LC, esc);
+    trace_link_insert<<<T.grid, TT, 0, c.s>>>(keys, src, dst, n, lt, T.LC, esc, wgt);
     g_last_launches++;
   }
   trace_link_count<<<T.grid, TT, 0, c.s>>>(lt, T.LC, esc, world, ccount, reinterpret_cast<unsigned long long*>(link_stats));
@@ -748,8 +749,25 @@ nsg_status nsg_trace_links_emit_peers(uint32_t world, uint64_t* const* peers_src
   return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }
 
+static nsg_status trace_stats_impl(const uint32_t* src, const uint32_t* dst, const uint64_t* keys,
+                                   const uint32_t* wgt, uint64_t n_packets, uint64_t* out, void* workspace,
+                                   size_t workspace_bytes, void* stream);
+
 nsg_status nsg_trace_stats(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
                            uint64_t* out, void* workspace, size_t workspace_bytes, void* stream) {
+  return trace_stats_impl(src, dst, keys, nullptr, n_packets, out, workspace, workspace_bytes, stream);
+}
+
+nsg_status nsg_trace_stats_weighted(const uint32_t* src, const uint32_t* dst, const uint64_t* keys,
+                                    const uint32_t* n_packets, uint64_t n_rows, uint64_t* out, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+  if (n_rows && (!n_packets || (reinterpret_cast<uintptr_t>(n_packets) & 3))) return NSG_ERR_INVALID_ARGUMENT;
+  return trace_stats_impl(src, dst, keys, n_packets, n_rows, out, workspace, workspace_bytes, stream);
+}
+
+static nsg_status trace_stats_impl(const uint32_t* src, const uint32_t* dst, const uint64_t* keys,
+                                   const uint32_t* wgt, uint64_t n_packets, uint64_t* out, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
   nsg::g_last_launches = 0;
   if (n_packets == 0) return NSG_OK;
   if (!nsg::input_ok(src, dst, reinterpret_cast<const nsg::u64*>(keys))) return NSG_ERR_INVALID_ARGUMENT;
@@ -765,7 +783,7 @@ nsg_status nsg_trace_stats(const uint32_t* src, const uint32_t* dst, const uint6
   nsg::u64* part = reinterpret_cast<nsg::u64*>(extra + 2 * nsg::align256((size_t)n_packets * 8));  // [12] + [2] counts
   // 256 B tail: link [0..2], src [4..6], dst [8..10], record counts [12..13]
   st = nsg::trace_links_impl(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_packets, 1, part, rec_src, rec_dst,
-                             part + 12, c);
+                             part + 12, c, wgt);
   if (st != NSG_OK) return st;
   // with one rank every record stays here; the node steps read the record counts from device memory, so
   // the whole call is asynchronous (no host sync for the counts)

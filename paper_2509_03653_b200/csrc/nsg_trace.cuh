@@ -184,22 +184,25 @@ __global__ void __launch_bounds__(TT) trace_part_scatter(const u64* __restrict__
 constexpr int TCACHE = 4096;
 __global__ void __launch_bounds__(TT) trace_link_insert(const u64* __restrict__ keys, const u32* __restrict__ src,
                                                         const u32* __restrict__ dst, u64 n, LSlot* __restrict__ lt,
-                                                        u64 LC, u32* __restrict__ esc) {
+                                                        u64 LC, u32* __restrict__ esc, const u32* __restrict__ wgt = nullptr) {
+  // wgt: weighted rows (n_packets per row; 0 adds nothing), NULL for raw packets
   __shared__ u64 ck[TCACHE];
   __shared__ u32 cc[TCACHE];
   for (int i = threadIdx.x; i < TCACHE; i += TT) { ck[i] = EMPTY64; cc[i] = 0; }
   __syncthreads();
   for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < n; i += (u64)gridDim.x * TT) {
+    const u32 a = wgt ? wgt[i] : 1u;
+    if (a == 0) continue;
     const u64 k = load_key(keys, src, dst, i);
-    if (k == EMPTY64) { atomicAdd(esc, 1u); continue; }  // the key ~0 is kept outside the table (reading R6)
+    if (k == EMPTY64) { atomicAdd(esc, a); continue; }  // the key ~0 is kept outside the table (reading R6)
     const u32 cs = (u32)((k * 0x9E3779B97F4A7C15ull) >> 52);  // an independent mix: owner and table use hash64
     u64 cur = ck[cs];
     if (cur == EMPTY64) {
       cur = atomicCAS(reinterpret_cast<unsigned long long*>(&ck[cs]), EMPTY64, k);
       if (cur == EMPTY64) cur = k;
     }
-    if (cur == k) atomicAdd(&cc[cs], 1u);
-    else tl_insert(lt, LC, k, 1u);
+    if (cur == k) atomicAdd(&cc[cs], a);
+    else tl_insert(lt, LC, k, a);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < TCACHE; i += TT)

@@ -143,3 +143,14 @@ def test_distributed_driver_two_ranks_one_gpu(cuda_device, transport):
     keys = gen.generate_host(gen.Dist("heavy"), 73, 0, n, packed=True)
     for r in range(world):
         assert results[r].view(np.uint64).tolist() == whole(keys)
+
+
+@pytest.mark.parametrize("n", [5000, 1 << 20])
+def test_trace_weighted(nsg, cuda_device, n):
+    """nsg_trace_stats_weighted: the whole trace of weighted rows vs O1w with window = n."""
+    keys = gen.generate_host(gen.Dist("zipf", 1.1, 1 << 16), 74, 0, n, packed=True)
+    wt = np.random.default_rng(n).integers(0, 7, n).astype(np.uint32)
+    kd = torch.from_numpy(keys.view(np.int64)).to(cuda_device)
+    got = nsg.trace_stats(kd, n_packets=torch.from_numpy(wt.view(np.int32)).to(cuda_device))
+    want = oracle.window_stats_weighted(keys=keys, weights=wt, window=n)[0]
+    assert got.cpu().numpy().view(np.uint64).tolist() == want.tolist()
