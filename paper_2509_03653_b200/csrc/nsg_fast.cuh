@@ -544,6 +544,22 @@ __device__ __noinline__ bool link_finish_h(u64* lkey, u32* lcnt, u32* hist, u32 
 
 constexpr u32 WAVE_TAIL = 512; // pending entries (<= list capacity) finish per lane: measured faster than barrier-separated waves
 
+// Drop the L2 lines lying entirely inside byte range [lo, hi) of `base` (this warp consumed them and
+// nobody reads them again before the slot is rewritten), so dead scratch is never written back to DRAM.
+// Lines shared with a neighbouring segment are kept.  All lanes of the warp call it.
+__device__ __forceinline__ void discard_interior(const unsigned char* base, u64 lo, u64 hi) {
+  const u64 first = (lo + 127) & ~127ull, last = hi & ~127ull;
+  for (u64 a = first + (u64)(threadIdx.x & 31) * 128; a < last; a += 32 * 128) discard_l2_line(base + a);
+}
+__device__ __forceinline__ void discard_segments(const void* base, u32 esize, const u32* wlo, const u32* wpre,
+                                                 u32 nseg) {
+#ifdef NSG_DISCARD_CONSUMED
+  for (u32 q = 0; q < nseg; ++q)
+    discard_interior(reinterpret_cast<const unsigned char*>(base), (u64)wlo[q] * esize,
+                     ((u64)wlo[q] + (wpre[q + 1] - wpre[q])) * esize);
+#endif
+}
+
 // Warp-level gather setup: lane q < nseg describes segment q of this warp (global element offset `lo`,
 // length `len`); the warp publishes segment starts and exclusive prefixes into its SMEM rows and
 // returns the warp's element total.  No CTA barrier is involved.
@@ -672,6 +688,8 @@ __device__ void item_link(const Geo& g, u64 w, u32 b, SL& s, SmemMisc& m, Claim&
     for (int o = 16; o > 0; o >>= 1) wl += __shfl_xor_sync(0xffffffffu, wl, o);
     if (lane == 0 && wl) atomicAdd(&m.wsum, wl);
   }
+  discard_segments(ks, 8, wlo, wpre, nseg);  // this warp's key segments are consumed
+  if constexpr (WT) discard_segments(wsc, 4, wlo, wpre, nseg);
   __syncthreads();
   pt.mark(g, 1, 1);
   prof_pending(g, 1, m.pcnt[0]);
@@ -1093,6 +1111,7 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
       const u32 sp = warp_sum(c_p), sf = warp_sum(c_f);
       if (lane == 0) ok = node_flush(s.key, s.P, s.F, m.esc, c_node, sp, sf) && ok;
     }
+    discard_segments(rs, 8, wlo, wpre, nseg);  // this warp's record segments are consumed
   }
   __syncthreads();
   pt.mark(g, 2, 1);
