@@ -22,6 +22,9 @@
 // once its previous window is final (RSLOTS windows in flight).  Dependencies are counted
 // semaphores: __syncthreads() + red.release.gpu by one thread to signal, ld.acquire.gpu spin by one
 // thread + __syncthreads() to wait.
+// Options of the same kernel (Geo): weighted rows (fast_kernel<true>: P and L items carry n_packets per
+// key), vector outputs (L items append each link, S items each node; S1 items count |S n D| from the
+// S0 item's node list), result mirrors (F writes its row into further tables, e.g. peer ranks').
 #pragma once
 #include "nsg.h"
 #include "nsg_common.cuh"
