@@ -48,6 +48,9 @@ def workload(name: str):
         return gen.Dist("heavy"), 3, "C3: heavy skew (Bernoulli(1/2) source 10.0.0.1, uniform dst), seed 3"
     if name == "C1":
         return gen.Dist("uniform"), 1, "C1-shaped: uniform 32-bit src/dst, seed 1"
+    if name in ("Z08", "Z13", "Z15"):  # SURVEY §8(d) optional sweep of the Zipf exponent
+        z = {"Z08": 0.8, "Z13": 1.3, "Z15": 1.5}[name]
+        return gen.Dist("zipf", z, 1 << 20), 2, f"{name}: Zipf(s={z}, K=2^20) IPv4 pairs, seed 2"
     raise SystemExit(f"unknown workload {name}")
 
 
