@@ -50,13 +50,18 @@ __global__ void __launch_bounds__(TT) trace_fill(LSlot* __restrict__ lt, u64 LC,
     reinterpret_cast<uint4*>(nt)[i] = make_uint4(EMPTY32, 0u, 0u, 0u);
 }
 
+// A free slot is claimed together with its first count by one 128-bit CAS ({~0, 0, 0} -> {key, add, 0}):
+// a new entry costs one probe load and one atomic instead of a CAS and an add (random DRAM sectors).
+typedef unsigned __int128 u128;
 __device__ __forceinline__ void tl_insert(LSlot* t, u64 LC, u64 key, u32 add) {
   u64 slot = hash64(key) & (LC - 1);
+  const u128 empty = (u128)EMPTY64;
   for (;;) {
     u64 k = ldcg64(&t[slot].key);
     if (k == EMPTY64) {
-      const u64 old = atomicCAS(reinterpret_cast<unsigned long long*>(&t[slot].key), EMPTY64, key);
-      k = (old == EMPTY64) ? key : old;
+      const u128 old = atomicCAS(reinterpret_cast<u128*>(&t[slot]), empty, (u128)key | ((u128)add << 64));
+      if (old == empty) return;
+      k = (u64)old;
     }
     if (k == key) { atomicAdd(&t[slot].cnt, add); return; }
     slot = (slot + 1) & (LC - 1);  // >= 2x the keys' slots: never full
@@ -66,11 +71,14 @@ __device__ __forceinline__ void tl_insert(LSlot* t, u64 LC, u64 key, u32 add) {
 __device__ __forceinline__ void tn_upsert(NSlot* t, u64 NC, u32* esc, u32 node, u32 p, u32 f) {
   if (node == EMPTY32) { atomicAdd(&esc[0], p); atomicAdd(&esc[1], f); return; }
   u64 slot = ((u64)hash32(node) * 0x9E3779B97F4A7C15ull >> 11) & (NC - 1);
+  const u128 empty = (u128)EMPTY32;  // {key ~0, P 0, F 0, pad 0}
   for (;;) {
     u32 k = ldcg32(&t[slot].key);
-    if (k == EMPTY32) {
-      const u32 old = atomicCAS(&t[slot].key, EMPTY32, node);
-      k = (old == EMPTY32) ? node : old;
+    if (k == EMPTY32) {  // claim with the first packets and links in one 128-bit CAS
+      const u128 old = atomicCAS(reinterpret_cast<u128*>(&t[slot]), empty,
+                                 (u128)node | ((u128)p << 32) | ((u128)f << 64));
+      if (old == empty) return;
+      k = (u32)old;
     }
     if (k == node) { atomicAdd(&t[slot].P, p); atomicAdd(&t[slot].F, f); return; }
     slot = (slot + 1) & (NC - 1);
