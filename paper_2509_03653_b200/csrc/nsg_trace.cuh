@@ -17,6 +17,7 @@
 namespace nsg {
 
 constexpr int TT = 512;          // threads per CTA of the trace kernels
+constexpr u64 TRACE_CAS_FIRST_SLOTS = 1ull << 26;  // tables this large live in DRAM: probe by CAS (tl_insert)
 constexpr int TRACE_MAX_WORLD = 1024;
 
 // owner rank of a link / of a node (independent of the table slots, which use the low bits)
@@ -53,11 +54,14 @@ __global__ void __launch_bounds__(TT) trace_fill(LSlot* __restrict__ lt, u64 LC,
 // A free slot is claimed together with its first count by one 128-bit CAS ({~0, 0, 0} -> {key, add, 0}):
 // a new entry costs one probe load and one atomic instead of a CAS and an add (random DRAM sectors).
 typedef unsigned __int128 u128;
-__device__ __forceinline__ void tl_insert(LSlot* t, u64 LC, u64 key, u32 add) {
+// cas_first: the CAS itself is the probe (it returns the slot's key when the claim fails) — fewer
+// operations per new key, best when the table lives in DRAM; otherwise a load probes first and only a
+// free slot is CASed — cheaper when occupied slots are L2 hits (measured crossover ~2^25 keys).
+__device__ __forceinline__ void tl_insert(LSlot* t, u64 LC, u64 key, u32 add, bool cas_first = false) {
   u64 slot = hash64(key) & (LC - 1);
   const u128 empty = (u128)EMPTY64;
   for (;;) {
-    u64 k = ldcg64(&t[slot].key);
+    u64 k = cas_first ? EMPTY64 : ldcg64(&t[slot].key);
     if (k == EMPTY64) {
       const u128 old = atomicCAS(reinterpret_cast<u128*>(&t[slot]), empty, (u128)key | ((u128)add << 64));
       if (old == empty) return;
@@ -68,15 +72,14 @@ __device__ __forceinline__ void tl_insert(LSlot* t, u64 LC, u64 key, u32 add) {
   }
 }
 
-__device__ __forceinline__ void tn_upsert(NSlot* t, u64 NC, u32* esc, u32 node, u32 p, u32 f) {
+__device__ __forceinline__ void tn_upsert(NSlot* t, u64 NC, u32* esc, u32 node, u32 p, u32 f, bool cas_first = false) {
   if (node == EMPTY32) { atomicAdd(&esc[0], p); atomicAdd(&esc[1], f); return; }
   u64 slot = ((u64)hash32(node) * 0x9E3779B97F4A7C15ull >> 11) & (NC - 1);
   const u128 empty = (u128)EMPTY32;  // {key ~0, P 0, F 0, pad 0}
-  for (;;) {
-    u32 k = ldcg32(&t[slot].key);
-    if (k == EMPTY32) {  // claim with the first packets and links in one 128-bit CAS
-      const u128 old = atomicCAS(reinterpret_cast<u128*>(&t[slot]), empty,
-                                 (u128)node | ((u128)p << 32) | ((u128)f << 64));
+  for (;;) {  // claim with the first packets and links in one 128-bit CAS (the probe, when cas_first)
+    u32 k = cas_first ? EMPTY32 : ldcg32(&t[slot].key);
+    if (k == EMPTY32) {
+      const u128 old = atomicCAS(reinterpret_cast<u128*>(&t[slot]), empty, (u128)node | ((u128)p << 32) | ((u128)f << 64));
       if (old == empty) return;
       k = (u32)old;
     }
@@ -194,6 +197,7 @@ __global__ void __launch_bounds__(TT) trace_link_insert(const u64* __restrict__ 
                                                         const u32* __restrict__ dst, u64 n, LSlot* __restrict__ lt,
                                                         u64 LC, u32* __restrict__ esc, const u32* __restrict__ wgt = nullptr) {
   // wgt: weighted rows (n_packets per row; 0 adds nothing), NULL for raw packets
+  const bool cas_first = LC >= TRACE_CAS_FIRST_SLOTS;
   __shared__ u64 ck[TCACHE];
   __shared__ u32 cc[TCACHE];
   for (int i = threadIdx.x; i < TCACHE; i += TT) { ck[i] = EMPTY64; cc[i] = 0; }
@@ -210,11 +214,11 @@ __global__ void __launch_bounds__(TT) trace_link_insert(const u64* __restrict__ 
       if (cur == EMPTY64) cur = k;
     }
     if (cur == k) atomicAdd(&cc[cs], a);
-    else tl_insert(lt, LC, k, a);
+    else tl_insert(lt, LC, k, a, cas_first);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < TCACHE; i += TT)
-    if (ck[i] != EMPTY64) tl_insert(lt, LC, ck[i], cc[i]);
+    if (ck[i] != EMPTY64) tl_insert(lt, LC, ck[i], cc[i], cas_first);
 }
 
 // Per CTA slot range: link statistics (valid = sum of counts, unique links, max link; PAPER.md:180, :181,
@@ -321,11 +325,11 @@ __device__ __forceinline__ void node_records(const u64* __restrict__ rec, u64 m,
       if (cur == EMPTY32) cur = node;
     }
     if (cur == node) { atomicAdd(&cp[cs], c); atomicAdd(&cf[cs], 1u); }
-    else tn_upsert(nt, NC, esc, node, c, 1u);
+    else tn_upsert(nt, NC, esc, node, c, 1u, NC >= TRACE_CAS_FIRST_SLOTS);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < TCACHE; i += TT)
-    if (ck[i] != EMPTY32) tn_upsert(nt, NC, esc, ck[i], cp[i], cf[i]);
+    if (ck[i] != EMPTY32) tn_upsert(nt, NC, esc, ck[i], cp[i], cf[i], NC >= TRACE_CAS_FIRST_SLOTS);
 }
 static_assert(TCACHE == 4096, "node cache slot uses 12 hash bits");
 
