@@ -444,10 +444,10 @@ static nsg_status trace_nodes_counted(const u64* rec, const u64* m_dev, u64* nod
   NSlot* nt = reinterpret_cast<NSlot*>(c.base + T.o_nt);
   if (cudaMemsetAsync(esc, 0, 8, c.s) != cudaSuccess || cudaMemsetAsync(node_stats, 0, 24, c.s) != cudaSuccess)
     return NSG_ERR_CUDA;
-  trace_fill<<<T.grid, TT, 0, c.s>>>(nullptr, 0, nt, T.NC);
+  trace_fill<<<T.grid, TT, 0, c.s>>>(nullptr, 0, nt, T.NC, m_dev);  // tables sized by the device record count
   g_last_launches++;
   trace_node_insert_dev<<<T.grid, TT, 0, c.s>>>(rec, m_dev, nt, T.NC, esc);
-  trace_node_scan<<<T.grid, TT, 0, c.s>>>(nt, T.NC, esc, reinterpret_cast<unsigned long long*>(node_stats));
+  trace_node_scan<<<T.grid, TT, 0, c.s>>>(nt, T.NC, esc, reinterpret_cast<unsigned long long*>(node_stats), m_dev);
   g_last_launches += 2;
   return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }

@@ -44,7 +44,19 @@ __device__ __forceinline__ u64 load_key(const u64* keys, const u32* src, const u
 struct __align__(16) LSlot { u64 key; u32 cnt; u32 pad; };
 struct __align__(16) NSlot { u32 key, P, F, pad; };
 
-__global__ void __launch_bounds__(TT) trace_fill(LSlot* __restrict__ lt, u64 LC, NSlot* __restrict__ nt, u64 NC) {
+// Node-table slots actually used: next_pow2(2m) for m records (m read from the device: the single-GPU
+// trace knows its record count only there), at most the workspace's NC.
+__device__ __forceinline__ u64 node_cap(u64 NC, const u64* m_dev) {
+  if (!m_dev) return NC;
+  const u64 m = *m_dev;
+  u64 c = 2;
+  while (c < 2 * m && c < NC) c <<= 1;
+  return c < NC ? c : NC;
+}
+
+__global__ void __launch_bounds__(TT) trace_fill(LSlot* __restrict__ lt, u64 LC, NSlot* __restrict__ nt, u64 NC,
+                                                 const u64* __restrict__ m_dev = nullptr) {
+  NC = node_cap(NC, m_dev);
   for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < LC; i += (u64)gridDim.x * TT)
     reinterpret_cast<ulonglong2*>(lt)[i] = make_ulonglong2(EMPTY64, 0ull);
   for (u64 i = (u64)blockIdx.x * TT + threadIdx.x; i < NC; i += (u64)gridDim.x * TT)
@@ -343,11 +355,13 @@ __global__ void __launch_bounds__(TT) trace_node_insert(const u64* __restrict__ 
 __global__ void __launch_bounds__(TT) trace_node_insert_dev(const u64* __restrict__ rec, const u64* __restrict__ m_dev,
                                                             NSlot* __restrict__ nt, u64 NC, u32* __restrict__ esc) {
   __shared__ u32 ck[TCACHE], cp[TCACHE], cf[TCACHE];
-  node_records(rec, *m_dev, nt, NC, esc, ck, cp, cf);
+  node_records(rec, *m_dev, nt, node_cap(NC, m_dev), esc, ck, cp, cf);
 }
 
 __global__ void __launch_bounds__(TT) trace_node_scan(const NSlot* __restrict__ nt, u64 NC, const u32* __restrict__ esc,
-                                                      unsigned long long* __restrict__ acc) {
+                                                      unsigned long long* __restrict__ acc,
+                                                      const u64* __restrict__ m_dev = nullptr) {
+  NC = node_cap(NC, m_dev);
   __shared__ unsigned long long s_n, s_p, s_f;
   if (threadIdx.x == 0) { s_n = 0; s_p = 0; s_f = 0; }
   __syncthreads();
