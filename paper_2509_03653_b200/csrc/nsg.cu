@@ -782,14 +782,25 @@ static nsg_status trace_stats_impl(const uint32_t* src, const uint32_t* dst, con
   nsg::u64* rec_dst = reinterpret_cast<nsg::u64*>(extra + nsg::align256((size_t)n_packets * 8));
   nsg::u64* part = reinterpret_cast<nsg::u64*>(extra + 2 * nsg::align256((size_t)n_packets * 8));  // [12] + [2] counts
   // 256 B tail: link [0..2], src [4..6], dst [8..10], record counts [12..13]
-  st = nsg::trace_links_impl(src, dst, reinterpret_cast<const nsg::u64*>(keys), n_packets, 1, part, rec_src, rec_dst,
-                             part + 12, c, wgt);
-  if (st != NSG_OK) return st;
-  // with one rank every record stays here; the node steps read the record counts from device memory, so
+  {  // links: one pass gives the statistics and both sides' records (same positions on both sides)
+    const nsg::TLayout& T = c.T;
+    nsg::u32* esc = reinterpret_cast<nsg::u32*>(c.base + T.o_acc);
+    nsg::LSlot* lt = reinterpret_cast<nsg::LSlot*>(c.base + T.o_lt);
+    if (cudaMemsetAsync(esc, 0, 16, c.s) != cudaSuccess || cudaMemsetAsync(part, 0, 16 * sizeof(nsg::u64), c.s) != cudaSuccess)
+      return NSG_ERR_CUDA;
+    nsg::trace_fill<<<T.grid, nsg::TT, 0, c.s>>>(lt, T.LC, nullptr, 0);
+    nsg::trace_link_insert<<<T.grid, nsg::TT, 0, c.s>>>(reinterpret_cast<const nsg::u64*>(keys), src, dst, n_packets,
+                                                        lt, T.LC, esc, wgt);
+    nsg::trace_link_emit1<<<T.grid, nsg::TT, 0, c.s>>>(lt, T.LC, esc, rec_src, rec_dst,
+                                                       reinterpret_cast<unsigned long long*>(part + 12),
+                                                       reinterpret_cast<unsigned long long*>(part));
+    nsg::g_last_launches += 3;
+  }
+  // with one rank every record stays here; the node steps read the record count from device memory, so
   // the whole call is asynchronous (no host sync for the counts)
   st = nsg::trace_nodes_counted(rec_src, part + 12, part + 4, c);
   if (st != NSG_OK) return st;
-  st = nsg::trace_nodes_counted(rec_dst, part + 13, part + 8, c);
+  st = nsg::trace_nodes_counted(rec_dst, part + 12, part + 8, c);
   if (st != NSG_OK) return st;
   nsg::trace_finish<<<1, 32, 0, c.s>>>(reinterpret_cast<unsigned long long*>(part),
                                        reinterpret_cast<unsigned long long*>(part + 4),

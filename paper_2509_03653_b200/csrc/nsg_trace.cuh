@@ -319,6 +319,80 @@ __global__ void __launch_bounds__(TT) trace_link_emit(const LSlot* __restrict__ 
   }
 }
 
+// ---- one rank (nsg_trace_stats): statistics and records in a single pass over the link table.  Each
+// CTA walks its slot range in tiles of TT*8 slots; a tile's links get consecutive record positions from
+// one global cursor (one atomic per tile), the same position on both sides.
+__global__ void __launch_bounds__(TT) trace_link_emit1(const LSlot* __restrict__ lt, u64 LC,
+                                                       const u32* __restrict__ esc, u64* __restrict__ rec_src,
+                                                       u64* __restrict__ rec_dst, unsigned long long* __restrict__ cursor,
+                                                       unsigned long long* __restrict__ acc) {
+  constexpr int PER = 8;
+  __shared__ u32 wsum[TT / 32];
+  __shared__ unsigned long long tile_base, s_sum, s_links, s_max;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  if (t == 0) { s_sum = 0; s_links = 0; s_max = 0; }
+  u64 lo, hi;
+  cta_range(LC, lo, hi);
+  unsigned long long sm = 0, nl = 0;
+  u32 mx = 0;
+  for (u64 t0 = lo; t0 < hi; t0 += (u64)TT * PER) {
+    ulonglong2 e[PER];
+    u32 cnt = 0;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const u64 i = t0 + (u64)t * PER + q;
+      e[q] = i < hi ? __ldcg(reinterpret_cast<const ulonglong2*>(lt) + i) : make_ulonglong2(EMPTY64, 0ull);
+      cnt += e[q].x != EMPTY64;
+    }
+    u32 x = cnt;  // block exclusive scan of the per-thread link counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      u32 w = lane < TT / 32 ? wsum[lane] : 0u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      if (lane < TT / 32) wsum[lane] = w;
+      if (lane == TT / 32 - 1) tile_base = w ? atomicAdd(cursor, (unsigned long long)w) : 0ull;
+    }
+    __syncthreads();
+    u64 pos = tile_base + (x - cnt) + (wid ? wsum[wid - 1] : 0u);
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      if (e[q].x == EMPTY64) continue;
+      const u32 c = (u32)e[q].y;
+      sm += c; nl += 1; mx = max(mx, c);
+      rec_src[pos] = link_rec((u32)(e[q].x >> 32), c);
+      rec_dst[pos] = link_rec((u32)e[q].x, c);
+      ++pos;
+    }
+    __syncthreads();  // wsum / tile_base are reused by the next tile
+  }
+  if (blockIdx.x == 0 && t == 0 && esc[0]) {  // the escaped key ~0 -> ~0
+    const u32 c = esc[0];
+    sm += c; nl += 1; mx = max(mx, c);
+    const u64 p = atomicAdd(cursor, 1ull);
+    rec_src[p] = link_rec(EMPTY32, c);
+    rec_dst[p] = link_rec(EMPTY32, c);
+  }
+  if (sm) atomicAdd(&s_sum, sm);
+  if (nl) atomicAdd(&s_links, nl);
+  if (mx) atomicMax(&s_max, (unsigned long long)mx);
+  __syncthreads();
+  if (t == 0) {
+    if (s_sum) atomicAdd(&acc[0], s_sum);
+    if (s_links) atomicAdd(&acc[1], s_links);
+    if (s_max) atomicMax(&acc[2], s_max);
+  }
+}
+
 // ---- nodes: merge the records of one side; unique nodes, max packets (:186), max fan (:188)
 // Records of a node are merged in a per-CTA SMEM cache first, as trace_link_insert does for links (hot
 // sources / destinations would otherwise serialise on one global counter).
