@@ -89,7 +89,9 @@ enum {
                                           overflowed window are then undefined (never use for results) */
   NSG_FLAG_PROFILE = 1u << 3           /* accumulate per-work-item-type SM cycles into the workspace:
                                           u64[112] at nsg_diag_offset()+64: [0..12) per type (partition, link,
-                                          side) {items, cycles, wait cycles, max work}; [16+16*type+phase] cycles per phase, [64+...] max */
+                                          side) {items, cycles, wait cycles, max work}; [16+16*type+phase] cycles per phase, [64+...] max */,
+  NSG_FLAG_LEGACY_FAST = 1u << 4       /* run the round-1 persistent kernel (nsg_fast.cuh) instead of the
+                                          round-2 kernel (nsg_win.cuh) for windows < 2^20 (A/B measurement) */
 };
 
 /* Number of windows: ceil(n_packets / window); 0 if n_packets == 0 or window == 0. */

@@ -13,7 +13,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.path.join(_PKG, "libnsg.so")
 SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("nsg.cu", "nsg_common.cuh", "nsg_fast.cuh", "nsg_global.cuh",
-                                                   "nsg_trace.cuh", "nsg_anon.cuh")]
+                                                   "nsg_trace.cuh", "nsg_anon.cuh", "nsg_flat.cuh")]
 HEADER = os.path.join(ROOT, "include", "nsg.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]

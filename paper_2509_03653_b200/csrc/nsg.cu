@@ -20,6 +20,7 @@
 #include "nsg.h"
 #include "nsg_common.cuh"
 #include "nsg_fast.cuh"
+#include "nsg_flat.cuh"
 #include "nsg_global.cuh"
 #include "nsg_trace.cuh"
 #include "nsg_anon.cuh"
@@ -38,6 +39,7 @@ constexpr size_t DIAG_OFFSET = 64;
 constexpr size_t PROF_OFFSET = 128;  // u64[16], NSG_FLAG_PROFILE
 constexpr size_t CTRL_BYTES = 4096;  // ticket, diag (64), prof u64[256] (128)
 constexpr u64 GLOBAL_BUDGET = 2ull << 30;  // cap on L2-path table memory
+constexpr u64 FLAT_BATCH = 64;             // windows per batch of the round-2 kernels (scratch ~2.5 MB per window)
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 static u64 next_pow2(u64 x) { u64 p = 1; while (p < x) p <<= 1; return p; }
@@ -50,6 +52,10 @@ struct Layout {
   u32 logB, B, logB2, B2, cp, cp_last, R;
   size_t o_pw, o_s0win, o_kscr, o_koff, o_rscr, o_roff, o_rend, o_lres, o_sres, o_s0list, o_wscr;
   size_t memset_bytes;
+  // round-2 per-window kernels (nsg_flat.cuh), overlaid on the fast-path scratch
+  bool flat;
+  u32 flogB, fB, flogBs, fBs, fCP, fNB;  // fNB: windows per batch
+  size_t o_fws, o_fkscr, o_fkoff, o_frscr, o_froff;
   // global
   u64 LC;
   u32 G;
@@ -93,6 +99,23 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     L.o_sres = o; o = align256(o + (size_t)L.R * 2 * L.B2 * 4 * sizeof(u32));
     L.o_s0list = o; o = align256(o + (size_t)L.R * L.B2 * TCAP_S * sizeof(u32));
     L.o_wscr = o; o = align256(o + (size_t)L.R * L.cp * CH * sizeof(u32));
+  }
+  L.flat = W <= flat::MAX_W;
+  if (L.flat) {  // overlaid on the fast path's scratch (one path or the other runs per call)
+    size_t q = L.memset_bytes;
+    const u64 want = (W + flat::BK - 1) / flat::BK;
+    L.fB = (u32)next_pow2(want < 1 ? 1 : want);
+    L.flogB = ilog2(L.fB);
+    L.fBs = L.fB;
+    L.flogBs = L.flogB;
+    L.fCP = (u32)((W + flat::CH - 1) / flat::CH);
+    L.fNB = (u32)(L.nw < (u64)FLAT_BATCH ? L.nw : (u64)FLAT_BATCH);
+    L.o_fws = q; q = align256(q + (size_t)L.nw * sizeof(flat::WinState));
+    L.o_fkscr = q; q = align256(q + (size_t)L.fNB * L.fCP * flat::CH * sizeof(u64));
+    L.o_fkoff = q; q = align256(q + (size_t)L.fNB * L.fCP * L.fB * sizeof(u32));
+    L.o_frscr = q; q = align256(q + (size_t)L.fNB * L.fB * flat::RCAP * sizeof(u64));
+    L.o_froff = q; q = align256(q + (size_t)L.fNB * L.fB * 2 * L.fBs * sizeof(u32));
+    if (q > o) o = q;
   }
   // L2-path table sets: the full path for large windows, the overflow hand-off otherwise.
   L.LC = next_pow2(2 * W);
@@ -146,6 +169,10 @@ static nsg_status dev_info(DevInfo& out) {
       if (per_sm < 1 || per_sm_w < 1) return NSG_ERR_UNSUPPORTED_DEVICE;
       d.fast_blocks = per_sm * d.sms;
       d.fast_blocks_w = per_sm_w * d.sms;
+      if (cudaFuncSetAttribute(flat::part_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(flat::SmemP)) != cudaSuccess ||
+          cudaFuncSetAttribute(flat::link_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(flat::SmemL)) != cudaSuccess ||
+          cudaFuncSetAttribute(flat::side_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(flat::SmemS)) != cudaSuccess)
+        return NSG_ERR_CUDA;
     }
     d.init = true;
   }
@@ -223,7 +250,15 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
   if (cudaMemsetAsync(base, 0, L.memset_bytes, s) != cudaSuccess) return NSG_ERR_CUDA;
   u32* arrived = reinterpret_cast<u32*>(base + L.o_pw) + 5 * L.nw;
   cudaEvent_t ev_copied = nullptr;
-  if (sin) {  // chunked H2D on the copy stream, after the workspace reset (which clears the flags)
+  const bool flat_path = L.flat && !(flags & (NSG_FLAG_FORCE_GLOBAL | NSG_FLAG_LEGACY_FAST)) && !vec && !wgt;
+  if (sin && flat_path) {  // the round-2 path copies per batch (below), after the work already on `s`
+    cudaEvent_t ev0 = nullptr;
+    if (cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming) != cudaSuccess) return NSG_ERR_CUDA;
+    const bool ok = cudaEventRecord(ev0, s) == cudaSuccess && cudaStreamWaitEvent(sin->cs, ev0, 0) == cudaSuccess;
+    cudaEventDestroy(ev0);
+    if (!ok) return NSG_ERR_CUDA;
+  }
+  if (sin && !flat_path) {  // chunked H2D on the copy stream, after the workspace reset (which clears the flags)
     WriteValue32Fn wv = write_value32();
     if (!wv) return NSG_ERR_CUDA;
     cudaEvent_t ev_reset = nullptr;
@@ -267,8 +302,54 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
   gg.wgt = wgt;
   gg.mirror = mirror; gg.n_mirror = n_mirror; gg.mirror_row0 = mirror_row0;
 
-  const bool use_fast = L.fast && !(flags & NSG_FLAG_FORCE_GLOBAL);
-  if (use_fast) {
+  gg.ovf_stride = 1;
+  const bool use_flat = flat_path;
+  const bool use_fast = !use_flat && L.fast && !(flags & NSG_FLAG_FORCE_GLOBAL);
+  if (use_flat) {
+    flat::FGeo g;
+    memset(&g, 0, sizeof(g));
+    g.n = n; g.W = W; g.nw = L.nw;
+    g.logB = L.flogB; g.B = L.fB; g.logBs = L.flogBs; g.Bs = L.fBs; g.CP = L.fCP;
+    g.ws = reinterpret_cast<flat::WinState*>(base + L.o_fws);
+    g.kscr = reinterpret_cast<u64*>(base + L.o_fkscr);
+    g.koff = reinterpret_cast<u32*>(base + L.o_fkoff);
+    g.rscr = reinterpret_cast<u64*>(base + L.o_frscr);
+    g.roff = reinterpret_cast<u32*>(base + L.o_froff);
+    g.diag = reinterpret_cast<u32*>(base + DIAG_OFFSET);
+    g.mirror = mirror; g.n_mirror = n_mirror; g.mirror_row0 = mirror_row0;
+    g.inject = (flags & NSG_FLAG_INJECT_OVERFLOW) ? 1u : 0u;
+    if (cudaMemsetAsync(base + L.o_fws, 0, (size_t)L.nw * sizeof(flat::WinState), s) != cudaSuccess) return NSG_ERR_CUDA;
+    if (ev_before && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_before), s) != cudaSuccess) return NSG_ERR_CUDA;
+    for (u64 w0 = 0; w0 < L.nw; w0 += L.fNB) {
+      g.w0 = w0;
+      g.nbw = (u32)(L.nw - w0 < (u64)L.fNB ? L.nw - w0 : (u64)L.fNB);
+      if (sin) {  // this batch's keys arrive on the copy stream
+        const u64 p0 = w0 * W, p1 = (w0 + g.nbw) * W < n ? (w0 + g.nbw) * W : n;
+        cudaEvent_t ev = nullptr;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return NSG_ERR_CUDA;
+        const bool ok = cudaMemcpyAsync(const_cast<u64*>(keys) + p0, sin->host + p0, (p1 - p0) * sizeof(u64),
+                                        cudaMemcpyHostToDevice, sin->cs) == cudaSuccess &&
+                        cudaEventRecord(ev, sin->cs) == cudaSuccess && cudaStreamWaitEvent(s, ev, 0) == cudaSuccess;
+        cudaEventDestroy(ev);
+        if (!ok) return NSG_ERR_CUDA;
+      }
+      flat::part_kernel<<<g.nbw * g.CP, flat::PTH, sizeof(flat::SmemP), s>>>(g, src, dst, keys);
+      flat::link_kernel<<<g.nbw * g.B, flat::LTH, sizeof(flat::SmemL), s>>>(g);
+      flat::side_kernel<<<g.nbw * 2 * g.Bs, flat::STH, sizeof(flat::SmemS), s>>>(g, out);
+      g_last_launches += 3;
+      if (cudaGetLastError() != cudaSuccess) return NSG_ERR_CUDA;
+    }
+    if (ev_after && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_after), s) != cudaSuccess) return NSG_ERR_CUDA;
+    if (ev_copied && cudaStreamWaitEvent(s, ev_copied, 0) != cudaSuccess) return NSG_ERR_CUDA;
+    if (!(flags & NSG_FLAG_NO_FALLBACK_CHECK)) {
+      gg.only_overflowed = 1;
+      gg.ovf = &g.ws[0].ovf;
+      gg.ovf_stride = sizeof(flat::WinState) / sizeof(u32);
+      global_kernel<<<L.G, GT, 0, s>>>(gg, src, dst, keys, out);
+      g_last_launches++;
+      if (cudaGetLastError() != cudaSuccess) return NSG_ERR_CUDA;
+    }
+  } else if (use_fast) {
     Geo g;
     g.n = n; g.W = W; g.nw = L.nw;
     g.logB = L.logB; g.B = L.B; g.logB2 = L.logB2; g.B2 = L.B2; g.cp = L.cp; g.cp_last = L.cp_last; g.R = L.R;
@@ -866,6 +947,7 @@ nsg_status nsg_window_vectors_weighted(const uint32_t* src, const uint32_t* dst,
 size_t nsg_diag_offset(void) { return nsg::DIAG_OFFSET; }
 
 unsigned nsg_last_launches(void) { return nsg::g_last_launches; }
+
 
 #ifdef NSG_EXP_TRACE
 // timing experiment only: copy the item trace of the last launches to `host` (u64[cap][4]) and reset

@@ -20,6 +20,7 @@ struct GGeo {
   u32* nP;      // [G][2][LC]
   u32* nF;      // [G][2][LC]
   const u32* ovf;
+  u32 ovf_stride;  // ovf of window w at ovf[w * ovf_stride]
   u32* diag;
   // optional vector outputs (as Geo): window w's entries at [w*W, w*W + count), hash order
   u64* v_lkey; u32* v_lpk;
@@ -82,7 +83,7 @@ global_kernel(GGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, 
   u64* lkey = g.lkey + (u64)blockIdx.x * LC;
   u32* lcnt = g.lcnt + (u64)blockIdx.x * LC;
   for (u64 w = blockIdx.x; w < g.nw; w += g.G) {
-    if (g.only_overflowed && ldcg32(&g.ovf[w]) == 0) continue;
+    if (g.only_overflowed && ldcg32(&g.ovf[w * g.ovf_stride]) == 0) continue;
     const u64 base = w * g.W;
     const u64 len = min(g.W, g.n - base);
     for (u64 i = t; i < LC; i += GT) {
