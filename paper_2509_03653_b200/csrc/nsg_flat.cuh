@@ -31,17 +31,15 @@ namespace flat {
 
 constexpr int CH = 4096;                      // keys per partition item
 constexpr int PTH = 256;                      // partition CTA threads
-constexpr int LTH = 512;                      // link CTA threads
-constexpr int STH = 512;                      // side CTA threads
-constexpr u64 BK = 2048;                      // target keys per link bucket / nodes per side bucket
-constexpr u64 MAX_W = 1ull << 18;             // windows this path takes (<= 128 link / side buckets)
+constexpr int LTH = 256;                      // link CTA threads
+constexpr int STH = 128;                      // side CTA threads
+constexpr u64 BK = 1024;                      // target keys per link bucket / nodes per side bucket
+constexpr u64 MAX_W = 1ull << 17;             // windows this path takes (<= 128 link / side buckets)
 constexpr int MAXB = 256;
-constexpr int LOG_TL = 12, TL = 1 << LOG_TL;  // link-table slots (load <= 5/8)
-constexpr int LOG_TS = 12, TS = 1 << LOG_TS;  // node-table slots
-constexpr u32 FILL_L = 2560, FILL_S = 2560;   // distinct entries before the window goes to the L2 path
-constexpr int LSK = 5124;                     // link stage (u64): keys per gather part, then the records
+constexpr int LOG_TL = 11, TL = 1 << LOG_TL;  // link-table slots (load <= 5/8)
+constexpr int LOG_TS = 11, TS = 1 << LOG_TS;  // node-table slots
+constexpr u32 FILL_L = 1280, FILL_S = 1280;   // distinct entries before the window goes to the L2 path
 constexpr u32 RCAP = 2 * (FILL_L + 1);        // records per link bucket (both sides)
-constexpr int SSK = 4096;                     // side stage (u64): records per gather part
 constexpr int PFS = 20;                       // node packets: 20-bit field (W < 2^20)
 constexpr u32 PMASK = (1u << PFS) - 1;
 constexpr u32 FMAX = 0xFFFu;                  // fan field: 12 bits; items with >= 4096 records track wraps
@@ -163,45 +161,63 @@ __device__ __forceinline__ void copy_out(u64* __restrict__ dstp, const u64* st, 
 
 // ---------------------------------------------------------------------------------------------
 // Warp-owned gathers: warp v of the CTA owns segments v, v + NW, ... of an item (its share of the
-// chunks / link buckets), enumerates their concatenation lane-parallel and loads the elements it
-// processes straight from L2 into registers.  The inserts then need no CTA barrier: a warp inserts
-// its own elements as soon as they arrive (slots only go from free to a key, so concurrent inserts
-// from other warps are safe), and one barrier ends the whole insert phase.
+// chunks / link buckets) and walks their concatenation 64 elements per step, loading each element
+// straight from L2 into a register.  The segment list lives in registers (lane k: the warp's k-th
+// non-empty segment), so locating an element's segment is a few bit operations, no search.  The
+// inserts need no CTA barrier: a slot only ever goes from free to a key, so concurrent inserts from
+// other warps are safe, and one barrier ends the whole insert phase.
 // ---------------------------------------------------------------------------------------------
-constexpr int WSEG = 16;  // segments per warp (>= segments / warps for W <= 2^18)
-
 struct WarpSegs {
   u32 n;      // elements of the warp's concatenation
-  u32 nseg;   // segments owned
+  u32 nseg;   // non-empty segments owned (<= 32)
+  u32 pre;    // lane k < nseg: first element of segment k in the concatenation
+  u32 d;      // lane k < nseg: element offset of segment k's storage minus pre
+  u32 kb;     // segments that start before the current step
 };
 
-// Load the warp's segment descriptors (desc(i) = start << 16 | count of segment i, i < nall) into
-// pre[] / st[] (this warp's SMEM slice): pre[k] = first element of its k-th segment.
-template <class D>
-__device__ __forceinline__ WarpSegs warp_segs(u32 nall, u32 nwarps, u32* pre, u32* st, D desc) {
+// desc(i) = start << 16 | count of segment i (i < nall), row(i) = element offset of segment i's row;
+// scr: 64 words of this warp's shared memory (the non-empty segments are compacted through it).
+template <class D, class R>
+__device__ __forceinline__ WarpSegs warp_segs(u32 nall, u32 nwarps, u32* scr, D desc, R row) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  WarpSegs r;
-  r.nseg = nall > (u32)wid ? (nall - 1 - wid) / nwarps + 1 : 0u;
+  const u32 nraw = nall > (u32)wid ? (nall - 1 - wid) / nwarps + 1 : 0u;  // <= 32 by construction
   const u32 i = wid + lane * nwarps;
-  const u32 v = (u32)lane < r.nseg ? desc(i) : 0u;
-  u32 x = v & 0xFFFFu;
+  const u32 v = (u32)lane < nraw ? desc(i) : 0u;
+  const u32 cnt = v & 0xFFFFu;
+  u32 x = cnt;
 #pragma unroll
   for (int k = 1; k < 32; k <<= 1) {
     const u32 y = __shfl_up_sync(0xffffffffu, x, k);
     if (lane >= k) x += y;
   }
-  if ((u32)lane < r.nseg) { pre[lane] = x - (v & 0xFFFFu); st[lane] = v >> 16; }
-  r.n = __shfl_sync(0xffffffffu, x, 31);
+  const u32 m = __ballot_sync(0xffffffffu, cnt != 0);
+  if (cnt) {
+    const u32 r = __popc(m & ((1u << lane) - 1u));
+    scr[r] = x - cnt;
+    scr[32 + r] = row(i) + (v >> 16) - (x - cnt);
+  }
   __syncwarp();
+  WarpSegs r;
+  r.nseg = __popc(m);
+  r.pre = scr[lane];
+  r.d = scr[32 + lane];
+  r.n = __shfl_sync(0xffffffffu, x, 31);
+  r.kb = 0;
   return r;
 }
 
-// element e (< n) of the warp's concatenation: its segment k and offset inside the segment
-__device__ __forceinline__ void warp_seg_find(const u32* pre, u32 nseg, u32 e, u32& k, u32& off) {
-  u32 j = 0;
-  for (u32 q = 1; q < nseg; ++q) j = (e >= pre[q]) ? q : j;
-  k = j;
-  off = e - pre[j];
+// Element offsets of elements e0 + lane and e0 + 32 + lane (callers check e < n); advances ws.kb.
+__device__ __forceinline__ void warp_seg_step(WarpSegs& ws, u32 e0, u32& oa, u32& ob) {
+  const int lane = threadIdx.x & 31;
+  const u32 rel = ((u32)lane < ws.nseg && ws.pre >= e0) ? ws.pre - e0 : 64u;
+  const u32 mlo = __reduce_or_sync(0xffffffffu, rel < 32 ? 1u << rel : 0u);
+  const u32 mhi = __reduce_or_sync(0xffffffffu, rel - 32 < 32 ? 1u << (rel - 32) : 0u);
+  const u32 le = (2u << lane) - 1u;  // bits 0..lane
+  const u32 ka = ws.kb + __popc(mlo & le) - 1;
+  const u32 kb = ws.kb + __popc(mlo) + __popc(mhi & le) - 1;
+  oa = __shfl_sync(0xffffffffu, ws.d, ka & 31) + e0 + lane;
+  ob = __shfl_sync(0xffffffffu, ws.d, kb & 31) + e0 + 32 + lane;
+  ws.kb += __popc(mlo) + __popc(mhi);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -285,102 +301,54 @@ part_kernel(const FGeo g, const u32* __restrict__ src, const u32* __restrict__ d
 // link(w, b)
 // ---------------------------------------------------------------------------------------------
 struct SmemL {
-  u64 stage[LSK];                  // 20 KB: the bucket's keys (part by part), then its records
-  u64 lkey[TL];                    // 16 KB
-  u32 lcnt[TL];                    // 8 KB
-  uint16_t claim[TL];              // 4 KB
+  u64 lkey[TL];
+  u32 lcnt[TL];
   u32 hist[2 * MAXB], offs[2 * MAXB];
-  u32 wpre[LTH / 32][WSEG], wst[LTH / 32][WSEG];  // per-warp segment prefixes / starts
+  uint16_t claim[FILL_L];          // the bucket's occupied slots
+  u32 segscr[LTH / 32][64];
   u32 red[4][LTH / 32];
   u32 ncl, esc, ovf, L0;
 };
 
-// One slot for `key`: 1 = counted (found), 2 = claimed and counted, 0 = holds another key.
-__device__ __forceinline__ u32 link_try(SmemL& s, u64 key, u32 sl, u64 cur) {
-  if (cur == key) { atomicAdd(&s.lcnt[sl], 1u); return 1; }
-  if (cur != EMPTY64) return 0;
-  const u64 old = atomicCAS(reinterpret_cast<unsigned long long*>(&s.lkey[sl]), (unsigned long long)EMPTY64,
-                            (unsigned long long)key);
-  if (old == EMPTY64) { atomicAdd(&s.lcnt[sl], 1u); return 2; }
-  if (old == key) { atomicAdd(&s.lcnt[sl], 1u); return 1; }
-  return 0;
+// Lockstep probe of two keys per lane: every lane advances its unfinished keys by one slot per
+// iteration (a found key, or a free slot claimed by CAS, finishes it), so the warp runs as many short
+// iterations as its longest probe sequence and never serialises divergent probe loops.
+// In: slot = home slot, cur = its content, act = key valid.  Out: slot = the key's slot.
+// Returns the number of slots claimed by this lane.
+template <class T, class Step>
+__device__ __forceinline__ u32 probe2(T* keys, u32 mask, T ka, T kb, u32& sa, u32& sb, T ca, T cb, bool aa, bool ab,
+                                      u32* ovf, Step step) {
+  constexpr T EMPTY = ~T(0);
+  u32 claimed = 0;
+  aa = aa && ca != ka;
+  ab = ab && cb != kb;
+  if (!__any_sync(0xffffffffu, aa || ab)) return 0;
+  const u32 pa = step(ka), pb = step(kb);
+  for (u32 it = 0;; ++it) {
+    if (aa && ca == EMPTY) {
+      const T o = atomicCAS(&keys[sa], EMPTY, ka);
+      claimed += o == EMPTY;
+      ca = o == EMPTY ? ka : o;
+    }
+    if (ab && cb == EMPTY) {
+      const T o = atomicCAS(&keys[sb], EMPTY, kb);
+      claimed += o == EMPTY;
+      cb = o == EMPTY ? kb : o;
+    }
+    aa = aa && ca != ka;
+    ab = ab && cb != kb;
+    if (!__any_sync(0xffffffffu, aa || ab)) break;
+    if (it >= mask) {  // table full (adversarial keys only)
+      if (aa || ab) *ovf = 1;
+      break;
+    }
+    if (aa) { sa = (sa + pa) & mask; ca = *reinterpret_cast<volatile T*>(&keys[sa]); }
+    if (ab) { sb = (sb + pb) & mask; cb = *reinterpret_cast<volatile T*>(&keys[sb]); }
+  }
+  return claimed;
 }
 
-constexpr int KR = 4;  // keys / records per thread per insert round
-// Insert up to KR keys per lane (bit i of vm: k[i] valid), all of the lane's loads / atomics in flight
-// together; colliding keys probe on by double hashing, all together per step.  Claimed slots are
-// appended to the claim list with one reservation per warp (ballot ranks).
-__device__ __forceinline__ void link_insert_regs(SmemL& s, const u64 (&k)[KR], u32 vm, u32 logB) {
-  const int lane = threadIdx.x & 31;
-  u64 cur[KR];
-  u32 sl[KR];
-  u32 vmask = 0, nesc = 0;
-#pragma unroll
-  for (int i = 0; i < KR; ++i) {
-    if ((vm >> i & 1u) && k[i] == EMPTY64) ++nesc;
-    else if (vm >> i & 1u) vmask |= 1u << i;
-    sl[i] = link_slot(k[i], logB);
-  }
-  if (*reinterpret_cast<volatile u32*>(&s.ovf)) vmask = 0;
-#pragma unroll
-  for (int i = 0; i < KR; ++i) cur[i] = (vmask >> i & 1u) ? *reinterpret_cast<volatile u64*>(&s.lkey[sl[i]]) : 0ull;
-  u32 pmask = 0, wmask = 0;
-#pragma unroll
-  for (int i = 0; i < KR; ++i) {
-    if (vmask >> i & 1u) {
-      const u32 r = link_try(s, k[i], sl[i], cur[i]);
-      if (r == 0) pmask |= 1u << i;
-      if (r == 2) wmask |= 1u << i;
-    }
-  }
-  if (nesc) atomicAdd(&s.esc, nesc);
-  if (__any_sync(0xffffffffu, pmask != 0)) {
-    u32 stp[KR];
-#pragma unroll
-    for (int i = 0; i < KR; ++i) stp[i] = link_step(k[i]);
-    for (u32 step = 1; __any_sync(0xffffffffu, pmask != 0); ++step) {
-      if (step >= (u32)TL) {  // table full (adversarial keys only)
-        if (pmask) s.ovf = 1;
-        break;
-      }
-#pragma unroll
-      for (int i = 0; i < KR; ++i)
-        if (pmask >> i & 1u) cur[i] = *reinterpret_cast<volatile u64*>(&s.lkey[(sl[i] + stp[i]) & (TL - 1)]);
-#pragma unroll
-      for (int i = 0; i < KR; ++i) {
-        if (pmask >> i & 1u) {
-          sl[i] = (sl[i] + stp[i]) & (TL - 1);
-          const u32 r = link_try(s, k[i], sl[i], cur[i]);
-          if (r) pmask &= ~(1u << i);
-          if (r == 2) wmask |= 1u << i;
-        }
-      }
-    }
-  }
-  // claim-list reservation: ballot ranks, one atomic per warp
-  u32 m[KR], tot = 0;
-#pragma unroll
-  for (int i = 0; i < KR; ++i) { m[i] = __ballot_sync(0xffffffffu, wmask >> i & 1u); tot += __popc(m[i]); }
-  if (tot) {
-    u32 base = 0;
-    if (lane == 0) {
-      base = atomicAdd(&s.ncl, tot);
-      if (base + tot > FILL_L) s.ovf = 1;  // more distinct links than the fast path takes
-    }
-    base = __shfl_sync(0xffffffffu, base, 0);
-    const u32 lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int i = 0; i < KR; ++i) {
-      if (wmask >> i & 1u) {
-        const u32 pos = base + __popc(m[i] & lt);
-        if (pos < (u32)TL) s.claim[pos] = (uint16_t)sl[i];
-      }
-      base += __popc(m[i]);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(LTH, 2)
+__global__ void __launch_bounds__(LTH, 7)
 link_kernel(const FGeo g) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemL& s = *reinterpret_cast<SmemL*>(smem_raw);
@@ -388,75 +356,84 @@ link_kernel(const FGeo g) {
   constexpr u32 NW = LTH / 32;
   const u32 wb = blockIdx.x / g.B, b = blockIdx.x % g.B;
   const u64 w = g.w0 + wb;
-  const u32 CP = g.CP, B = g.B, Bs = g.Bs, logBs = g.logBs;
-  for (u32 i = t; i < (u32)TL / 2; i += LTH) {  // table init (conflict-free wide stores)
-    reinterpret_cast<ulonglong2*>(s.lkey)[i] = make_ulonglong2(EMPTY64, EMPTY64);
-    reinterpret_cast<uint2*>(s.lcnt)[i] = make_uint2(0u, 0u);
-  }
-  if (t == 0) { s.ncl = 0; s.esc = 0; s.ovf = 0; }
+  const u32 CP = g.CP, B = g.B, Bs = g.Bs, logBs = g.logBs, logB = g.logB;
+  for (u32 i = t; i < (u32)TL / 2; i += LTH) reinterpret_cast<ulonglong2*>(s.lkey)[i] = make_ulonglong2(EMPTY64, EMPTY64);
+  for (u32 i = t; i < (u32)TL / 4; i += LTH) reinterpret_cast<uint4*>(s.lcnt)[i] = make_uint4(0u, 0u, 0u, 0u);
   for (u32 i = t; i < 2 * Bs; i += LTH) s.hist[i] = 0;
+  if (t == 0) { s.ncl = 0; s.esc = 0; s.ovf = 0; }
   // this warp's share of the bucket: its segment of chunks wid, wid + NW, ...
-  u32* pre = s.wpre[wid];
-  u32* sst = s.wst[wid];
   const u32* ko = g.koff + (u64)wb * CP * B + b;
-  const WarpSegs ws = warp_segs(CP, NW, pre, sst, [&](u32 c) { return ldcg32(ko + (u64)c * B); });
+  WarpSegs ws = warp_segs(CP, NW, s.segscr[wid], [&](u32 c) { return ldcg32(ko + (u64)c * B); }, [&](u32 c) { return c * (u32)CH; });
   const u64* kb = g.kscr + (u64)wb * CP * CH;
   __syncthreads();  // table initialised
-  for (u32 r0 = 0; r0 < ws.n; r0 += 32 * KR) {
-    u64 k[KR];
-    u32 vm = 0;
+  {
+    u32 nesc = 0;
+    for (u32 e0 = 0; e0 < ws.n; e0 += 64) {
+      u32 oa, ob;
+      warp_seg_step(ws, e0, oa, ob);
+      const bool va = e0 + lane < ws.n, vb = e0 + 32 + lane < ws.n;
+      const u64 ka = va ? __ldcg(reinterpret_cast<const unsigned long long*>(kb + oa)) : EMPTY64;
+      const u64 kc = vb ? __ldcg(reinterpret_cast<const unsigned long long*>(kb + ob)) : EMPTY64;
+      if (*reinterpret_cast<volatile u32*>(&s.ovf)) break;
+      const bool aa = ka != EMPTY64, ab = kc != EMPTY64;  // the key ~0 is counted apart
+      nesc += (va && !aa) + (vb && !ab);
+      u32 sa = link_slot(ka, logB), sb = link_slot(kc, logB);
+      const u64 ca = *reinterpret_cast<volatile u64*>(&s.lkey[sa]);
+      const u64 cb = *reinterpret_cast<volatile u64*>(&s.lkey[sb]);
+      probe2<unsigned long long>(reinterpret_cast<unsigned long long*>(s.lkey), TL - 1, ka, kc, sa, sb, ca, cb, aa, ab,
+                                 &s.ovf, [](u64 k) { return link_step(k); });
+      if (aa) atomicAdd(&s.lcnt[sa], 1u);
+      if (ab) atomicAdd(&s.lcnt[sb], 1u);
+    }
+    nesc = __reduce_add_sync(0xffffffffu, nesc);
+    if (lane == 0 && nesc) atomicAdd(&s.esc, nesc);
+  }
+  __syncthreads();  // every key of the bucket is counted
+  // ---- final: the occupied slots compacted into the claim list, then visited densely
+  constexpr int SPT = TL / LTH;  // slots per thread: [t * SPT, t * SPT + SPT)
+  static_assert(SPT % 4 == 0 && SPT <= 32, "slots are scanned 4 at a time");
+  {
+    u32 occ = 0;
 #pragma unroll
-    for (int i = 0; i < KR; ++i) {
-      const u32 e = r0 + i * 32 + lane;
-      k[i] = 0;
-      if (e < ws.n) {
-        u32 kk, off;
-        warp_seg_find(pre, ws.nseg, e, kk, off);
-        k[i] = __ldcg(reinterpret_cast<const unsigned long long*>(kb + (u64)(wid + kk * NW) * CH + sst[kk] + off));
-        vm |= 1u << i;
+    for (int j = 0; j < SPT; j += 4) {
+      const uint4 c4 = *reinterpret_cast<const uint4*>(&s.lcnt[t * SPT + j]);
+      occ |= (c4.x ? 1u : 0u) << j | (c4.y ? 2u : 0u) << j | (c4.z ? 4u : 0u) << j | (c4.w ? 8u : 0u) << j;
+    }
+    const u32 c = __popc(occ);
+    u32 x = c;
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, x, k);
+      if (lane >= k) x += y;
+    }
+    u32 base = 0;
+    if (lane == 31 && x) base = atomicAdd(&s.ncl, x);
+    u32 p = __shfl_sync(0xffffffffu, base, 31) + x - c;
+#pragma unroll
+    for (int j = 0; j < SPT; ++j)
+      if (occ >> j & 1u) {
+        if (p < FILL_L) s.claim[p] = (uint16_t)(t * SPT + j);
+        ++p;
       }
-    }
-    link_insert_regs(s, k, vm, g.logB);
   }
-  __syncthreads();  // every key of the bucket is in the table
-  // ---- final: the bucket's links (claim list), window statistics, records by side bucket
-  const bool ovf = s.ovf != 0;
-  const u32 ncl = min(s.ncl, (u32)TL);
-  constexpr int SPT = TL / LTH;
-  const int kmax = (int)((ncl + LTH - 1) / LTH);  // rounds with claims (warp-uniform bound)
-  u64 lk[SPT];
-  u32 lc[SPT], lb[SPT], r0[SPT], r1[SPT];
+  __syncthreads();
+  const bool ovf = s.ovf != 0 || s.ncl > FILL_L;  // more links than the records take: L2 path
+  const u32 ncl = ovf ? 0u : s.ncl;
   u32 nl = 0, mx = 0, sm = 0;
-#pragma unroll
-  for (int k = 0; k < SPT; ++k) { lc[k] = 0; lk[k] = 0; lb[k] = 0; r0[k] = 0; r1[k] = 0; }
-#pragma unroll
-  for (int k = 0; k < SPT; ++k) {
-    if (k >= kmax) break;
-    const u32 e = k * LTH + t;
-    const u32 sl = e < ncl ? s.claim[e] : 0u;
-    lc[k] = e < ncl ? s.lcnt[sl] : 0u;
-    lk[k] = e < ncl ? s.lkey[sl] : 0ull;
-  }
-#pragma unroll
-  for (int k = 0; k < SPT; ++k) {
-    if (k >= kmax) break;
-    if (lc[k]) { nl += 1; mx = max(mx, lc[k]); sm += lc[k]; }
-    lb[k] = node_bucket((u32)(lk[k] >> 32), logBs) | (node_bucket((u32)lk[k], logBs) << 16);
-  }
-#pragma unroll
-  for (int k = 0; k < SPT; ++k) {
-    if (k >= kmax) break;
-    if (lc[k] && !ovf) {
-      r0[k] = atomicAdd(&s.hist[lb[k] & 0xFFFFu], 1u);
-      r1[k] = atomicAdd(&s.hist[Bs + (lb[k] >> 16)], 1u);
-    }
+  for (u32 e = t; e < ncl; e += LTH) {
+    const u32 sl = s.claim[e];
+    const u32 c = s.lcnt[sl];
+    const u64 key = s.lkey[sl];
+    nl += 1; mx = max(mx, c); sm += c;
+    atomicAdd(&s.hist[node_bucket((u32)(key >> 32), logBs)], 1u);
+    atomicAdd(&s.hist[Bs + node_bucket((u32)key, logBs)], 1u);
   }
   const u32 esc = s.esc;
-  u32 er0 = 0, er1 = 0;
   const u32 eb = node_bucket(EMPTY32, logBs);
-  if (t == 0 && esc) {  // the key ~0 (kept out of the table) is one more link
+  if (t == 0 && esc && !ovf) {  // the key ~0 (kept out of the table) is one more link
     nl += 1; mx = max(mx, esc); sm += esc;
-    if (!ovf) { er0 = atomicAdd(&s.hist[eb], 1u); er1 = atomicAdd(&s.hist[Bs + eb], 1u); }
+    atomicAdd(&s.hist[eb], 1u);
+    atomicAdd(&s.hist[Bs + eb], 1u);
   }
   {
     u32 z = 0;
@@ -471,8 +448,8 @@ link_kernel(const FGeo g) {
     return;
   }
   if (wid == 0) {
-    u32 a = lane < LTH / 32 ? s.red[0][lane] : 0u, m2 = lane < LTH / 32 ? s.red[1][lane] : 0u, z = 0,
-        d = lane < LTH / 32 ? s.red[3][lane] : 0u;
+    u32 a = lane < (int)NW ? s.red[0][lane] : 0u, m2 = lane < (int)NW ? s.red[1][lane] : 0u, z = 0,
+        d = lane < (int)NW ? s.red[3][lane] : 0u;
     warp_reduce4(a, m2, z, d);
     if (lane == 0 && a) {
       WinState* st = &g.ws[w];
@@ -487,48 +464,28 @@ link_kernel(const FGeo g) {
       for (u32 i = lane; i < Bs; i += 32) L0 += s.hist[i];
     L0 = warp_sum(L0);
     u32* r = ro + wid * Bs;
-    const u32 tot = warp_exscan(s.hist + wid * Bs, s.offs + wid * Bs, Bs, lane,
-                                [&](u32 i, u32 ex, u32 v) { r[i] = ((L0 + ex) << 16) | v; });
+    const u32 tot = warp_exscan(s.hist + wid * Bs, s.offs + wid * Bs, Bs, lane, [&](u32 i, u32 ex, u32 v) {
+      r[i] = ((L0 + ex) << 16) | v;
+      s.offs[wid * Bs + i] = L0 + ex;
+    });
     if (wid == 0 && lane == 0) s.L0 = tot;
   }
   __syncthreads();
-  const u32 L0 = s.L0;
-  u64* rdst = g.rscr + ((u64)wb * B + b) * RCAP;
-  const bool one = 2 * L0 <= (u32)LSK;
-  u32 p0[SPT], p1[SPT];
-#pragma unroll
-  for (int k = 0; k < SPT; ++k) {
-    p0[k] = 0; p1[k] = 0;
-    if (k >= kmax) break;
-    p0[k] = lc[k] ? s.offs[lb[k] & 0xFFFFu] : 0u;
-    p1[k] = lc[k] ? s.offs[Bs + (lb[k] >> 16)] : 0u;
-  }
-#pragma unroll
-  for (int k = 0; k < SPT; ++k) {
-    if (k >= kmax) break;
-    if (lc[k]) {
-      s.stage[p0[k] + r0[k]] = (lk[k] & 0xFFFFFFFF00000000ull) | lc[k];
-      if (one) s.stage[L0 + p1[k] + r1[k]] = (lk[k] << 32) | lc[k];
-    }
+  // records (node << 32 | count) straight to the item's record row, placed by side bucket with a
+  // cursor per bucket (side 0 first, then side 1 from L0)
+  u64* rrow = g.rscr + ((u64)wb * B + b) * RCAP;
+  for (u32 e = t; e < ncl; e += LTH) {
+    const u32 sl = s.claim[e];
+    const u32 c = s.lcnt[sl];
+    const u64 key = s.lkey[sl];
+    const u32 p0 = atomicAdd(&s.offs[node_bucket((u32)(key >> 32), logBs)], 1u);
+    const u32 p1 = atomicAdd(&s.offs[Bs + node_bucket((u32)key, logBs)], 1u);
+    __stcg(reinterpret_cast<unsigned long long*>(rrow + p0), (key & 0xFFFFFFFF00000000ull) | c);
+    __stcg(reinterpret_cast<unsigned long long*>(rrow + p1), (key << 32) | c);
   }
   if (t == 0 && esc) {
-    s.stage[s.offs[eb] + er0] = ((u64)EMPTY32 << 32) | esc;
-    if (one) s.stage[L0 + s.offs[Bs + eb] + er1] = ((u64)EMPTY32 << 32) | esc;
-  }
-  __syncthreads();
-  if (one) {
-    copy_out<LTH>(rdst, s.stage, 2 * L0);
-  } else {
-    copy_out<LTH>(rdst, s.stage, L0);
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      if (k >= kmax) break;
-      if (lc[k]) s.stage[p1[k] + r1[k]] = (lk[k] << 32) | lc[k];
-    }
-    if (t == 0 && esc) s.stage[s.offs[Bs + eb] + er1] = ((u64)EMPTY32 << 32) | esc;
-    __syncthreads();
-    copy_out<LTH>(rdst + L0, s.stage, L0);
+    rrow[atomicAdd(&s.offs[eb], 1u)] = ((u64)EMPTY32 << 32) | esc;
+    rrow[atomicAdd(&s.offs[Bs + eb], 1u)] = ((u64)EMPTY32 << 32) | esc;
   }
 }
 
@@ -536,26 +493,17 @@ link_kernel(const FGeo g) {
 // side(w, s, q)
 // ---------------------------------------------------------------------------------------------
 struct SmemS {
-  u32 nkey[TS];                    // 8 KB
-  u32 npf[TS];                     // 8 KB   packets | fan << 20
-  uint16_t claim[TS];              // 4 KB
-  u32 wpre[STH / 32][WSEG], wst[STH / 32][WSEG];
+  u32 nkey[TS];
+  u32 npf[TS];                     // packets | fan << 20
   u32 wrap[WRAPCAP];
+  u32 segscr[STH / 32][64];
   u32 red[3][STH / 32];
-  u32 ncl, escP, escF, ovf, nwrap, last;
+  u32 escP, escF, ovf, nwrap, last;
 };
 
-// One slot for `node`: 1 = its slot, 2 = claimed now, 0 = holds another node.
-__device__ __forceinline__ u32 node_try(SmemS& s, u32 node, u32 sl, u32 cur) {
-  if (cur == node) return 1;
-  if (cur != EMPTY32) return 0;
-  const u32 old = atomicCAS(&s.nkey[sl], EMPTY32, node);
-  if (old == EMPTY32) return 2;
-  return old == node ? 1u : 0u;
-}
-
-// packets += c, fan += 1.  An item with fewer than 4096 records cannot carry a fan past the 12-bit
-// field: a fire-and-forget add.  Otherwise a fan field that passes 4095 is noted in the wrap list.
+// packets += c, fan += 1 for the node in slot `slot`.  An item with fewer than 4096 records cannot
+// carry a fan past the 12-bit field: a fire-and-forget add.  Otherwise a fan field that passes 4095 is
+// noted in the wrap list.
 __device__ __forceinline__ void node_add(SmemS& s, u32 slot, u32 c, bool wrapcheck) {
   if (!wrapcheck) { atomicAdd(&s.npf[slot], c | (1u << PFS)); return; }
   const u32 o = atomicAdd(&s.npf[slot], c | (1u << PFS));
@@ -563,78 +511,6 @@ __device__ __forceinline__ void node_add(SmemS& s, u32 slot, u32 c, bool wrapche
     const u32 i = atomicAdd(&s.nwrap, 1u);
     if (i < (u32)WRAPCAP) s.wrap[i] = slot;
     else s.ovf = 1;
-  }
-}
-
-__device__ __forceinline__ void node_insert_regs(SmemS& s, const u32 (&nd)[KR], const u32 (&cc)[KR], u32 vm, u32 logBs,
-                                                 bool wrapcheck) {
-  const int lane = threadIdx.x & 31;
-  u32 sl[KR], cur[KR];
-  u32 vmask = 0, escP = 0, escF = 0;
-#pragma unroll
-  for (int i = 0; i < KR; ++i) {
-    if ((vm >> i & 1u) && nd[i] == EMPTY32) { escP += cc[i]; ++escF; }
-    else if (vm >> i & 1u) vmask |= 1u << i;
-    sl[i] = node_slot(nd[i], logBs);
-  }
-  if (*reinterpret_cast<volatile u32*>(&s.ovf)) vmask = 0;
-#pragma unroll
-  for (int i = 0; i < KR; ++i) cur[i] = (vmask >> i & 1u) ? *reinterpret_cast<volatile u32*>(&s.nkey[sl[i]]) : 0u;
-  u32 pmask = 0, wmask = 0;
-#pragma unroll
-  for (int i = 0; i < KR; ++i) {
-    if (vmask >> i & 1u) {
-      const u32 r = node_try(s, nd[i], sl[i], cur[i]);
-      if (r == 0) pmask |= 1u << i;
-      if (r == 2) wmask |= 1u << i;
-    }
-  }
-  if (escF) { atomicAdd(&s.escP, escP); atomicAdd(&s.escF, escF); }
-  if (__any_sync(0xffffffffu, pmask != 0)) {
-    u32 stp[KR];
-#pragma unroll
-    for (int i = 0; i < KR; ++i) stp[i] = node_step(nd[i]);
-    for (u32 step = 1; __any_sync(0xffffffffu, pmask != 0); ++step) {
-      if (step >= (u32)TS) {
-        if (pmask) { s.ovf = 1; vmask &= ~pmask; }
-        break;
-      }
-#pragma unroll
-      for (int i = 0; i < KR; ++i)
-        if (pmask >> i & 1u) cur[i] = *reinterpret_cast<volatile u32*>(&s.nkey[(sl[i] + stp[i]) & (TS - 1)]);
-#pragma unroll
-      for (int i = 0; i < KR; ++i) {
-        if (pmask >> i & 1u) {
-          sl[i] = (sl[i] + stp[i]) & (TS - 1);
-          const u32 r = node_try(s, nd[i], sl[i], cur[i]);
-          if (r) pmask &= ~(1u << i);
-          if (r == 2) wmask |= 1u << i;
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < KR; ++i)
-    if (vmask >> i & 1u) node_add(s, sl[i], cc[i], wrapcheck);
-  u32 m[KR], tot = 0;
-#pragma unroll
-  for (int i = 0; i < KR; ++i) { m[i] = __ballot_sync(0xffffffffu, wmask >> i & 1u); tot += __popc(m[i]); }
-  if (tot) {
-    u32 base = 0;
-    if (lane == 0) {
-      base = atomicAdd(&s.ncl, tot);
-      if (base + tot > FILL_S) s.ovf = 1;
-    }
-    base = __shfl_sync(0xffffffffu, base, 0);
-    const u32 lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int i = 0; i < KR; ++i) {
-      if (wmask >> i & 1u) {
-        const u32 pos = base + __popc(m[i] & lt);
-        if (pos < (u32)TS) s.claim[pos] = (uint16_t)sl[i];
-      }
-      base += __popc(m[i]);
-    }
   }
 }
 
@@ -662,11 +538,12 @@ __device__ void finalize(const FGeo& g, u64 w, u64* out) {
   for (u32 m = 0; m < g.n_mirror; ++m) store_row(g.mirror[m] + (g.mirror_row0 + w) * NSG_NUM_STATS, row);
 }
 
-__global__ void __launch_bounds__(STH, 3)
+__global__ void __launch_bounds__(STH, 12)
 side_kernel(const FGeo g, u64* __restrict__ out) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemS& s = *reinterpret_cast<SmemS*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  constexpr u32 NW = STH / 32;
   const u32 Bs = g.Bs, B = g.B, logBs = g.logBs;
   const u32 wb = blockIdx.x / (2 * Bs), q = blockIdx.x % (2 * Bs);
   const u64 w = g.w0 + wb;
@@ -674,12 +551,9 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
     reinterpret_cast<uint4*>(s.nkey)[i] = make_uint4(EMPTY32, EMPTY32, EMPTY32, EMPTY32);
     reinterpret_cast<uint4*>(s.npf)[i] = make_uint4(0u, 0u, 0u, 0u);
   }
-  if (t == 0) { s.ncl = 0; s.escP = 0; s.escF = 0; s.ovf = 0; s.nwrap = 0; }
-  constexpr u32 NW = STH / 32;
-  u32* pre = s.wpre[wid];
-  u32* sst = s.wst[wid];
+  if (t == 0) { s.escP = 0; s.escF = 0; s.ovf = 0; s.nwrap = 0; }
   const u32* ro = g.roff + (u64)wb * B * 2 * Bs + q;
-  const WarpSegs ws = warp_segs(B, NW, pre, sst, [&](u32 b) { return ldcg32(ro + (u64)b * 2 * Bs); });
+  WarpSegs ws = warp_segs(B, NW, s.segscr[wid], [&](u32 b) { return ldcg32(ro + (u64)b * 2 * Bs); }, [&](u32 b) { return b * RCAP; });
   if (lane == 0) s.red[0][wid] = ws.n;
   __syncthreads();  // table initialised, per-warp counts visible
   u32 ntot = 0;
@@ -687,26 +561,32 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
   for (u32 i = 0; i < NW; ++i) ntot += s.red[0][i];
   const bool wrapcheck = ntot > FMAX;
   const u64* rb = g.rscr + (u64)wb * B * RCAP;
-  for (u32 r0 = 0; r0 < ws.n; r0 += 32 * KR) {
-    u32 nd[KR], cc[KR];
-    u32 vm = 0;
-#pragma unroll
-    for (int i = 0; i < KR; ++i) {
-      const u32 e = r0 + i * 32 + lane;
-      u64 rec = 0;
-      if (e < ws.n) {
-        u32 kk, off;
-        warp_seg_find(pre, ws.nseg, e, kk, off);
-        rec = __ldcg(reinterpret_cast<const unsigned long long*>(rb + (u64)(wid + kk * NW) * RCAP + sst[kk] + off));
-        vm |= 1u << i;
-      }
-      nd[i] = (u32)(rec >> 32);
-      cc[i] = (u32)rec;
+  {
+    u32 escP = 0, escF = 0;
+    for (u32 e0 = 0; e0 < ws.n; e0 += 64) {
+      u32 oa, ob;
+      warp_seg_step(ws, e0, oa, ob);
+      const bool va = e0 + lane < ws.n, vb = e0 + 32 + lane < ws.n;
+      const u64 ra = va ? __ldcg(reinterpret_cast<const unsigned long long*>(rb + oa)) : ~0ull;
+      const u64 rc = vb ? __ldcg(reinterpret_cast<const unsigned long long*>(rb + ob)) : ~0ull;
+      if (*reinterpret_cast<volatile u32*>(&s.ovf)) break;
+      const u32 na = (u32)(ra >> 32), nb = (u32)(rc >> 32);
+      u32 sa = node_slot(na, logBs), sb = node_slot(nb, logBs);
+      const u32 ca = *reinterpret_cast<volatile u32*>(&s.nkey[sa]);
+      const u32 cb = *reinterpret_cast<volatile u32*>(&s.nkey[sb]);
+      const bool aa = na != EMPTY32, ab = nb != EMPTY32;  // the node ~0 is merged apart
+      if (va && !aa) { escP += (u32)ra; ++escF; }
+      if (vb && !ab) { escP += (u32)rc; ++escF; }
+      probe2<u32>(s.nkey, TS - 1, na, nb, sa, sb, ca, cb, aa, ab, &s.ovf, [](u32 k) { return node_step(k); });
+      if (aa) node_add(s, sa, (u32)ra, wrapcheck);
+      if (ab) node_add(s, sb, (u32)rc, wrapcheck);
     }
-    node_insert_regs(s, nd, cc, vm, logBs, wrapcheck);
+    escF = __reduce_add_sync(0xffffffffu, escF);
+    escP = __reduce_add_sync(0xffffffffu, escP);
+    if (lane == 0 && escF) { atomicAdd(&s.escP, escP); atomicAdd(&s.escF, escF); }
   }
   __syncthreads();
-  // ---- final: the side bucket's nodes (claim list)
+  // ---- final: the side bucket's nodes
   u32 wrapmax = 0;
   const u32 nwrap = min(s.nwrap, (u32)WRAPCAP);
   for (u32 i = lane; i < nwrap; i += 32) {  // exact fan of the nodes whose 12-bit field wrapped
@@ -716,16 +596,16 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
     wrapmax = max(wrapmax, (s.npf[sl] >> PFS) + (FMAX + 1) * cnt);
   }
   const bool ovf = s.ovf != 0;
-  const u32 ncl = min(s.ncl, (u32)TS);
   constexpr int SPT = TS / STH;
-  const int kmax = (int)((ncl + STH - 1) / STH);
+  static_assert(SPT % 4 == 0, "slots are scanned 4 at a time");
   u32 nn = 0, mp = 0, mf = wrapmax;
 #pragma unroll
-  for (int k = 0; k < SPT; ++k) {
-    if (k >= kmax) break;
-    const u32 e = k * STH + t;
-    const u32 pf = e < ncl ? s.npf[s.claim[e]] : 0u;
-    if (pf) { nn += 1; mp = max(mp, pf & PMASK); mf = max(mf, pf >> PFS); }
+  for (int j = 0; j < SPT; j += 4) {
+    const uint4 p4 = *reinterpret_cast<const uint4*>(&s.npf[t * SPT + j]);
+    const u32 ps[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (ps[i]) { nn += 1; mp = max(mp, ps[i] & PMASK); mf = max(mf, ps[i] >> PFS); }
   }
   if (t == 0 && s.escF) { nn += 1; mp = max(mp, s.escP); mf = max(mf, s.escF); }
   u32 z = 0;
@@ -733,9 +613,9 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
   if (lane == 0) { s.red[0][wid] = nn; s.red[1][wid] = mp; s.red[2][wid] = mf; }
   __syncthreads();
   if (wid == 0) {
-    nn = lane < STH / 32 ? s.red[0][lane] : 0u;
-    mp = lane < STH / 32 ? s.red[1][lane] : 0u;
-    mf = lane < STH / 32 ? s.red[2][lane] : 0u;
+    nn = lane < (int)NW ? s.red[0][lane] : 0u;
+    mp = lane < (int)NW ? s.red[1][lane] : 0u;
+    mf = lane < (int)NW ? s.red[2][lane] : 0u;
     warp_reduce4(nn, mp, mf, z);
     if (lane == 0) {
       WinState* st = &g.ws[w];
