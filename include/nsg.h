@@ -39,7 +39,10 @@
  *     workspace); wider vector loads are used internally when the data happens to be 16 B aligned.
  *   - Output: out is device memory, row-major [nsg_num_windows(n, window)][NSG_NUM_STATS] u64.
  *   - Errors: argument errors and launch errors are returned synchronously; nothing is launched on an
- *     argument error.  There is no CPU fallback: a device that is not sm_100 returns
+ *     argument error.  Device-detected inconsistencies (the per-window self-check: the link counts of a
+ *     window must sum to its length) are counted in the workspace diagnostics
+ *     (nsg_diag_offset); a debug build of the library (-DNSG_DEBUG_CHECKS, libnsg_debug.so) synchronises
+ *     `stream` after the nsg_window_stats* calls, reads them back and returns NSG_ERR_INTERNAL if any.  There is no CPU fallback: a device that is not sm_100 returns
  *     NSG_ERR_UNSUPPORTED_DEVICE.
  *   - Thread safety: calls are independent; two concurrent calls must not share a workspace.
  */
@@ -80,18 +83,12 @@ typedef enum {
 /* Largest supported window (per-window counts are kept in 32 bits on the device). */
 #define NSG_MAX_WINDOW (1ull << 31)
 
-/* Flags for nsg_window_stats_ex (testing / fault injection; 0 = normal operation). */
+/* Flags for nsg_window_stats_ex (fault injection for tests; 0 = normal operation).  Measurement and
+ * development switches live in nsg_internal.h (not part of the product interface). */
 enum {
   NSG_FLAG_FORCE_GLOBAL = 1u << 0,     /* run every window on the L2 (global-table) path */
-  NSG_FLAG_INJECT_OVERFLOW = 1u << 1,  /* mark every odd window as overflowed on the fast path, so the
-                                          overflow hand-off to the L2 path is exercised */
-  NSG_FLAG_NO_FALLBACK_CHECK = 1u << 2, /* internal/benchmark: skip the fallback launch; results of an
-                                          overflowed window are then undefined (never use for results) */
-  NSG_FLAG_PROFILE = 1u << 3           /* accumulate per-work-item-type SM cycles into the workspace:
-                                          u64[112] at nsg_diag_offset()+64: [0..12) per type (partition, link,
-                                          side) {items, cycles, wait cycles, max work}; [16+16*type+phase] cycles per phase, [64+...] max */,
-  NSG_FLAG_LEGACY_FAST = 1u << 4       /* run the round-1 persistent kernel (nsg_fast.cuh) instead of the
-                                          round-2 kernel (nsg_win.cuh) for windows < 2^20 (A/B measurement) */
+  NSG_FLAG_INJECT_OVERFLOW = 1u << 1   /* mark every odd window as overflowed on the shared-memory path, so
+                                          the overflow hand-off to the L2 path is exercised */
 };
 
 /* Number of windows: ceil(n_packets / window); 0 if n_packets == 0 or window == 0. */
@@ -113,14 +110,6 @@ nsg_status nsg_window_stats_packed(const uint64_t* keys, uint64_t n_packets, uin
 nsg_status nsg_window_stats_ex(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
                                uint64_t window, uint64_t* out, void* workspace, size_t workspace_bytes,
                                void* stream, uint32_t flags);
-
-/* nsg_window_stats_ex plus measurement hooks: ev_before / ev_after (cudaEvent_t as void*, may be NULL)
- * are recorded on `stream` immediately before and after the main kernel (the persistent fast-path
- * kernel, or the L2-path kernel), excluding the workspace reset and the overflow-check launch, so a
- * caller can time the dominant kernel with CUDA events without changing the work. */
-nsg_status nsg_window_stats_timed(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
-                                  uint64_t window, uint64_t* out, void* workspace, size_t workspace_bytes,
-                                  void* stream, uint32_t flags, void* ev_before, void* ev_after);
 
 /* End-to-end call on HOST input, overlapping the host->device copy with the computation (PAPER.md
  * line 173: the per-window statistics of Table 2, as nsg_window_stats_packed).

@@ -14,7 +14,6 @@ from .api import (  # noqa: F401
     DEFAULT_WINDOW,
     FLAG_FORCE_GLOBAL,
     FLAG_INJECT_OVERFLOW,
-    FLAG_NO_FALLBACK_CHECK,
     IP_SET_NAMES,
     NUM_STATS,
     STAT_NAMES,

@@ -12,13 +12,15 @@ import subprocess
 _PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(_PKG)
 LIB_PATH = os.path.join(_PKG, "libnsg.so")
+DEBUG_LIB_PATH = os.path.join(_PKG, "libnsg_debug.so")  # -DNSG_DEBUG_CHECKS: self-check read back (tests)
 SOURCES = [os.path.join(_PKG, "csrc", f) for f in ("nsg.cu", "nsg_common.cuh", "nsg_fast.cuh", "nsg_global.cuh",
                                                    "nsg_trace.cuh", "nsg_anon.cuh", "nsg_flat.cuh")]
 HEADER = os.path.join(ROOT, "include", "nsg.h")
+INTERNAL_HEADER = os.path.join(ROOT, "include", "nsg_internal.h")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 
-# Every symbol include/nsg.h declares (checked by tests/test_abi.py).
+# Every symbol include/nsg.h and include/nsg_internal.h declare (checked by tests/test_abi.py).
 EXPORTS = (
     "nsg_num_windows",
     "nsg_workspace_bytes",
@@ -65,17 +67,20 @@ STATUS = {
 }
 
 
-def build_libnsg(force: bool = False, verbose: bool = False) -> str:
-    """nvcc -gencode arch=compute_100a,code=sm_100a ... -> paper_2509_03653_b200/libnsg.so"""
-    newest = max(os.path.getmtime(p) for p in SOURCES + [HEADER])
-    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < newest:
-        tmp = LIB_PATH + f".tmp{os.getpid()}"
-        cmd = ["nvcc", *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", tmp, SOURCES[0]]
+def build_libnsg(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    """nvcc -gencode arch=compute_100a,code=sm_100a ... -> paper_2509_03653_b200/libnsg.so
+    (debug=True: libnsg_debug.so, the same sources with -DNSG_DEBUG_CHECKS)."""
+    path = DEBUG_LIB_PATH if debug else LIB_PATH
+    newest = max(os.path.getmtime(p) for p in SOURCES + [HEADER, INTERNAL_HEADER])
+    if force or not os.path.exists(path) or os.path.getmtime(path) < newest:
+        tmp = path + f".tmp{os.getpid()}"
+        cmd = ["nvcc", *NVCC_FLAGS, *(["-DNSG_DEBUG_CHECKS"] if debug else []), "-I", os.path.join(ROOT, "include"),
+               "-o", tmp, SOURCES[0]]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)
-        os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+        os.replace(tmp, path)
+    return path
 
 
 class NsgVectors(ctypes.Structure):
@@ -91,10 +96,10 @@ class NsgError(RuntimeError):
         self.status = status
 
 
-def load() -> ctypes.CDLL:
-    path = os.environ.get("NSG_LIB_PATH_DEV", LIB_PATH)  # development override: a variant build of libnsg
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libnsg (the product library; tests may pass DEBUG_LIB_PATH)."""
     if not os.path.exists(path):
-        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+        raise ImportError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
                           "(there is no CPU fallback)")
     lib = ctypes.CDLL(path)
     u64, sz, vp, u32 = ctypes.c_uint64, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_uint32

@@ -33,9 +33,13 @@ STAT_NAMES = (
 DEFAULT_WINDOW = 1 << 17
 MAX_WINDOW = 1 << 31
 
+# include/nsg.h fault-injection flags (tests of the L2-path hand-off)
 FLAG_FORCE_GLOBAL = 1
 FLAG_INJECT_OVERFLOW = 2
-FLAG_NO_FALLBACK_CHECK = 4
+# include/nsg_internal.h: measurement / development switches, not part of the product interface
+_FLAG_NO_FALLBACK_CHECK = 4
+_FLAG_LEGACY_FAST = 16
+_FLAG_INJECT_SELF_CHECK = 32
 
 _U32_TYPES = (torch.int32, torch.uint32)
 _U64_TYPES = (torch.int64, torch.uint64)
@@ -83,19 +87,24 @@ class Workspace:
 _ws_cache: dict = {}
 
 
-def _workspace(n: int, window: int, device: torch.device, workspace: Optional[Workspace]) -> Workspace:
+def _workspace(n: int, window: int, device: torch.device, workspace: Optional[Workspace], stream=None) -> Workspace:
+    """The caller's workspace, or an implicit one cached per (device, shape, stream): two calls on
+    different streams never share scratch, and an evicted entry is dropped only after its stream has
+    drained."""
     if workspace is not None:
         if not workspace.fits(n, window):
             raise NsgError(3, "workspace too small")
         return workspace
-    key = (device.index, n, window)
-    ws = _ws_cache.get(key)
-    if ws is None:
-        if len(_ws_cache) > 8:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    key = (device.index, n, window, s.cuda_stream)
+    hit = _ws_cache.get(key)
+    if hit is None:
+        if len(_ws_cache) >= 8:
+            for ws_old, s_old in _ws_cache.values():
+                s_old.synchronize()
             _ws_cache.clear()
-        ws = Workspace(n, window, device)
-        _ws_cache[key] = ws
-    return ws
+        hit = _ws_cache[key] = (Workspace(n, window, device), s)
+    return hit[0]
 
 
 def _check(t: torch.Tensor, name: str, dtypes) -> None:
@@ -107,6 +116,15 @@ def _check(t: torch.Tensor, name: str, dtypes) -> None:
         raise TypeError(f"{name} has dtype {t.dtype}; expected one of {dtypes}")
     if t.dim() != 1 or not t.is_contiguous():
         raise ValueError(f"{name} must be a contiguous 1-D tensor")
+
+
+def _keep(stream, *tensors) -> None:
+    """The tensors are used by work enqueued on `stream`: the caching allocator must not hand their memory
+    to another stream before that work completes (they may be temporaries of this call, or be freed by the
+    caller while `stream` still runs)."""
+    for t in tensors:
+        if t is not None and t.is_cuda:
+            t.record_stream(stream)
 
 
 def _launch(src, dst, keys, n, window, out, workspace, stream, flags, device, events=None):
@@ -121,21 +139,29 @@ def _launch(src, dst, keys, n, window, out, workspace, stream, flags, device, ev
             raise ValueError("out must be a contiguous CUDA int64/uint64 tensor with >= n_windows*9 elements")
     if n == 0:
         return out
-    ws = _workspace(n, window, device, workspace)
     s = stream if stream is not None else torch.cuda.current_stream(device)
-    ev0 = ev1 = None
-    if events is not None:
+    ws = _workspace(n, window, device, workspace, s)
+    _keep(s, out, ws.buffer, src, dst, keys)
+    u64p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
+    if events is not None:  # measurement: nsg_window_stats_timed (include/nsg_internal.h)
         for e in events:
             if not e.cuda_event:  # torch creates the cudaEvent_t lazily, on first record
                 e.record(s)
         ev0, ev1 = (ctypes.c_void_p(e.cuda_event) for e in events)
-    rc = _lib.nsg_window_stats_timed(
-        None if src is None else src.data_ptr(),
-        None if dst is None else dst.data_ptr(),
-        None if keys is None else keys.data_ptr(),
-        n, window, out.data_ptr(), ws.ptr, ws.nbytes, ctypes.c_void_p(s.cuda_stream), int(flags), ev0, ev1)
+        rc, name = _lib.nsg_window_stats_timed(u64p(src), u64p(dst), u64p(keys), n, window, out.data_ptr(), ws.ptr,
+                                               ws.nbytes, ctypes.c_void_p(s.cuda_stream), int(flags), ev0,
+                                               ev1), "nsg_window_stats_timed"
+    elif flags:
+        rc, name = _lib.nsg_window_stats_ex(u64p(src), u64p(dst), u64p(keys), n, window, out.data_ptr(), ws.ptr,
+                                            ws.nbytes, ctypes.c_void_p(s.cuda_stream), int(flags)), "nsg_window_stats_ex"
+    elif keys is not None:
+        rc, name = _lib.nsg_window_stats_packed(keys.data_ptr(), n, window, out.data_ptr(), ws.ptr, ws.nbytes,
+                                                ctypes.c_void_p(s.cuda_stream)), "nsg_window_stats_packed"
+    else:
+        rc, name = _lib.nsg_window_stats(src.data_ptr(), dst.data_ptr(), n, window, out.data_ptr(), ws.ptr,
+                                         ws.nbytes, ctypes.c_void_p(s.cuda_stream)), "nsg_window_stats"
     if rc != 0:
-        raise NsgError(rc, "nsg_window_stats_timed")
+        raise NsgError(rc, name)
     return out
 
 
@@ -212,7 +238,9 @@ def window_stats_from_host(keys_host: torch.Tensor, window: int = DEFAULT_WINDOW
     elif out_host.is_cuda or not out_host.is_pinned() or out_host.numel() < nw * NUM_STATS or not out_host.is_contiguous():
         raise ValueError("out_host must be a pinned contiguous CPU tensor with >= n_windows*9 elements")
     if n:
-        ws = _workspace(n, window, dev, workspace)
+        ws = _workspace(n, window, dev, workspace, s)
+        _keep(s, ws.buffer, keys_dev, out)
+        _keep(cs, keys_dev)  # written by the copy stream
         rc = _lib.nsg_window_stats_from_host(
             keys_host.data_ptr(), n, window, keys_dev.data_ptr(), out.data_ptr(), out_host.data_ptr(), ws.ptr,
             ws.nbytes, ctypes.c_void_p(s.cuda_stream), ctypes.c_void_p(cs.cuda_stream), int(chunk_windows))
@@ -290,8 +318,9 @@ def window_vectors(keys: Optional[torch.Tensor] = None, window: int = DEFAULT_WI
         v.ip_sets = r["ip_sets"].data_ptr()
     if n == 0:
         return r
-    ws = _workspace(n, window, device, workspace)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    ws = _workspace(n, window, device, workspace, s)
+    _keep(s, ws.buffer, src, dst, keys, n_packets, *r.values())
     if n_packets is not None:
         _check(n_packets, "n_packets", _U32_TYPES)
         if n_packets.numel() != n or n_packets.device != device:
@@ -345,8 +374,9 @@ def window_stats_weighted(keys: Optional[torch.Tensor] = None, n_packets: Option
         raise ValueError("out must be a contiguous CUDA int64/uint64 tensor with >= n_windows*9 elements")
     if n == 0:
         return out
-    ws = _workspace(n, window, device, workspace)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    ws = _workspace(n, window, device, workspace, s)
+    _keep(s, ws.buffer, src, dst, keys, n_packets, out)
     rc = _lib.nsg_window_stats_weighted(
         None if src is None else src.data_ptr(), None if dst is None else dst.data_ptr(),
         None if keys is None else keys.data_ptr(), n_packets.data_ptr(), n, window, out.data_ptr(), ws.ptr,
@@ -411,6 +441,7 @@ def trace_stats(keys: Optional[torch.Tensor] = None, *, src=None, dst=None, out=
         return out.zero_()
     ws = _Scratch(_lib.nsg_trace_stats_workspace_bytes(n), device)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    _keep(s, ws.buffer, out, src, dst, keys, n_packets)
     if n_packets is not None:
         _check(n_packets, "n_packets", _U32_TYPES)
         if n_packets.numel() != n or n_packets.device != device:
@@ -434,6 +465,7 @@ def trace_partition(keys: torch.Tensor, world: int, workspace: TraceWorkspace, s
     send = torch.empty(n, dtype=torch.int64, device=device)
     counts = torch.zeros(world, dtype=torch.int64, device=device)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    _keep(s, keys, send, counts, workspace.buffer)
     rc = _lib.nsg_trace_partition(None, None, keys.data_ptr(), n, int(world), send.data_ptr(), counts.data_ptr(),
                                   workspace.ptr, workspace.nbytes, workspace.key_capacity, workspace.record_capacity,
                                   ctypes.c_void_p(s.cuda_stream))
@@ -451,6 +483,7 @@ def trace_links(keys: torch.Tensor, world: int, workspace: TraceWorkspace, strea
     rd = torch.empty(max(n, 1), dtype=torch.int64, device=device)
     rc_ = torch.zeros((2, world), dtype=torch.int64, device=device)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    _keep(s, keys, stats, rs, rd, rc_, workspace.buffer)
     rc = _lib.nsg_trace_links(None, None, keys.data_ptr() if n else None, n, int(world), stats.data_ptr(), rs.data_ptr(),
                               rd.data_ptr(), rc_.data_ptr(), workspace.ptr, workspace.nbytes, workspace.key_capacity,
                               workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
@@ -464,6 +497,7 @@ def trace_nodes(records: torch.Tensor, workspace: TraceWorkspace, stream=None) -
     m, device = records.numel(), records.device
     stats = torch.zeros(3, dtype=torch.int64, device=device)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    _keep(s, records, stats, workspace.buffer)
     rc = _lib.nsg_trace_nodes(records.data_ptr() if m else None, m, stats.data_ptr(), workspace.ptr, workspace.nbytes,
                               workspace.key_capacity, workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
     if rc != 0:
@@ -487,10 +521,11 @@ def anonymize(keys: Optional[torch.Tensor] = None, *, src=None, dst=None, seed: 
     so = torch.empty(n, dtype=torch.int32, device=device)
     do = torch.empty(n, dtype=torch.int32, device=device)
     nu = torch.zeros(1, dtype=torch.int64, device=device)
-    ws = _anon_ws.get(device.index)
-    if ws is None:
-        ws = _anon_ws[device.index] = _Scratch(_lib.nsg_anonymize_workspace_bytes(), device)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    ws = _anon_ws.get((device.index, s.cuda_stream))  # one scratch per stream: concurrent calls never share it
+    if ws is None:
+        ws = _anon_ws[(device.index, s.cuda_stream)] = _Scratch(_lib.nsg_anonymize_workspace_bytes(), device)
+    _keep(s, ws.buffer, so, do, nu, src, dst, keys)
     rc = _lib.nsg_anonymize(_p(src), _p(dst), _p(keys), n, int(seed) & (2 ** 64 - 1), int(rounds), so.data_ptr(),
                             do.data_ptr(), nu.data_ptr(), ws.ptr, ws.nbytes, ctypes.c_void_p(s.cuda_stream))
     if rc != 0:
@@ -549,6 +584,7 @@ def trace_owner_counts(keys: torch.Tensor, world: int, workspace: TraceWorkspace
     n, device = _rows(keys, None, None)
     counts = torch.zeros(world, dtype=torch.int64, device=device)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    _keep(s, keys, counts, workspace.buffer)
     rc = _lib.nsg_trace_owner_counts(None, None, keys.data_ptr() if n else None, n, int(world), counts.data_ptr(),
                                      workspace.ptr, workspace.nbytes, workspace.key_capacity,
                                      workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
@@ -562,6 +598,7 @@ def trace_partition_peers(keys: torch.Tensor, world: int, peer_ptrs: torch.Tenso
     """Scatter the keys straight into the owners' receive buffers (nsg_trace_partition_peers)."""
     n, device = _rows(keys, None, None)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    _keep(s, keys, peer_ptrs, peer_base, workspace.buffer)
     rc = _lib.nsg_trace_partition_peers(None, None, keys.data_ptr() if n else None, n, int(world), peer_ptrs.data_ptr(),
                                         peer_base.data_ptr(), workspace.ptr, workspace.nbytes, workspace.key_capacity,
                                         workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
@@ -576,6 +613,7 @@ def trace_links_count(keys: torch.Tensor, world: int, workspace: TraceWorkspace,
     stats = torch.zeros(3, dtype=torch.int64, device=device)
     rc_ = torch.zeros((2, world), dtype=torch.int64, device=device)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    _keep(s, keys, stats, rc_, workspace.buffer)
     rc = _lib.nsg_trace_links_count(None, None, keys.data_ptr() if n else None, n, int(world), stats.data_ptr(),
                                     rc_.data_ptr(), workspace.ptr, workspace.nbytes, workspace.key_capacity,
                                     workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
@@ -589,6 +627,7 @@ def trace_links_emit_peers(world: int, ptrs_src: torch.Tensor, ptrs_dst: torch.T
     """Emit the records of the table left by trace_links_count straight into the owners' buffers."""
     device = ptrs_src.device
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    _keep(s, ptrs_src, ptrs_dst, base_src, base_dst, workspace.buffer)
     rc = _lib.nsg_trace_links_emit_peers(int(world), ptrs_src.data_ptr(), ptrs_dst.data_ptr(), base_src.data_ptr(),
                                          base_dst.data_ptr(), workspace.ptr, workspace.nbytes, workspace.key_capacity,
                                          workspace.record_capacity, ctypes.c_void_p(s.cuda_stream))
@@ -610,8 +649,9 @@ def window_stats_mirrored(keys: torch.Tensor, mirrors: torch.Tensor, row0: int, 
         out = torch.empty((nw, NUM_STATS), dtype=torch.int64, device=device)
     if n == 0:
         return out
-    ws = _workspace(n, window, device, workspace)
     s = stream if stream is not None else torch.cuda.current_stream(device)
+    ws = _workspace(n, window, device, workspace, s)
+    _keep(s, ws.buffer, keys, mirrors, out)
     rc = _lib.nsg_window_stats_mirrored(None, None, keys.data_ptr(), n, window, out.data_ptr(), ws.ptr, ws.nbytes,
                                         ctypes.c_void_p(s.cuda_stream), int(flags), mirrors.data_ptr(),
                                         mirrors.numel(), int(row0))

@@ -17,7 +17,7 @@
 // This file holds the C ABI: argument checks, workspace layout, launches.
 #include <algorithm>
 #include <cuda.h>  // driver types for cuStreamWriteValue32 (resolved at run time: no libcuda link)
-#include "nsg.h"
+#include "nsg_internal.h"
 #include "nsg_common.cuh"
 #include "nsg_fast.cuh"
 #include "nsg_flat.cuh"
@@ -97,7 +97,7 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     L.o_rend = o; o = align256(o + (size_t)L.R * L.B * (2 * L.B2) * sizeof(u32));
     L.o_lres = o; o = align256(o + (size_t)L.R * L.B * 4 * sizeof(u32));
     L.o_sres = o; o = align256(o + (size_t)L.R * 2 * L.B2 * 4 * sizeof(u32));
-    L.o_s0list = o; o = align256(o + (size_t)L.R * L.B2 * TCAP_S * sizeof(u32));
+    L.o_s0list = o; o = align256(o + (size_t)L.R * L.B2 * S0LIST * sizeof(u32));
     L.o_wscr = o; o = align256(o + (size_t)L.R * L.cp * CH * sizeof(u32));
   }
   L.flat = W <= flat::MAX_W;
@@ -211,7 +211,7 @@ static WriteValue32Fn write_value32() {
   return fn;
 }
 
-static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u64 W, u64* out, void* ws,
+static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 n, u64 W, u64* out, void* ws,
                       size_t ws_bytes, void* stream, u32 flags, void* ev_before = nullptr, void* ev_after = nullptr,
                       const StreamIn* sin = nullptr, const nsg_vectors* vec = nullptr, const u32* wgt = nullptr,
                       u64* const* mirror = nullptr, u32 n_mirror = 0, u64 mirror_row0 = 0) {
@@ -317,7 +317,7 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
     g.roff = reinterpret_cast<u32*>(base + L.o_froff);
     g.diag = reinterpret_cast<u32*>(base + DIAG_OFFSET);
     g.mirror = mirror; g.n_mirror = n_mirror; g.mirror_row0 = mirror_row0;
-    g.inject = (flags & NSG_FLAG_INJECT_OVERFLOW) ? 1u : 0u;
+    g.inject = ((flags & NSG_FLAG_INJECT_OVERFLOW) ? 1u : 0u) | ((flags & NSG_FLAG_INJECT_SELF_CHECK) ? 2u : 0u);
     if (cudaMemsetAsync(base + L.o_fws, 0, (size_t)L.nw * sizeof(flat::WinState), s) != cudaSuccess) return NSG_ERR_CUDA;
     if (ev_before && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_before), s) != cudaSuccess) return NSG_ERR_CUDA;
     for (u64 w0 = 0; w0 < L.nw; w0 += L.fNB) {
@@ -440,6 +440,28 @@ static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u6
     if (ev_after && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_after), s) != cudaSuccess) return NSG_ERR_CUDA;
   }
   return NSG_OK;
+}
+
+// The nsg_window_stats* entry points.  A debug build (-DNSG_DEBUG_CHECKS) reads the device self-check
+// back (nsg.h "Errors"): it synchronises the stream and returns NSG_ERR_INTERNAL if any window failed it.
+static nsg_status run(const u32* src, const u32* dst, const u64* keys, u64 n, u64 W, u64* out, void* ws,
+                      size_t ws_bytes, void* stream, u32 flags, void* ev_before = nullptr, void* ev_after = nullptr,
+                      const StreamIn* sin = nullptr, const nsg_vectors* vec = nullptr, const u32* wgt = nullptr,
+                      u64* const* mirror = nullptr, u32 n_mirror = 0, u64 mirror_row0 = 0) {
+  const nsg_status st = run_impl(src, dst, keys, n, W, out, ws, ws_bytes, stream, flags, ev_before, ev_after, sin, vec,
+                                 wgt, mirror, n_mirror, mirror_row0);
+#ifdef NSG_DEBUG_CHECKS
+  if (st == NSG_OK && n) {
+    u32 dg[4];
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (cudaMemcpyAsync(dg, reinterpret_cast<unsigned char*>(ws) + DIAG_OFFSET, sizeof(dg), cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return NSG_ERR_CUDA;
+    if (dg[1] != 0) return NSG_ERR_INTERNAL;
+  }
+#endif
+  return st;
 }
 
 // ------------------------------------------------------------------------------------------

@@ -19,7 +19,7 @@
 // small enough to stay in L2, and the gather is one table probe per address; otherwise every address
 // is ranked and permuted directly.
 #pragma once
-#include "nsg.h"
+#include "nsg_internal.h"
 #include "nsg_common.cuh"
 
 namespace nsg {

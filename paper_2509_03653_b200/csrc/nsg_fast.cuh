@@ -26,7 +26,7 @@
 // key), vector outputs (L items append each link, S items each node; S1 items count |S n D| from the
 // S0 item's node list), result mirrors (F writes its row into further tables, e.g. peer ranks').
 #pragma once
-#include "nsg.h"
+#include "nsg_internal.h"
 #include "nsg_common.cuh"
 
 namespace nsg {
@@ -58,6 +58,7 @@ constexpr int TCAP = NSG_TCAP;               // link-table slots (slot = (h * TC
 #define NSG_LOG_FAST_WINDOW 20
 #endif
 constexpr int TCAP_S = NSG_TCAP_S;           // node-table slots of a side item
+constexpr u32 S0LIST = TCAP_S + 1;           // a side-0 node list: a full table plus the address ~0
 constexpr int NODE_BUCKET = TCAP_S / 2;      // side buckets are sized for <= 4096 nodes (load <= 1/2)
 constexpr int PCAP_S = NSG_PCAP_S;           // side items' pending-list capacity
 constexpr int BUCKET_KEYS = NSG_BUCKET_KEYS; // target keys per link bucket (table load factor <= 1/2)
@@ -116,7 +117,7 @@ struct Geo {
   u32* v_node[2]; u32* v_pk[2]; u32* v_fan[2];  // per side: node, packets, fan              (:185, :187, :173)
   u64* v_ipsets;                             // [nw][4] |S u D|, |S \ D|, |D \ S|, |S n D|   (:209)
   u32* vfill;   // [nw][3] fill counters of the link / source / destination vectors
-  u32* s0list;  // [R][B2][TCAP_S] node list of each side-0 item (read by the side-1 item of the bucket)
+  u32* s0list;  // [R][B2][S0LIST] node list of each side-0 item (read by the side-1 item of the bucket)
   u32* s0cnt;   // [R][B2]
   u32* s0win;   // [R][B2]         w+1 once side item S0(w, sb) has published its list (release)
   // Weighted rows (nsg_window_stats_weighted): n_packets per row, or NULL.
@@ -341,6 +342,12 @@ __device__ __forceinline__ long long wait_geq(const u32* p, u32 v, u32 first) {
   return clock64() - t0;
 }
 
+#ifdef NSG_PROFILE_BUILD
+constexpr bool kProfile = true;
+#else
+constexpr bool kProfile = false;
+#endif
+#ifdef NSG_PROFILE_BUILD
 // Phase timer (NSG_FLAG_PROFILE): thread 0 adds the cycles since the previous mark to
 // prof[16 + type*16 + phase].  Marks are placed right after a __syncthreads().
 // profiling: after the first wave, add the number of entries that wanted the pending list to
@@ -373,6 +380,13 @@ __device__ __forceinline__ void prof_add(const Geo& g, int type, long long cyc, 
     atomicMax(reinterpret_cast<unsigned long long*>(&g.prof[type * 4 + 3]), (unsigned long long)(cyc - wait));
   }
 }
+#else  // production build: no profiling code in the kernel
+__device__ __forceinline__ void prof_pending(const Geo&, int, u32) {}
+struct PhaseTimer {
+  __device__ __forceinline__ void mark(const Geo&, int, int) {}
+};
+__device__ __forceinline__ void prof_add(const Geo&, int, long long, long long) {}
+#endif
 
 // ------------------------------------------------------------------------------------------
 // P item: partition one chunk of window w by link bucket
@@ -956,7 +970,7 @@ __device__ __noinline__ void side_vectors(const SideVec g, u64 w, int side, u32 
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const bool nodes = g.node != nullptr;
   const bool list0 = side == 0 && g.ipsets;
-  u32* list = g.s0list + ((u64)slot * g.B2 + sb) * TCAP_S;
+  u32* list = g.s0list + ((u64)slot * g.B2 + sb) * S0LIST;
   if (t == 0) {
     u32 tot = 0;
     for (int i = 0; i < NWARP; ++i) tot += m.wtmp[4 * NWARP + i];
@@ -1040,7 +1054,7 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
     u32* wlo = s.wlo[wid];
     u32* wpre = s.wpre[wid];
     const u32 total = warp_segments(wlo, wpre, nseg, lo, len);
-    if (lane == 0 && (g.flags & NSG_FLAG_PROFILE) && w == 0 && side * B2 + sb < 64)
+    if (kProfile && lane == 0 && (g.flags & NSG_FLAG_PROFILE) && w == 0 && side * B2 + sb < 64)
       atomicAdd(reinterpret_cast<unsigned long long*>(&g.prof[192 + side * B2 + sb]), (unsigned long long)total);
     u64 r[KPT];
 #pragma unroll
@@ -1179,7 +1193,7 @@ __device__ void item_side(const Geo& g, u64 w, int side, u32 sb, SmemS& s, SmemM
     u32 bp = lane < NWARP ? m.wtmp[5 * NWARP + lane] : 0u;
     u32 cf = lane < NWARP ? m.wtmp[6 * NWARP + lane] : 0u;
     a = warp_sum(a); bp = warp_max(bp); cf = warp_max(cf);
-    if (lane == 0 && (g.flags & NSG_FLAG_PROFILE) && w == 0 && side * B2 + sb < 64) {  // window-0 detail
+    if (kProfile && lane == 0 && (g.flags & NSG_FLAG_PROFILE) && w == 0 && side * B2 + sb < 64) {  // window-0 detail
       g.prof[128 + side * B2 + sb] = (u64)(clock64() - tstart);
     }
     if (lane == 0) {

@@ -23,7 +23,7 @@
 // aggregated increment, never a CAS); collisions probe on with double hashing; claimed slots are kept
 // in a dense claim list so that the final scans visit entries only.
 #pragma once
-#include "nsg.h"
+#include "nsg_internal.h"
 #include "nsg_common.cuh"
 
 namespace nsg {
@@ -69,7 +69,8 @@ struct FGeo {
   u64* const* mirror;
   u32 n_mirror;
   u64 mirror_row0;
-  u32 inject;                      // NSG_FLAG_INJECT_OVERFLOW: odd windows are handed to the L2 path
+  u32 inject;                      // bit 0 NSG_FLAG_INJECT_OVERFLOW: odd windows are handed to the L2 path;
+                                   // bit 1 NSG_FLAG_INJECT_SELF_CHECK: window 0 counts a self-check failure
 };
 
 __device__ __forceinline__ u32 link_bucket(u64 key, u32 logB) { return logB ? (u32)((key * MUL_L) >> (64 - logB)) : 0u; }
@@ -517,7 +518,7 @@ __device__ __forceinline__ void node_add(SmemS& s, u32 slot, u32 c, bool wrapche
 __device__ void finalize(const FGeo& g, u64 w, u64* out) {
   WinState* st = &g.ws[w];
   u32 ovf = ldcg32(&st->ovf);
-  if (g.inject && (w & 1)) { st->ovf = 1; ovf = 1; }
+  if ((g.inject & 1u) && (w & 1)) { st->ovf = 1; ovf = 1; }
   if (ovf) {  // recomputed by the L2 path; diag[0] counts the windows handed over
     atomicAdd(&g.diag[0], 1u);
     return;
@@ -533,7 +534,7 @@ __device__ void finalize(const FGeo& g, u64 w, u64* out) {
   row[6] = ldcg32(&st->nodes[1]);
   row[7] = ldcg32(&st->maxp[1]);
   row[8] = ldcg32(&st->maxf[1]);
-  if (row[0] != len) atomicAdd(&g.diag[1], 1u);  // self-check: the counts sum to the window's packets
+  if (row[0] != len || ((g.inject & 2u) && w == 0)) atomicAdd(&g.diag[1], 1u);  // self-check: the counts sum to the window's packets
   store_row(out + w * NSG_NUM_STATS, row);
   for (u32 m = 0; m < g.n_mirror; ++m) store_row(g.mirror[m] + (g.mirror_row0 + w) * NSG_NUM_STATS, row);
 }

@@ -2,7 +2,7 @@
 // Used for windows larger than the fast path supports and as the fast path's overflow hand-off.
 // Same definitions as the fast path (Table 2; mirrors line 173).
 #pragma once
-#include "nsg.h"
+#include "nsg_internal.h"
 #include "nsg_common.cuh"
 
 namespace nsg {

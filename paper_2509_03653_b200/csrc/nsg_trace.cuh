@@ -10,7 +10,7 @@
 //              :187; the column mirrors for destination records, :173) -> unique, max packets, max fan
 // With world = 1 nothing is exchanged: nsg_trace_stats runs links -> nodes(src) -> nodes(dst).
 #pragma once
-#include "nsg.h"
+#include "nsg_internal.h"
 #include "nsg_common.cuh"
 #include "nsg_global.cuh"
 

@@ -82,6 +82,10 @@ def distributed_window_stats(keys_local: torch.Tensor, n_windows: int, window: i
     if tab is None:
         tab = _result_tables[key] = PeerBuffers(n_windows * NUM_STATS, group, device)
     w0, w1 = window_block(n_windows, rank, world)
+    # The kernels below store into every peer's table: first let every rank finish reading its table
+    # from the previous call (the clone below runs asynchronously on its stream).
+    torch.cuda.synchronize(device)
+    dist.barrier(group=group)
     window_stats_mirrored(keys_local, tab.ptrs, w0, window, workspace=workspace)
     torch.cuda.synchronize(device)
     dist.barrier(group=group)  # every rank's rows are in every table

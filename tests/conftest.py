@@ -20,6 +20,7 @@ def pytest_sessionstart(session):
 
     lib = __graft_entry__._load_file("_nsg_build_lib", os.path.join(ROOT, "paper_2509_03653_b200", "_lib.py"))
     lib.build_libnsg()
+    lib.build_libnsg(debug=True)  # -DNSG_DEBUG_CHECKS variant (tests of the NSG_ERR_INTERNAL readback)
     import gen
     import oracle
 

@@ -1,5 +1,6 @@
-"""The C-ABI library loads and exports every symbol include/nsg.h declares; host-side argument
-handling (no compute call needs a GPU here)."""
+"""The C-ABI library loads and exports every symbol include/nsg.h (product interface) and
+include/nsg_internal.h (measurement / test hooks) declare; the debug build exports the same; host-side
+argument handling (no compute call needs a GPU here)."""
 import ctypes
 import os
 import re
@@ -9,13 +10,32 @@ import pytest
 from nsg_testutil import ROOT
 
 HEADER = os.path.join(ROOT, "include", "nsg.h")
+INTERNAL = os.path.join(ROOT, "include", "nsg_internal.h")
 LIB = os.path.join(ROOT, "paper_2509_03653_b200", "libnsg.so")
+DEBUG_LIB = os.path.join(ROOT, "paper_2509_03653_b200", "libnsg_debug.so")
 
 
-def declared_functions():
-    src = open(HEADER).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(nsg_[a-z_]+)\s*\(", src)))
+def declared_functions(headers=(HEADER, INTERNAL)):
+    names = set()
+    for h in headers:
+        src = re.sub(r"/\*.*?\*/", "", open(h).read(), flags=re.S)
+        names |= set(re.findall(r"\b(nsg_[a-z_]+)\s*\(", src))
+    return sorted(names)
+
+
+def test_measurement_hooks_are_not_in_the_product_header():
+    public = declared_functions((HEADER,))
+    assert "nsg_window_stats_timed" not in public
+    text = open(HEADER).read()
+    for flag in ("NSG_FLAG_NO_FALLBACK_CHECK", "NSG_FLAG_PROFILE", "NSG_FLAG_LEGACY_FAST"):
+        assert flag not in text
+        assert flag in open(INTERNAL).read()
+
+
+def test_debug_library_exports_the_same_symbols():
+    lib = ctypes.CDLL(DEBUG_LIB)
+    for name in declared_functions():
+        assert hasattr(lib, name), name
 
 
 def test_header_declares_expected_entry_points():

@@ -71,3 +71,57 @@ def test_window_sharded_gather(cuda_device, transport, world, n):
         want = oracle.window_stats_sort(keys=keys, window=W)
         for r in range(world):
             assert results[r][rep].view(np.uint64).tolist() == want.tolist(), (r, rep)
+
+
+def _c4_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from gen.configs import CONFIGS
+    from paper_2509_03653_b200.distributed import distributed_window_stats, packet_block
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        c = CONFIGS["C4"]
+        nw = c.n_packets // c.window
+        p0, p1 = packet_block(c.n_packets, c.window, rank, world)
+        kd = torch.empty(p1 - p0, dtype=torch.int64, device="cuda")
+        gen.generate_device(c.dist, c.seed, p0, p1 - p0, keys=kd)  # this rank's windows only
+        table = distributed_window_stats(kd, nw, c.window).cpu().numpy()
+        q.put((rank, table if rank == 0 else int(table.sum())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_c4_split_over_8_ranks(cuda_device):
+    """C4 (2^30 packets, 8192 windows) as bench.py --gpus 8 splits it: 8 ranks (processes sharing the
+    one GPU, gloo standing in for NCCL) each generate and compute their contiguous window block, then
+    distributed_window_stats gathers the [8192, 9] table onto every rank; rank 0's table is compared
+    with the oracle O2 on every window, the other ranks' tables by checksum."""
+    import torch.multiprocessing as mp
+
+    from gen.configs import CONFIGS
+
+    world = 8
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_c4_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    table = results[0].view(np.uint64)
+    assert all(results[r] == int(results[0].sum()) for r in range(1, world))
+    c = CONFIGS["C4"]
+    blk = 256 * c.window
+    kd = torch.empty(blk, dtype=torch.int64, device=cuda_device)
+    for b0 in range(0, c.n_packets, blk):
+        gen.generate_device(c.dist, c.seed, b0, blk, keys=kd)
+        want = oracle.window_stats_sort(keys=kd.cpu().numpy().view(np.uint64), window=c.window)
+        w0 = b0 // c.window
+        assert table[w0:w0 + want.shape[0]].tolist() == want.tolist(), w0

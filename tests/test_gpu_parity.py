@@ -1,8 +1,7 @@
 """CUDA path (libnsg, through the C ABI) vs the CPU oracle, element by element (-m gpu).
 
 Bit-exact is the bar: every output is an integer.  Cases: the BASELINE configs
-at full size (C1-C3 fully; C4 2^30 packets in bench.py's launch configuration, sampled windows
-regenerated on the host by the counter-based generator), ragged tails, window sizes spanning one to
+at full size (C1-C3 fully; C4 2^30 packets in bench.py's launch configuration, all 8192 windows), ragged tails, window sizes spanning one to
 many partition chunks and link buckets, the L2 path (forced, and the overflow hand-off), adversarial
 keys (the empty-slot sentinels, all-equal windows, stars), misaligned bases, both input layouts.
 """
@@ -199,22 +198,26 @@ def test_device_generator_matches_host(nsg, cuda_device):
         assert np.array_equal(kd.cpu().numpy().view(np.uint64), host)
 
 
-def test_c4_full_size_sampled(nsg, cuda_device):
+def test_c4_full_size_all_windows(nsg, cuda_device):
     """C4: 2^30 packets generated on device, one launch over all 8192 windows (bench.py's launch
-    configuration at N=1); sampled windows (first, last, and a spread) checked against the oracle on
-    windows regenerated on the host."""
+    configuration at N=1); EVERY window checked against the oracle O2.  The oracle's input is the same
+    seeded generator's output (gen/, which holds none of the method's arithmetic and is pinned equal
+    to the host generator by test_device_generator_matches_host), copied to the host block by block."""
     c = CONFIGS["C4"]
     kd = torch.empty(c.n_packets, dtype=torch.int64, device=cuda_device)
     gen.generate_device(c.dist, c.seed, 0, c.n_packets, keys=kd)
     got = nsg.window_stats_packed(kd, c.window).cpu().numpy().view(np.uint64)
-    del kd
     nw = c.n_packets // c.window
     assert got.shape == (nw, 9)
-    assert np.all(got[:, 0] == c.window)
-    sample = sorted(set([0, 1, nw // 2, nw - 2, nw - 1] + list(np.random.default_rng(4).integers(0, nw, 11))))
-    for w in sample:
+    blk = 256 * c.window
+    host = torch.empty(blk, dtype=torch.int64).pin_memory()
+    for b0 in range(0, c.n_packets, blk):
+        host.copy_(kd[b0:b0 + blk])
+        want = oracle.window_stats_sort(keys=host.numpy().view(np.uint64), window=c.window)
+        w0 = b0 // c.window
+        assert_parity(got[w0:w0 + want.shape[0]], want)
+    del kd
+    # a spot check that does not rely on the device generator: windows regenerated on the host
+    for w in (0, nw // 2, nw - 1):
         k = gen.generate_host(c.dist, c.seed, w * c.window, c.window, packed=True)
         assert got[w].tolist() == oracle.window_stats_sort(keys=k, window=c.window)[0].tolist(), w
-    # property that holds at any size: the invariants of every window
-    v, L, mL, uS, mSP, mFO, uD, mDP, mFI = [got[:, i].astype(np.int64) for i in range(9)]
-    assert np.all((mFO <= uD) & (mFI <= uS) & (mL <= np.minimum(mSP, mDP)) & (np.maximum(uS, uD) <= L) & (L <= v))

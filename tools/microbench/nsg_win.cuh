@@ -26,7 +26,7 @@
 // consumers' and producers' critical paths.  An item only waits on items with smaller tickets, and each
 // CTA processes its items in ticket order, so the schedule is deadlock-free.
 #pragma once
-#include "nsg.h"
+#include "nsg_internal.h"
 #include "nsg_common.cuh"
 
 namespace nsg {
