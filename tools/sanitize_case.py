@@ -1,0 +1,30 @@
+"""One call of the per-window path for compute-sanitizer (memcheck / racecheck / synccheck), checked
+against the oracle.  usage: python tools/sanitize_case.py {C1|C2r} {flat|legacy|vectors}
+C2r = the first 4 windows of C2 (sanitizer replay is slow)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+import oracle  # noqa: E402
+import paper_2509_03653_b200 as nsg  # noqa: E402
+from gen.configs import CONFIGS  # noqa: E402
+
+cfg, path = sys.argv[1], sys.argv[2]
+c = CONFIGS["C1" if cfg == "C1" else "C2"]
+n = c.n_packets if cfg == "C1" else 4 * c.window + 1234
+keys = gen.generate_host(c.dist, c.seed, 0, n, packed=True)
+kd = torch.from_numpy(keys.view(np.int64)).cuda()
+want = oracle.window_stats_sort(keys=keys, window=c.window)
+if path == "vectors":
+    got = nsg.window_vectors(kd, c.window)["stats"]
+else:
+    got = nsg.window_stats_packed(kd, c.window, flags=nsg.api._FLAG_LEGACY_FAST if path == "legacy" else 0)
+got = got.cpu().numpy().view(np.uint64)
+ok = np.array_equal(got, want)
+print(f"{cfg} {path}: parity {'OK' if ok else 'FAIL'}")
+sys.exit(0 if ok else 1)
