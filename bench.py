@@ -4,11 +4,14 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C2|C3|C1]
 
 One step = one pass of the whole hot path (partition -> link buckets -> side buckets -> the nine
-statistics of every window) over one C2-sized batch: 64 windows x 2^17 packets per GPU (weak
-scaling), Zipf(s=1.1, K=2^20) IPv4 pairs from the seeded counter-based generator, generated on the
-device.  Steps cycle through a 1 GiB ring of 16 such batches per GPU, so every step reads inputs
-that are not L2-resident (126 MB L2).  For N > 1 (torchrun, one rank per GPU, NCCL) each rank owns
-its own window blocks and the 72 B/window results are all-gathered every step.
+statistics of every window) over one batch of windows:
+  N = 1 (default workload C2): one C2 batch, 64 windows x 2^17 packets, Zipf(s=1.1, K=2^20) IPv4 pairs
+        from the seeded counter-based generator, generated on the device; steps cycle through a 1 GiB ring
+        of 16 such batches, so every step reads inputs that are not L2-resident (126 MB L2).
+  N > 1 (default workload C4, torchrun, one rank per GPU, NCCL): the 2^30-packet C4 input (8192
+        windows) split into contiguous window blocks, one per rank, resident in HBM; one call per rank
+        per step over its whole block, then the NCCL all_gather_into_tensor of the 72 B/window result rows
+        inside the timed region (strong scaling; the line also reports the rate without the gather).
 
 The JSON line carries: value (device-timed aggregate packets/s, max over ranks), e2e (the same
 metric through the public API from pinned HOST buffers, H2D + D2H inside the timed region),
@@ -37,6 +40,7 @@ WINDOWS_PER_STEP = 64
 RING = 16
 BYTES_PER_PACKET = 8          # algorithmic: one packed u64 key (src<<32|dst) read once
 BYTES_PER_WINDOW_OUT = 72     # nine u64 per window written
+C4_PACKETS = 1 << 30          # BASELINE configs[3]: 8192 windows
 
 
 def workload(name: str):
@@ -44,6 +48,8 @@ def workload(name: str):
 
     if name == "C2":
         return gen.Dist("zipf", 1.1, 1 << 20), 2, "C2: Zipf(s=1.1, K=2^20) IPv4 pairs, seed 2"
+    if name == "C4":
+        return gen.Dist("zipf", 1.1, 1 << 20), 4, "C4: 2^30 packets (8192 windows), Zipf(s=1.1, K=2^20), seed 4"
     if name == "C3":
         return gen.Dist("heavy"), 3, "C3: heavy skew (Bernoulli(1/2) source 10.0.0.1, uniform dst), seed 3"
     if name == "C1":
@@ -64,14 +70,21 @@ def peaks():
 
 
 def traffic_per_launch(workload_name: str):
-    """dram__bytes_read+write per launch of the persistent kernel from a committed ncu --set full capture."""
+    """dram__bytes_read+write per call (all kernels of one call) from the committed ncu capture
+    profiles/ncu_traffic.json, only if it was taken on the build being benched (same build id)."""
+    from paper_2509_03653_b200 import _lib
+
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             t = json.load(f)
-        e = t.get(workload_name)
-        return None if e is None else float(e["dram_bytes_per_launch"])
     except Exception:
-        return None
+        return None, "no profiles/ncu_traffic.json"
+    e = t.get(workload_name)
+    if e is None:
+        return None, f"no entry for {workload_name}"
+    if e.get("build_id") != _lib.build_id():
+        return None, f"stale: captured on build {e.get('build_id')}, benching {_lib.build_id()}"
+    return float(e["dram_bytes_per_call"]), f"ncu capture of build {e['build_id']} ({e.get('source', '')})"
 
 
 class ClockSampler:
@@ -127,24 +140,57 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(dist, seed, budget_s: float = 10.0):
-    """The CPU oracle (O2, all host threads) on a bounded sample of the same workload."""
+    """The CPU oracle (O2) on a bounded sample of the same workload: all host threads, and one thread."""
     import gen
     import oracle
 
     threads = oracle.hardware_threads()
     done_pkts, t_total, w = 0, 0.0, 0
     batch = WINDOWS_PER_STEP
-    while t_total < budget_s and w < 16 * batch:
+    while t_total < budget_s and w < 128 * batch:
         keys = gen.generate_host(dist, seed, w * WINDOW, batch * WINDOW, packed=True)
         t0 = time.perf_counter()
         oracle.window_stats_sort(keys=keys, window=WINDOW, threads=threads)
         t_total += time.perf_counter() - t0
         done_pkts += batch * WINDOW
         w += batch
+    one = gen.generate_host(dist, seed, 0, 8 * WINDOW, packed=True)
+    t0 = time.perf_counter()
+    oracle.window_stats_sort(keys=one, window=WINDOW, threads=1)
+    t1 = time.perf_counter() - t0
     return {"value": done_pkts / t_total, "unit": UNIT, "cores": threads, "kind": "oracle",
             "sample": f"{w} windows x 2^17 packets of the same stream (O2 std::sort oracle, {threads} threads, "
-                      f"{t_total:.1f} s)"}
+                      f"{t_total:.1f} s)",
+            "value_1core": 8 * WINDOW / t1, "sample_1core": f"8 windows x 2^17 packets, 1 thread, {t1:.2f} s",
+            "cpu_model": cpu_model()}
+
+
+def spot_check(dist, seed, got_rows, first_packet: int, windows):
+    """After the timed region: windows of the last step's device output against the oracle on the same
+    windows regenerated on the host (gen's host generator, which the device generator is pinned to)."""
+    import numpy as np
+
+    import gen
+    import oracle
+
+    ok = True
+    for w in windows:
+        keys = gen.generate_host(dist, seed, first_packet + w * WINDOW, WINDOW, packed=True)
+        want = oracle.window_stats_sort(keys=keys, window=WINDOW)[0]
+        ok = ok and np.array_equal(got_rows[w].view(np.uint64), want)
+    return {"windows": [int(w) for w in windows], "match": bool(ok), "oracle": "O2 (std::sort)"}
 
 
 def run_reference(args):
@@ -157,7 +203,8 @@ def run_reference(args):
         return 0
     dist_, seed, desc = workload(args.workload)
     threads = oracle.hardware_threads()
-    per_step = 8  # windows per reference step: a bounded sample of the workload
+    # windows per reference step: a C2 batch (64 windows), and at least one window per host thread
+    per_step = max(WINDOWS_PER_STEP, threads)
     samples = [gen.generate_host(dist_, seed, i * per_step * WINDOW, per_step * WINDOW, packed=True)
                for i in range(min(4, args.steps + args.warmup))]
     for i in range(args.warmup):
@@ -175,7 +222,8 @@ def run_reference(args):
         "config": {"workload": desc + f" ({per_step} windows of 2^17 packets per step: bounded CPU sample)",
                    "window": WINDOW},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": f"{per_step} windows per step x {args.steps} steps, O2 oracle, {threads} threads"},
+                         "sample": f"{per_step} windows per step x {args.steps} steps, O2 oracle, {threads} threads",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -188,7 +236,7 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--workload", default=None, help="C2 (default at N=1), C4 (default at N>1), C3, C1, Z08/13/15")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--once", action="store_true", help="a single untimed call (for ncu)")
     ap.add_argument("--path", choices=["windows", "trace", "anonymize"], default="windows",
@@ -214,6 +262,8 @@ def main():
                          "destination vectors and IP set counts (nsg_window_vectors, SURVEY §8(f) f1, f3)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.workload is None:
+        args.workload = "C2" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "C4"
     if args.impl == "reference":
         return run_reference(args)
 
@@ -243,24 +293,39 @@ def main():
             tdist.init_process_group(backend)
     dist_, seed, desc = workload(args.workload)
 
-    n = WINDOWS_PER_STEP * WINDOW
-    # this rank's ring: batch i of rank r covers packets [((i * world) + r) * n, ...) of the stream
-    ring_n = RING if args.l2 == "cold" else 1
-    ring = torch.empty((ring_n, n), dtype=torch.int64, device=dev)
-    for i in range(ring_n):
-        gen.generate_device(dist_, seed, ((i * world) + rank) * n, n, keys=ring[i])
+    c4 = args.workload == "C4"
+    if c4:  # the whole C4 input, this rank's contiguous window block resident in HBM (> L2 at any N <= 8)
+        from paper_2509_03653_b200.distributed import packet_block
+
+        c4_p0, c4_p1 = packet_block(C4_PACKETS, WINDOW, rank, world)
+        n = c4_p1 - c4_p0
+        wps, total_windows, ring_n = n // WINDOW, C4_PACKETS // WINDOW, 1
+        ring = torch.empty((1, n), dtype=torch.int64, device=dev)
+        gen.generate_device(dist_, seed, c4_p0, n, keys=ring[0])
+        first_packet = lambda i: c4_p0  # noqa: E731
+    else:
+        n = WINDOWS_PER_STEP * WINDOW
+        wps, total_windows = WINDOWS_PER_STEP, WINDOWS_PER_STEP * world
+        # this rank's ring: batch i of rank r covers packets [((i * world) + r) * n, ...) of the stream
+        ring_n = RING if args.l2 == "cold" else 1
+        ring = torch.empty((ring_n, n), dtype=torch.int64, device=dev)
+        for i in range(ring_n):
+            gen.generate_device(dist_, seed, ((i * world) + rank) * n, n, keys=ring[i])
+        first_packet = lambda i: (((i % ring_n) * world) + rank) * n  # noqa: E731
     torch.cuda.synchronize(dev)
     ws = nsg.Workspace(n, WINDOW, dev)
-    outs = [torch.empty((WINDOWS_PER_STEP, 9), dtype=torch.int64, device=dev) for _ in range(RING)]
+    outs = [torch.empty((wps, 9), dtype=torch.int64, device=dev) for _ in range(RING)]
     vec = args.outputs == "vectors"
     wtd = args.input == "weighted"
     p2p_tab = None
     if world > 1 and args.transport == "p2p":  # the result gather done by the kernels' epilogues (peer memory)
         from paper_2509_03653_b200.distributed import PeerBuffers
 
-        p2p_tab = PeerBuffers(WINDOWS_PER_STEP * world * 9, None, dev)
+        p2p_tab = PeerBuffers(total_windows * 9, None, dev)
     trace = args.path == "trace"
     anon = args.path == "anonymize"
+    if c4 and (trace or anon or vec or wtd or args.transport != "nccl"):
+        raise SystemExit("--workload C4: the per-window statistics with the NCCL gather only")
     if anon and (vec or wtd or world > 1):
         raise SystemExit("--path anonymize: one GPU, --input packets --outputs stats only")
     if trace and (vec or wtd):
@@ -285,7 +350,7 @@ def main():
     # Plain per-window statistics: batches alternate over `nstreams` streams (double-buffered workspaces);
     # each call is still one whole pass of the hot path over its batch.  At N>1 the result gathers stay on
     # one stream of their own, in step order (one communicator is never driven from two streams at once).
-    nstreams = max(1, args.streams) if not (anon or trace) and (world == 1 or not (vec or wtd)) else 1
+    nstreams = max(1, args.streams) if not (anon or trace or c4) and (world == 1 or not (vec or wtd)) else 1
     wss = [ws] + [nsg.Workspace(n, WINDOW, dev) for _ in range(nstreams - 1)]
     vbufs = [vbuf] + ([nsg.window_vectors(ring[0], WINDOW, out=outs[1], workspace=wss[1]) for _ in range(nstreams - 1)]
                       if vec else [None] * (nstreams - 1))
@@ -321,7 +386,7 @@ def main():
             if gstream is not None:
                 gstream.wait_stream(s_i)
                 with torch.cuda.stream(gstream):
-                    gather_window_stats(r, WINDOWS_PER_STEP * world)
+                    gather_window_stats(r, total_windows)
             return r
         if anon:  # events around the whole call (bitmap reset + mark + rank prefix + relabel)
             if evs:
@@ -361,7 +426,7 @@ def main():
         else:
             r = nsg.window_stats_packed(ring[i % ring_n], WINDOW, out=outs[i % RING], workspace=ws, kernel_events=evs)
         if world > 1:
-            gather_window_stats(r, WINDOWS_PER_STEP * world)
+            gather_window_stats(r, total_windows)
         return r
 
     for i in range(args.warmup):
@@ -404,14 +469,17 @@ def main():
         tt = torch.tensor([t_ms, k_avg], dtype=torch.float64, device=coll_dev)
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
         t_ms, k_avg = float(tt[0]), float(tt[1])
-    total_pkts = n * world * args.steps
+    pkts_per_step = C4_PACKETS if c4 else n * world
+    total_pkts = pkts_per_step * args.steps
     value = total_pkts / (t_ms / 1e3)
+    value_no_gather = pkts_per_step / (k_avg / 1e3)  # kernels only (per-step CUDA events, max over ranks)
+    last_rows = outs[(args.steps - 1) % RING].cpu().numpy()
 
     # ---- e2e: the public API from pinned host buffers (H2D of the keys + D2H of the result inside)
     host = ring[0].cpu().pin_memory()
     keys_dev = torch.empty(n, dtype=torch.int64, device=dev)
-    out_host = torch.empty((WINDOWS_PER_STEP, 9), dtype=torch.int64, pin_memory=True)
-    e2e_steps = max(3, min(args.steps, 50))
+    out_host = torch.empty((wps, 9), dtype=torch.int64, pin_memory=True)
+    e2e_steps = 3 if c4 else max(3, min(args.steps, 50))
     if vec:  # H2D of the keys, the call, D2H of the statistics and every vector array
         vhost = {k: torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for k, t in vbuf.items() if k != "stats"}
 
@@ -453,7 +521,9 @@ def main():
         def e2e_once():
             nsg.window_stats_from_host(host, WINDOW, device=dev, keys_dev=keys_dev, out=outs[0], out_host=out_host,
                                        workspace=ws)
-        d2h_bytes = WINDOWS_PER_STEP * 9 * 8
+            if world > 1:
+                gather_window_stats(outs[0], total_windows)
+        d2h_bytes = wps * 9 * 8
     for _ in range(2):
         e2e_once()
     if world > 1:
@@ -474,7 +544,7 @@ def main():
 
     if rank == 0:
         peak, peak_src = peaks()
-        alg_bytes = n * (BYTES_PER_PACKET + (4 if wtd else 0)) + WINDOWS_PER_STEP * BYTES_PER_WINDOW_OUT
+        alg_bytes = n * (BYTES_PER_PACKET + (4 if wtd else 0)) + wps * BYTES_PER_WINDOW_OUT
         if vec:  # + the vectors written: 12 B per link / source / destination, 32 B of IP sets per window
             cnt = outs[0][:, [1, 3, 6]].sum().item()
             alg_bytes += 12 * cnt + 32 * WINDOWS_PER_STEP
@@ -487,11 +557,21 @@ def main():
             alg_bytes += n * 8
         if world == 1 and not args.no_cpu_baseline and not (trace or anon):
             cpu = cpu_baseline(dist_, seed)
+        spot = None
+        if not (trace or anon or wtd):
+            spot = spot_check(dist_, seed, last_rows, first_packet(args.steps - 1), sorted({0, wps // 2, wps - 1}))
+        suffix = "-vectors" if vec else "-weighted" if wtd else "-trace" if trace else "-anonymize" if anon else ""
+        traffic, traffic_src = traffic_per_launch(args.workload + suffix)
+        if c4:
+            per_gpu = f"{wps} windows x 2^17 packets on this rank (C4 split over {world} ranks)"
+        else:
+            per_gpu = f"{WINDOWS_PER_STEP} windows x 2^17 packets per GPU per step (C2 batch)"
         line = {
             "metric": METRIC, "value": value, "unit": "rows/s" if wtd else UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if c4 else "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": desc + f"; {WINDOWS_PER_STEP} windows x 2^17 packets per GPU per step (C2 batch)"
+            "config": {"workload": desc + "; " + per_gpu
                        + ("; outputs: stats + link/source/destination vectors + IP sets" if vec else "")
                        + ("; weighted rows (src, dst, n_packets ~ U[1,8]), unit rows/s" if wtd else "")
                        + ("; WHOLE-TRACE statistics of each step's packets (all ranks' packets together)"
@@ -500,28 +580,37 @@ def main():
                           "8 B/packet written" if anon else ""),
                        "window": WINDOW, "packets_per_gpu_per_step": n, "parallelism": f"windows sharded dp{world}",
                        "l2": (f"inputs larger than L2: ring of {RING} x {n * 8 >> 20} MiB batches per GPU, no flush"
-                              if ring_n > 1 else f"L2-warm: one {n * 8 >> 20} MiB batch reused every step"),
+                              if ring_n > 1 else
+                              f"inputs larger than L2: one resident {n * 8 >> 20} MiB block per GPU, no flush" if c4
+                              else f"L2-warm: one {n * 8 >> 20} MiB batch reused every step"),
                        "input": "device-resident packed u64 keys (src<<32|dst)",
+                       "gather": (f"NCCL all_gather_into_tensor of the [{total_windows}, 9] rows inside the timed region"
+                                  if world > 1 else "none (N=1)"),
                        "streams": nstreams},
+            "value_without_gather": value_no_gather if world > 1 else None,
             "e2e": {"value": e2e_value, "unit": "rows/s" if wtd else UNIT, "h2d_bytes_per_step": n * (12 if wtd else 8),
                     "d2h_bytes_per_step": d2h_bytes, "steps": e2e_steps},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "frac_vs_nominal_8000": achieved / 8000.0,
-                         "traffic": traffic_per_launch(args.workload + ("-vectors" if vec else "-weighted" if wtd else "-trace" if trace else "-anonymize" if anon else "")), "peak_source": peak_src,
+                         "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                          "kernel": ("nsg::anon_* (512 MiB bitmap; events around the whole call)" if anon else
                                     "nsg::trace_* (HBM tables; events around the whole call)" if trace else
-                                    "nsg::fast_kernel" + (" (+ reset and overflow-check launches: events around "
-                                                          "the whole call)" if (vec or wtd) else "")),
+                                    "nsg::fast_kernel (round-1 kernel; + reset and overflow-check launches: events "
+                                    "around the whole call)" if (vec or wtd) else
+                                    "nsg::flat::part_kernel + link_kernel + side_kernel: every launch of one call "
+                                    "(CUDA events around the whole kernel sequence, excluding the workspace reset)"),
                          "kernel_ms_avg": per_launch_ms,
                          "launch_ms_avg_measured": k_avg,
-                         "timing": ("time per launch = step time: consecutive launches overlap on "
-                                    f"{nstreams} streams" if nstreams > 1 else "CUDA events around each launch"),
+                         "timing": ("time per call = step time: consecutive calls overlap on "
+                                    f"{nstreams} streams" if nstreams > 1 else "CUDA events around each call's kernels"),
                          "algorithmic_bytes_per_launch": alg_bytes},
             "cpu_baseline": cpu,
+            "spot_check": spot,
             "clocks": clocks,
             "gpu_launches": launches * args.steps,
             "wall_s_timed_region": wall,
             "diag": diag,
+            "build_id": __import__("paper_2509_03653_b200._lib", fromlist=["build_id"]).build_id(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:

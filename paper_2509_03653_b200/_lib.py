@@ -67,6 +67,18 @@ STATUS = {
 }
 
 
+def build_id() -> str:
+    """Content hash of what libnsg.so is built from (sources, headers, nvcc flags): names the build that a
+    committed measurement (e.g. profiles/ncu_traffic.json) belongs to."""
+    import hashlib
+
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for p in SOURCES + [HEADER, INTERNAL_HEADER]:
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def build_libnsg(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
     """nvcc -gencode arch=compute_100a,code=sm_100a ... -> paper_2509_03653_b200/libnsg.so
     (debug=True: libnsg_debug.so, the same sources with -DNSG_DEBUG_CHECKS)."""

@@ -39,7 +39,10 @@ constexpr size_t DIAG_OFFSET = 64;
 constexpr size_t PROF_OFFSET = 128;  // u64[16], NSG_FLAG_PROFILE
 constexpr size_t CTRL_BYTES = 4096;  // ticket, diag (64), prof u64[256] (128)
 constexpr u64 GLOBAL_BUDGET = 2ull << 30;  // cap on L2-path table memory
-constexpr u64 FLAT_BATCH = 64;             // windows per batch of the round-2 kernels (scratch ~2.5 MB per window)
+#ifndef NSG_FLAT_BATCH
+#define NSG_FLAT_BATCH 64
+#endif
+constexpr u64 FLAT_BATCH = NSG_FLAT_BATCH;  // windows per batch of the round-2 kernels (scratch ~3.6 MB per window)
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 static u64 next_pow2(u64 x) { u64 p = 1; while (p < x) p <<= 1; return p; }
