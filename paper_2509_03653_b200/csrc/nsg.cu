@@ -16,6 +16,9 @@
 //                    in steps a multi-GPU driver interleaves with all-to-all exchanges.
 // This file holds the C ABI: argument checks, workspace layout, launches.
 #include <algorithm>
+#include <mutex>
+#include <utility>
+#include <vector>
 #include <cuda.h>  // driver types for cuStreamWriteValue32 (resolved at run time: no libcuda link)
 #include "nsg_internal.h"
 #include "nsg_common.cuh"
@@ -40,7 +43,7 @@ constexpr size_t PROF_OFFSET = 128;  // u64[16], NSG_FLAG_PROFILE
 constexpr size_t CTRL_BYTES = 4096;  // ticket, diag (64), prof u64[256] (128)
 constexpr u64 GLOBAL_BUDGET = 2ull << 30;  // cap on L2-path table memory
 #ifndef NSG_FLAT_BATCH
-#define NSG_FLAT_BATCH 64
+#define NSG_FLAT_BATCH 32
 #endif
 constexpr u64 FLAT_BATCH = NSG_FLAT_BATCH;  // windows per batch of the round-2 kernels (scratch ~3.6 MB per window)
 
@@ -58,7 +61,7 @@ struct Layout {
   // round-2 per-window kernels (nsg_flat.cuh), overlaid on the fast-path scratch
   bool flat;
   u32 flogB, fB, flogBs, fBs, fCP, fNB;  // fNB: windows per batch
-  size_t o_fws, o_fkscr, o_fkoff, o_frscr, o_froff;
+  size_t o_fws, o_fkscr, o_fkoff, o_frscr, o_froff, o_fend;
   // global
   u64 LC;
   u32 G;
@@ -118,6 +121,7 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     L.o_fkoff = q; q = align256(q + (size_t)L.fNB * L.fCP * L.fB * sizeof(u32));
     L.o_frscr = q; q = align256(q + (size_t)L.fNB * L.fB * flat::RCAP * sizeof(u64));
     L.o_froff = q; q = align256(q + (size_t)L.fNB * L.fB * 2 * L.fBs * sizeof(u32));
+    L.o_fend = q;
     if (q > o) o = q;
   }
   // L2-path table sets: the full path for large windows, the overflow hand-off otherwise.
@@ -212,6 +216,32 @@ static WriteValue32Fn write_value32() {
       fn = reinterpret_cast<WriteValue32Fn>(p);
   }
   return fn;
+}
+
+// Side stream and events of the round-2 batch pipeline, one set per caller stream (created on first use,
+// kept for the process; calls on one caller stream are ordered, so they can share it).
+struct Aux {
+  cudaStream_t a;
+  cudaEvent_t part_done, link_done, copied;
+};
+static Aux* aux_for(cudaStream_t s) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<int, cudaStream_t>, Aux*>> tab;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : tab)
+    if (e.first.first == dev && e.first.second == s) return e.second;
+  Aux* x = new Aux();
+  if (cudaStreamCreateWithFlags(&x->a, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x->part_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x->link_done, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x->copied, cudaEventDisableTiming) != cudaSuccess) {
+    delete x;
+    return nullptr;
+  }
+  tab.push_back({{dev, s}, x});
+  return x;
 }
 
 static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 n, u64 W, u64* out, void* ws,
@@ -323,24 +353,38 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
     g.inject = ((flags & NSG_FLAG_INJECT_OVERFLOW) ? 1u : 0u) | ((flags & NSG_FLAG_INJECT_SELF_CHECK) ? 2u : 0u);
     if (cudaMemsetAsync(base + L.o_fws, 0, (size_t)L.nw * sizeof(flat::WinState), s) != cudaSuccess) return NSG_ERR_CUDA;
     if (ev_before && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_before), s) != cudaSuccess) return NSG_ERR_CUDA;
+    // Batches pipeline over two streams: part(i) runs on the side stream `a` as soon as link(i-1) has read
+    // the key scratch (so it overlaps side(i-1)); link(i) waits for part(i) and follows side(i-1) on `s`
+    // (the record scratch).  One scratch set of FLAT_BATCH windows stays L2-resident.
+    Aux* ax = aux_for(s);
+    if (!ax) return NSG_ERR_CUDA;
+    if (cudaEventRecord(ax->link_done, s) != cudaSuccess) return NSG_ERR_CUDA;  // the reset above
     for (u64 w0 = 0; w0 < L.nw; w0 += L.fNB) {
       g.w0 = w0;
       g.nbw = (u32)(L.nw - w0 < (u64)L.fNB ? L.nw - w0 : (u64)L.fNB);
+      if (cudaStreamWaitEvent(ax->a, ax->link_done, 0) != cudaSuccess) return NSG_ERR_CUDA;
       if (sin) {  // this batch's keys arrive on the copy stream
         const u64 p0 = w0 * W, p1 = (w0 + g.nbw) * W < n ? (w0 + g.nbw) * W : n;
-        cudaEvent_t ev = nullptr;
-        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return NSG_ERR_CUDA;
         const bool ok = cudaMemcpyAsync(const_cast<u64*>(keys) + p0, sin->host + p0, (p1 - p0) * sizeof(u64),
                                         cudaMemcpyHostToDevice, sin->cs) == cudaSuccess &&
-                        cudaEventRecord(ev, sin->cs) == cudaSuccess && cudaStreamWaitEvent(s, ev, 0) == cudaSuccess;
-        cudaEventDestroy(ev);
+                        cudaEventRecord(ax->copied, sin->cs) == cudaSuccess &&
+                        cudaStreamWaitEvent(ax->a, ax->copied, 0) == cudaSuccess;
         if (!ok) return NSG_ERR_CUDA;
       }
-      flat::part_kernel<<<g.nbw * g.CP, flat::PTH, sizeof(flat::SmemP), s>>>(g, src, dst, keys);
+      flat::part_kernel<<<g.nbw * g.CP, flat::PTH, sizeof(flat::SmemP), ax->a>>>(g, src, dst, keys);
+      if (cudaEventRecord(ax->part_done, ax->a) != cudaSuccess || cudaStreamWaitEvent(s, ax->part_done, 0) != cudaSuccess)
+        return NSG_ERR_CUDA;
       flat::link_kernel<<<g.nbw * g.B, flat::LTH, sizeof(flat::SmemL), s>>>(g);
+      if (cudaEventRecord(ax->link_done, s) != cudaSuccess) return NSG_ERR_CUDA;
       flat::side_kernel<<<g.nbw * 2 * g.Bs, flat::STH, sizeof(flat::SmemS), s>>>(g, out);
       g_last_launches += 3;
       if (cudaGetLastError() != cudaSuccess) return NSG_ERR_CUDA;
+    }
+    {  // the scratch is dead: drop it from L2 (no write-back of dirty scratch lines to HBM)
+      const u64 bytes = (u64)(L.o_fend - L.o_fkscr);
+      const u32 blocks = (u32)std::min<u64>((bytes / 128 + 255) / 256, (u64)4 * 148);
+      flat::discard_kernel<<<blocks, 256, 0, s>>>(base + L.o_fkscr, bytes);
+      g_last_launches++;
     }
     if (ev_after && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_after), s) != cudaSuccess) return NSG_ERR_CUDA;
     if (ev_copied && cudaStreamWaitEvent(s, ev_copied, 0) != cudaSuccess) return NSG_ERR_CUDA;

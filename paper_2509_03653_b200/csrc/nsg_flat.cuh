@@ -32,21 +32,22 @@ namespace flat {
 constexpr int CH = 4096;                      // keys per partition item
 constexpr int PTH = 256;                      // partition CTA threads
 constexpr int LTH = 256;                      // link CTA threads
-constexpr int STH = 128;                      // side CTA threads
+constexpr int STH = 256;                      // side CTA threads
 constexpr u64 BK = 1024;                      // target keys per link bucket / nodes per side bucket
 constexpr u64 MAX_W = 1ull << 17;             // windows this path takes (<= 128 link / side buckets)
 constexpr int MAXB = 256;
 constexpr int LOG_TL = 11, TL = 1 << LOG_TL;  // link-table slots (load <= 5/8)
 constexpr int LOG_TS = 11, TS = 1 << LOG_TS;  // node-table slots
 constexpr u32 FILL_L = 1280, FILL_S = 1280;   // distinct entries before the window goes to the L2 path
-constexpr u32 RCAP = 2 * (FILL_L + 1);        // records per link bucket (both sides)
+constexpr u32 RCAP = (2 * (FILL_L + 1) + 15) & ~15u;  // records per link bucket (both sides), whole lines
 constexpr int PFS = 20;                       // node packets: 20-bit field (W < 2^20)
 constexpr u32 PMASK = (1u << PFS) - 1;
 constexpr u32 FMAX = 0xFFFu;                  // fan field: 12 bits; items with >= 4096 records track wraps
 constexpr int WRAPCAP = 64;
+constexpr u32 HEAVY_S = 2048;                 // side items with more records aggregate per node per warp step
 constexpr u64 MUL_L = 0x9E3779B97F4A7C15ull;  // link hash: top bits of key * phi64
 constexpr u32 MUL_N = 0x9E3779B9u;            // node hash: top bits of node * phi32
-static_assert(RCAP % 2 == 0, "record regions stay 16-B aligned");
+static_assert((RCAP * 8) % 128 == 0, "record rows are whole 128-B lines (16-B stores, L2 discards)");
 
 // Per-window state (64 B), zeroed by the host before the launches.
 struct WinState {
@@ -89,14 +90,21 @@ __device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-__device__ __forceinline__ u64 ld_stream64(const u64* p) {
+// Input keys are read once: loaded with an L2 evict-first policy so that the stream does not push the
+// (dirty, L2-resident) scratch of the batch pipeline out to HBM.
+__device__ __forceinline__ u64 l2_evict_first() {
+  u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ u64 ld_stream64(const u64* p, u64 pol) {
   u64 v;
-  asm volatile("ld.global.cs.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
   return v;
 }
-__device__ __forceinline__ ulonglong2 ld_stream128(const u64* p) {
+__device__ __forceinline__ ulonglong2 ld_stream128(const u64* p, u64 pol) {
   ulonglong2 v;
-  asm volatile("ld.global.cs.v2.u64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p));
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;" : "=l"(v.x), "=l"(v.y) : "l"(p), "l"(pol));
   return v;
 }
 
@@ -244,6 +252,7 @@ part_kernel(const FGeo g, const u32* __restrict__ src, const u32* __restrict__ d
   for (u32 i = t; i < B; i += PTH) s.hist[i] = 0;
   constexpr int KPT = CH / PTH;
   u64 kk[KPT];
+  const u64 pol = l2_evict_first();
   if (keys) {
     const u64* p = keys + base;
     if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
@@ -251,10 +260,10 @@ part_kernel(const FGeo g, const u32* __restrict__ src, const u32* __restrict__ d
       for (int i = 0; i < KPT / 2; ++i) {
         const u32 e = 2 * (i * PTH + t);
         if (e + 1 < n) {
-          const ulonglong2 v = ld_stream128(p + e);
+          const ulonglong2 v = ld_stream128(p + e, pol);
           kk[2 * i] = v.x; kk[2 * i + 1] = v.y;
         } else {
-          kk[2 * i] = e < n ? ld_stream64(p + e) : 0ull;
+          kk[2 * i] = e < n ? ld_stream64(p + e, pol) : 0ull;
           kk[2 * i + 1] = 0ull;
         }
       }
@@ -262,8 +271,8 @@ part_kernel(const FGeo g, const u32* __restrict__ src, const u32* __restrict__ d
 #pragma unroll
       for (int i = 0; i < KPT / 2; ++i) {
         const u32 e = 2 * (i * PTH + t);
-        kk[2 * i] = e < n ? ld_stream64(p + e) : 0ull;
-        kk[2 * i + 1] = e + 1 < n ? ld_stream64(p + e + 1) : 0ull;
+        kk[2 * i] = e < n ? ld_stream64(p + e, pol) : 0ull;
+        kk[2 * i + 1] = e + 1 < n ? ld_stream64(p + e + 1, pol) : 0ull;
       }
     }
   } else {
@@ -369,12 +378,19 @@ link_kernel(const FGeo g) {
   __syncthreads();  // table initialised
   {
     u32 nesc = 0;
-    for (u32 e0 = 0; e0 < ws.n; e0 += 64) {
+    // the next step's keys are loaded while this step's are inserted (L2 latency off the chain)
+    u64 nxa = EMPTY64, nxc = EMPTY64;
+    auto fetch = [&](u32 e0) {
       u32 oa, ob;
       warp_seg_step(ws, e0, oa, ob);
+      nxa = e0 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(kb + oa)) : EMPTY64;
+      nxc = e0 + 32 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(kb + ob)) : EMPTY64;
+    };
+    if (ws.n) fetch(0);
+    for (u32 e0 = 0; e0 < ws.n; e0 += 64) {
       const bool va = e0 + lane < ws.n, vb = e0 + 32 + lane < ws.n;
-      const u64 ka = va ? __ldcg(reinterpret_cast<const unsigned long long*>(kb + oa)) : EMPTY64;
-      const u64 kc = vb ? __ldcg(reinterpret_cast<const unsigned long long*>(kb + ob)) : EMPTY64;
+      const u64 ka = nxa, kc = nxc;
+      if (e0 + 64 < ws.n) fetch(e0 + 64);
       if (*reinterpret_cast<volatile u32*>(&s.ovf)) break;
       const bool aa = ka != EMPTY64, ab = kc != EMPTY64;  // the key ~0 is counted apart
       nesc += (va && !aa) + (vb && !ab);
@@ -515,6 +531,24 @@ __device__ __forceinline__ void node_add(SmemS& s, u32 slot, u32 c, bool wrapche
   }
 }
 
+// node_add for the records of a warp step that share a node (same slot): one aggregated add by the
+// group's first lane (packets summed, fan += group size).  Used for heavy side items (a heavy hitter
+// sends thousands of records to one slot; lane-by-lane adds to one address would serialise).
+// Must be called by the whole warp.
+__device__ __forceinline__ void node_add_warp(SmemS& s, u32 slot, u32 c, bool active, bool wrapcheck) {
+  const u32 m = __match_any_sync(0xffffffffu, active ? slot : 0xFFFFFFFFu);
+  if (!active) return;
+  const u32 sum = __reduce_add_sync(m, c);
+  if ((threadIdx.x & 31) != (u32)(__ffs(m) - 1)) return;
+  const u32 k = __popc(m);  // <= 32: the 12-bit fan field wraps at most once per add
+  const u32 o = atomicAdd(&s.npf[slot], sum | (k << PFS));
+  if (wrapcheck && (o >> PFS) + k > FMAX) {
+    const u32 i = atomicAdd(&s.nwrap, 1u);
+    if (i < (u32)WRAPCAP) s.wrap[i] = slot;
+    else s.ovf = 1;
+  }
+}
+
 __device__ void finalize(const FGeo& g, u64 w, u64* out) {
   WinState* st = &g.ws[w];
   u32 ovf = ldcg32(&st->ovf);
@@ -539,7 +573,7 @@ __device__ void finalize(const FGeo& g, u64 w, u64* out) {
   for (u32 m = 0; m < g.n_mirror; ++m) store_row(g.mirror[m] + (g.mirror_row0 + w) * NSG_NUM_STATS, row);
 }
 
-__global__ void __launch_bounds__(STH, 12)
+__global__ void __launch_bounds__(STH, 6)
 side_kernel(const FGeo g, u64* __restrict__ out) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemS& s = *reinterpret_cast<SmemS*>(smem_raw);
@@ -561,15 +595,22 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
 #pragma unroll
   for (u32 i = 0; i < NW; ++i) ntot += s.red[0][i];
   const bool wrapcheck = ntot > FMAX;
+  const bool heavy = ntot > HEAVY_S;
   const u64* rb = g.rscr + (u64)wb * B * RCAP;
   {
     u32 escP = 0, escF = 0;
-    for (u32 e0 = 0; e0 < ws.n; e0 += 64) {
+    u64 nxa = ~0ull, nxc = ~0ull;  // the next step's records, loaded while this step's are merged
+    auto fetch = [&](u32 e0) {
       u32 oa, ob;
       warp_seg_step(ws, e0, oa, ob);
+      nxa = e0 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(rb + oa)) : ~0ull;
+      nxc = e0 + 32 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(rb + ob)) : ~0ull;
+    };
+    if (ws.n) fetch(0);
+    for (u32 e0 = 0; e0 < ws.n; e0 += 64) {
       const bool va = e0 + lane < ws.n, vb = e0 + 32 + lane < ws.n;
-      const u64 ra = va ? __ldcg(reinterpret_cast<const unsigned long long*>(rb + oa)) : ~0ull;
-      const u64 rc = vb ? __ldcg(reinterpret_cast<const unsigned long long*>(rb + ob)) : ~0ull;
+      const u64 ra = nxa, rc = nxc;
+      if (e0 + 64 < ws.n) fetch(e0 + 64);
       if (*reinterpret_cast<volatile u32*>(&s.ovf)) break;
       const u32 na = (u32)(ra >> 32), nb = (u32)(rc >> 32);
       u32 sa = node_slot(na, logBs), sb = node_slot(nb, logBs);
@@ -579,8 +620,13 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
       if (va && !aa) { escP += (u32)ra; ++escF; }
       if (vb && !ab) { escP += (u32)rc; ++escF; }
       probe2<u32>(s.nkey, TS - 1, na, nb, sa, sb, ca, cb, aa, ab, &s.ovf, [](u32 k) { return node_step(k); });
-      if (aa) node_add(s, sa, (u32)ra, wrapcheck);
-      if (ab) node_add(s, sb, (u32)rc, wrapcheck);
+      if (heavy) {  // a heavy hitter's records: one add per node per warp step
+        node_add_warp(s, sa, (u32)ra, aa, wrapcheck);
+        node_add_warp(s, sb, (u32)rc, ab, wrapcheck);
+      } else {
+        if (aa) node_add(s, sa, (u32)ra, wrapcheck);
+        if (ab) node_add(s, sb, (u32)rc, wrapcheck);
+      }
     }
     escF = __reduce_add_sync(0xffffffffu, escF);
     escP = __reduce_add_sync(0xffffffffu, escP);
@@ -636,6 +682,14 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
       }
     }
   }
+}
+
+// After a call's last batch: its scratch (keys, records, descriptors) is dead; drop it from L2 so that the
+// dirty lines are never written back to HBM (the earlier batches' scratch was overwritten in L2).
+__global__ void __launch_bounds__(256)
+discard_kernel(const unsigned char* base, u64 bytes) {
+  for (u64 i = (u64)blockIdx.x * 256 + threadIdx.x; i < bytes / 128; i += (u64)gridDim.x * 256)
+    discard_l2_line(base + i * 128);
 }
 
 }  // namespace flat

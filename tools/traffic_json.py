@@ -26,8 +26,8 @@ for arg in sys.argv[1:]:
             d = launches.setdefault(int(x["ID"]), {"kernel": x["Kernel Name"].split("(")[0]})
             d[x["Metric Name"]] = float(x["Metric Value"].replace(",", ""))
     seq = [launches[k] for k in sorted(launches)]
-    # one call of C2 = one batch: part, link, side (LAUNCHES_PER_CALL for other batchings)
-    per_call = int(os.environ.get("LAUNCHES_PER_CALL", "3"))
+    # one call of C2 = two 32-window batches (part, link, side) + the scratch discard (LAUNCHES_PER_CALL otherwise)
+    per_call = int(os.environ.get("LAUNCHES_PER_CALL", "7"))
     calls = [seq[i:i + per_call] for i in range(0, len(seq) - per_call + 1, per_call)]
     tail = calls[len(calls) // 2:]
 
