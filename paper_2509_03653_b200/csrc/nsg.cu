@@ -112,8 +112,8 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     const u64 want = (W + flat::BK - 1) / flat::BK;
     L.fB = (u32)next_pow2(want < 1 ? 1 : want);
     L.flogB = ilog2(L.fB);
-    L.fBs = L.fB;
-    L.flogBs = L.flogB;
+    L.fBs = L.fB > 1 ? L.fB / 2 : 1;  // side buckets: ~2x the records of a link bucket per item
+    L.flogBs = L.flogB > 0 ? L.flogB - 1 : 0;
     L.fCP = (u32)((W + flat::CH - 1) / flat::CH);
     L.fNB = (u32)(L.nw < (u64)FLAT_BATCH ? L.nw : (u64)FLAT_BATCH);
     L.o_fws = q; q = align256(q + (size_t)L.nw * sizeof(flat::WinState));

@@ -37,14 +37,14 @@ constexpr u64 BK = 1024;                      // target keys per link bucket / n
 constexpr u64 MAX_W = 1ull << 17;             // windows this path takes (<= 128 link / side buckets)
 constexpr int MAXB = 256;
 constexpr int LOG_TL = 11, TL = 1 << LOG_TL;  // link-table slots (load <= 5/8)
-constexpr int LOG_TS = 11, TS = 1 << LOG_TS;  // node-table slots
+constexpr int LOG_TS = 12, TS = 1 << LOG_TS;  // node-table slots
 constexpr u32 FILL_L = 1280, FILL_S = 1280;   // distinct entries before the window goes to the L2 path
 constexpr u32 RCAP = (2 * (FILL_L + 1) + 15) & ~15u;  // records per link bucket (both sides), whole lines
 constexpr int PFS = 20;                       // node packets: 20-bit field (W < 2^20)
 constexpr u32 PMASK = (1u << PFS) - 1;
 constexpr u32 FMAX = 0xFFFu;                  // fan field: 12 bits; items with >= 4096 records track wraps
 constexpr int WRAPCAP = 64;
-constexpr u32 HEAVY_S = 2048;                 // side items with more records aggregate per node per warp step
+constexpr u32 HEAVY_S = 8192;                 // side items with more records aggregate per node per warp step
 constexpr u64 MUL_L = 0x9E3779B97F4A7C15ull;  // link hash: top bits of key * phi64
 constexpr u32 MUL_N = 0x9E3779B9u;            // node hash: top bits of node * phi32
 static_assert((RCAP * 8) % 128 == 0, "record rows are whole 128-B lines (16-B stores, L2 discards)");
