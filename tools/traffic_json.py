@@ -13,7 +13,8 @@ from paper_2509_03653_b200 import _lib  # noqa: E402
 
 out_path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
 res = json.load(open(out_path)) if os.path.exists(out_path) else {}
-for arg in sys.argv[1:]:
+print_only = "--print-only" in sys.argv
+for arg in [a for a in sys.argv[1:] if a != "--print-only"]:
     name, path = arg.split("=", 1)
     rows = list(csv.reader(open(path)))
     hdr, launches = None, {}
@@ -51,4 +52,5 @@ for arg in sys.argv[1:]:
                  "build_id": _lib.build_id(),
                  "source": f"ncu --cache-control none --clock-control none, {len(calls)} calls of tools/traffic_case.py"}
     print(name, json.dumps(res[name]))
-json.dump(res, open(out_path, "w"), indent=1)
+if not print_only:
+    json.dump(res, open(out_path, "w"), indent=1)
