@@ -237,7 +237,7 @@ struct SmemP {
   u32 hist[MAXB], offs[MAXB];
 };
 
-__global__ void __launch_bounds__(PTH, 4)
+__global__ void __launch_bounds__(PTH, 3)
 part_kernel(const FGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, const u64* __restrict__ keys) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemP& s = *reinterpret_cast<SmemP*>(smem_raw);
