@@ -44,7 +44,7 @@ constexpr int PFS = 20;                       // node packets: 20-bit field (W <
 constexpr u32 PMASK = (1u << PFS) - 1;
 constexpr u32 FMAX = 0xFFFu;                  // fan field: 12 bits; items with >= 4096 records track wraps
 constexpr int WRAPCAP = 64;
-constexpr u32 HEAVY_S = 8192;                 // side items with more records aggregate per node per warp step
+constexpr u32 HEAVY_S = 8192;                 // side items with more records cache a hot node per warp
 constexpr u64 MUL_L = 0x9E3779B97F4A7C15ull;  // link hash: top bits of key * phi64
 constexpr u32 MUL_N = 0x9E3779B9u;            // node hash: top bits of node * phi32
 static_assert((RCAP * 8) % 128 == 0, "record rows are whole 128-B lines (16-B stores, L2 discards)");
@@ -531,21 +531,31 @@ __device__ __forceinline__ void node_add(SmemS& s, u32 slot, u32 c, bool wrapche
   }
 }
 
-// node_add for the records of a warp step that share a node (same slot): one aggregated add by the
-// group's first lane (packets summed, fan += group size).  Used for heavy side items (a heavy hitter
-// sends thousands of records to one slot; lane-by-lane adds to one address would serialise).
-// Must be called by the whole warp.
-__device__ __forceinline__ void node_add_warp(SmemS& s, u32 slot, u32 c, bool active, bool wrapcheck) {
-  const u32 m = __match_any_sync(0xffffffffu, active ? slot : 0xFFFFFFFFu);
-  if (!active) return;
-  const u32 sum = __reduce_add_sync(m, c);
-  if ((threadIdx.x & 31) != (u32)(__ffs(m) - 1)) return;
-  const u32 k = __popc(m);  // <= 32: the 12-bit fan field wraps at most once per add
-  const u32 o = atomicAdd(&s.npf[slot], sum | (k << PFS));
-  if (wrapcheck && (o >> PFS) + k > FMAX) {
-    const u32 i = atomicAdd(&s.nwrap, 1u);
-    if (i < (u32)WRAPCAP) s.wrap[i] = slot;
-    else s.ovf = 1;
+// One lane merges a cached node's totals (packets P, fan F, F possibly > 4095) into the table: probe to
+// its slot, then add in steps of at most 4095 fan so that every wrap of the 12-bit field is recorded.
+__device__ __noinline__ void node_merge(SmemS& s, u32 node, u32 P, u32 F, u32 logBs) {
+  u32 sl = node_slot(node, logBs);
+  const u32 stp = node_step(node);
+  for (u32 probe = 0;; ++probe) {
+    const u32 cur = *reinterpret_cast<volatile u32*>(&s.nkey[sl]);
+    if (cur == node) break;
+    if (cur == EMPTY32) {
+      const u32 o = atomicCAS(&s.nkey[sl], EMPTY32, node);
+      if (o == EMPTY32 || o == node) break;
+      continue;  // re-read this slot
+    }
+    if (probe >= (u32)TS) { s.ovf = 1; return; }
+    sl = (sl + stp) & (TS - 1);
+  }
+  for (bool first = true; F; first = false) {
+    const u32 a = min(F, FMAX);
+    const u32 o = atomicAdd(&s.npf[sl], (first ? P : 0u) | (a << PFS));
+    if ((o >> PFS) + a > FMAX) {
+      const u32 i = atomicAdd(&s.nwrap, 1u);
+      if (i < (u32)WRAPCAP) s.wrap[i] = sl;
+      else s.ovf = 1;
+    }
+    F -= a;
   }
 }
 
@@ -607,6 +617,10 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
       nxc = e0 + 32 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(rb + ob)) : ~0ull;
     };
     if (ws.n) fetch(0);
+    // A heavy item (a heavy hitter's bucket) caches one node per warp in lane registers: its records are
+    // summed there instead of in one contended table slot, and merged once at the end.
+    const u32 hot = heavy && ws.n ? __shfl_sync(0xffffffffu, (u32)(nxa >> 32), 0) : EMPTY32;
+    u32 hP = 0, hF = 0;
     for (u32 e0 = 0; e0 < ws.n; e0 += 64) {
       const bool va = e0 + lane < ws.n, vb = e0 + 32 + lane < ws.n;
       const u64 ra = nxa, rc = nxc;
@@ -614,20 +628,20 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
       if (*reinterpret_cast<volatile u32*>(&s.ovf)) break;
       const u32 na = (u32)(ra >> 32), nb = (u32)(rc >> 32);
       u32 sa = node_slot(na, logBs), sb = node_slot(nb, logBs);
-      const u32 ca = *reinterpret_cast<volatile u32*>(&s.nkey[sa]);
-      const u32 cb = *reinterpret_cast<volatile u32*>(&s.nkey[sb]);
-      const bool aa = na != EMPTY32, ab = nb != EMPTY32;  // the node ~0 is merged apart
+      bool aa = na != EMPTY32, ab = nb != EMPTY32;  // the node ~0 is merged apart
       if (va && !aa) { escP += (u32)ra; ++escF; }
       if (vb && !ab) { escP += (u32)rc; ++escF; }
+      if (aa && na == hot) { hP += (u32)ra; ++hF; aa = false; }
+      if (ab && nb == hot) { hP += (u32)rc; ++hF; ab = false; }
+      const u32 ca = aa ? *reinterpret_cast<volatile u32*>(&s.nkey[sa]) : 0u;
+      const u32 cb = ab ? *reinterpret_cast<volatile u32*>(&s.nkey[sb]) : 0u;
       probe2<u32>(s.nkey, TS - 1, na, nb, sa, sb, ca, cb, aa, ab, &s.ovf, [](u32 k) { return node_step(k); });
-      if (heavy) {  // a heavy hitter's records: one add per node per warp step
-        node_add_warp(s, sa, (u32)ra, aa, wrapcheck);
-        node_add_warp(s, sb, (u32)rc, ab, wrapcheck);
-      } else {
-        if (aa) node_add(s, sa, (u32)ra, wrapcheck);
-        if (ab) node_add(s, sb, (u32)rc, wrapcheck);
-      }
+      if (aa) node_add(s, sa, (u32)ra, wrapcheck);
+      if (ab) node_add(s, sb, (u32)rc, wrapcheck);
     }
+    hP = __reduce_add_sync(0xffffffffu, hP);
+    hF = __reduce_add_sync(0xffffffffu, hF);
+    if (lane == 0 && hF) node_merge(s, hot, hP, hF, logBs);
     escF = __reduce_add_sync(0xffffffffu, escF);
     escP = __reduce_add_sync(0xffffffffu, escP);
     if (lane == 0 && escF) { atomicAdd(&s.escP, escP); atomicAdd(&s.escF, escF); }
