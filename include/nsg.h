@@ -208,7 +208,9 @@ nsg_status nsg_window_vectors(const uint32_t* src, const uint32_t* dst, const ui
  * pointer is device memory, 8 B aligned; all calls are asynchronous on `stream`; the workspace (256 B
  * aligned, nsg_trace_workspace_bytes) may be reused by the next step once this one is enqueued (steps on
  * one stream are ordered).  Capacities: n <= key_capacity keys per links call, m <= record_capacity
- * records per nodes call, 1 <= world <= 1024; violations are NSG_ERR_INVALID_ARGUMENT. */
+ * records per nodes call, 1 <= world <= 1024, fewer than 2^32 keys per links call (per-link and per-node
+ * sums are 32-bit); violations are NSG_ERR_INVALID_ARGUMENT.  Weighted rows: the caller keeps the total
+ * n_packets of a trace below 2^32 (the sums are not checked for wrap-around). */
 size_t nsg_trace_workspace_bytes(uint64_t key_capacity, uint64_t record_capacity, uint32_t world);
 
 /* send_keys u64[n] (device): the keys grouped by owner rank, rank o's segment at the exclusive prefix
@@ -268,7 +270,8 @@ nsg_status nsg_trace_links_emit_peers(uint32_t world, uint64_t* const* peers_src
                                       void* stream);
 
 /* One GPU: the nine whole-trace statistics into out u64[9] (device), north_star column order; the steps
- * above with world = 1 and no host synchronisation.  Workspace: nsg_trace_stats_workspace_bytes(n). */
+ * above with world = 1 and no host synchronisation.  Workspace: nsg_trace_stats_workspace_bytes(n).
+ * n_packets >= 2^32 is NSG_ERR_INVALID_ARGUMENT (32-bit per-link / per-node sums). */
 size_t nsg_trace_stats_workspace_bytes(uint64_t n_packets);
 nsg_status nsg_trace_stats(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
                            uint64_t* out, void* workspace, size_t workspace_bytes, void* stream);

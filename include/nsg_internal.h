@@ -33,6 +33,11 @@ nsg_status nsg_window_stats_timed(const uint32_t* src, const uint32_t* dst, cons
                                   uint64_t window, uint64_t* out, void* workspace, size_t workspace_bytes,
                                   void* stream, uint32_t flags, void* ev_before, void* ev_after);
 
+/* Whole-trace tables of at least `slots` slots probe by CAS (the CAS returns the occupant) instead of a load
+ * first; 0 restores the default (2^26 slots: DRAM-resident tables).  Process-wide, for tests that run the
+ * CAS-as-probe inserts on small inputs; not thread safe against concurrent trace calls. */
+nsg_status nsg_debug_trace_cas_first_slots(uint64_t slots);
+
 #ifdef __cplusplus
 }
 #endif

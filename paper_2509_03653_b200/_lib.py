@@ -52,6 +52,7 @@ EXPORTS = (
     "nsg_anonymize_workspace_bytes",
     "nsg_anonymize",
     "nsg_diag_offset",
+    "nsg_debug_trace_cas_first_slots",
     "nsg_last_launches",
     "nsg_status_string",
     "nsg_version",
@@ -153,6 +154,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.nsg_anonymize_workspace_bytes.argtypes = []
     lib.nsg_anonymize.restype = ctypes.c_int
     lib.nsg_anonymize.argtypes = [vp, vp, vp, u64, u64, u32, vp, vp, vp, vp, sz, vp]
+    lib.nsg_debug_trace_cas_first_slots.restype = ctypes.c_int
+    lib.nsg_debug_trace_cas_first_slots.argtypes = [u64]
     lib.nsg_ipc_handle_bytes.restype = sz
     lib.nsg_ipc_handle_bytes.argtypes = []
     lib.nsg_ipc_alloc.restype = ctypes.c_int

@@ -750,7 +750,7 @@ nsg_status nsg_trace_links(const uint32_t* src, const uint32_t* dst, const uint6
                            void* workspace, size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity,
                            void* stream) {
   nsg::g_last_launches = 0;
-  if (n > key_capacity) return NSG_ERR_INVALID_ARGUMENT;
+  if (n > key_capacity || n >= (1ull << 32)) return NSG_ERR_INVALID_ARGUMENT;  // 32-bit link sums
   if (n && !nsg::input_ok(src, dst, reinterpret_cast<const nsg::u64*>(keys))) return NSG_ERR_INVALID_ARGUMENT;
   const void* p8[] = {link_stats, rec_src, rec_dst, rec_counts};
   for (const void* p : p8)
@@ -852,7 +852,7 @@ nsg_status nsg_trace_links_count(const uint32_t* src, const uint32_t* dst, const
                                  uint32_t world, uint64_t* link_stats, uint64_t* rec_counts, void* workspace,
                                  size_t workspace_bytes, uint64_t key_capacity, uint64_t record_capacity, void* stream) {
   nsg::g_last_launches = 0;
-  if (n > key_capacity) return NSG_ERR_INVALID_ARGUMENT;
+  if (n > key_capacity || n >= (1ull << 32)) return NSG_ERR_INVALID_ARGUMENT;  // 32-bit link sums
   if (n && !nsg::input_ok(src, dst, reinterpret_cast<const nsg::u64*>(keys))) return NSG_ERR_INVALID_ARGUMENT;
   if (!link_stats || !rec_counts || (reinterpret_cast<uintptr_t>(link_stats) & 7) ||
       (reinterpret_cast<uintptr_t>(rec_counts) & 7))
@@ -920,6 +920,7 @@ static nsg_status trace_stats_impl(const uint32_t* src, const uint32_t* dst, con
                                    size_t workspace_bytes, void* stream) {
   nsg::g_last_launches = 0;
   if (n_packets == 0) return NSG_OK;
+  if (n_packets >= (1ull << 32)) return NSG_ERR_INVALID_ARGUMENT;  // per-link / per-node sums are 32-bit
   if (!nsg::input_ok(src, dst, reinterpret_cast<const nsg::u64*>(keys))) return NSG_ERR_INVALID_ARGUMENT;
   if (!out || (reinterpret_cast<uintptr_t>(out) & 7)) return NSG_ERR_INVALID_ARGUMENT;
   if (workspace_bytes < nsg_trace_stats_workspace_bytes(n_packets)) return NSG_ERR_WORKSPACE_TOO_SMALL;
@@ -1014,6 +1015,11 @@ nsg_status nsg_window_vectors_weighted(const uint32_t* src, const uint32_t* dst,
 }
 
 size_t nsg_diag_offset(void) { return nsg::DIAG_OFFSET; }
+
+nsg_status nsg_debug_trace_cas_first_slots(uint64_t slots) {
+  const nsg::u64 v = slots ? slots : nsg::TRACE_CAS_FIRST_SLOTS;
+  return cudaMemcpyToSymbol(nsg::g_trace_cas_first_slots, &v, sizeof(v)) == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
+}
 
 unsigned nsg_last_launches(void) { return nsg::g_last_launches; }
 

@@ -18,6 +18,9 @@ namespace nsg {
 
 constexpr int TT = 512;          // threads per CTA of the trace kernels
 constexpr u64 TRACE_CAS_FIRST_SLOTS = 1ull << 26;  // tables this large live in DRAM: probe by CAS (tl_insert)
+// The threshold as the kernels read it (tests lower it to run the CAS-as-probe inserts on small inputs:
+// nsg_debug_trace_cas_first_slots in nsg_internal.h).
+__device__ u64 g_trace_cas_first_slots = TRACE_CAS_FIRST_SLOTS;
 constexpr int TRACE_MAX_WORLD = 1024;
 
 // owner rank of a link / of a node (independent of the table slots, which use the low bits)
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(TT) trace_link_insert(const u64* __restrict__ 
                                                         const u32* __restrict__ dst, u64 n, LSlot* __restrict__ lt,
                                                         u64 LC, u32* __restrict__ esc, const u32* __restrict__ wgt = nullptr) {
   // wgt: weighted rows (n_packets per row; 0 adds nothing), NULL for raw packets
-  const bool cas_first = LC >= TRACE_CAS_FIRST_SLOTS;
+  const bool cas_first = LC >= g_trace_cas_first_slots;
   __shared__ u64 ck[TCACHE];
   __shared__ u32 cc[TCACHE];
   for (int i = threadIdx.x; i < TCACHE; i += TT) { ck[i] = EMPTY64; cc[i] = 0; }
@@ -411,11 +414,11 @@ __device__ __forceinline__ void node_records(const u64* __restrict__ rec, u64 m,
       if (cur == EMPTY32) cur = node;
     }
     if (cur == node) { atomicAdd(&cp[cs], c); atomicAdd(&cf[cs], 1u); }
-    else tn_upsert(nt, NC, esc, node, c, 1u, NC >= TRACE_CAS_FIRST_SLOTS);
+    else tn_upsert(nt, NC, esc, node, c, 1u, NC >= g_trace_cas_first_slots);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < TCACHE; i += TT)
-    if (ck[i] != EMPTY32) tn_upsert(nt, NC, esc, ck[i], cp[i], cf[i], NC >= TRACE_CAS_FIRST_SLOTS);
+    if (ck[i] != EMPTY32) tn_upsert(nt, NC, esc, ck[i], cp[i], cf[i], NC >= g_trace_cas_first_slots);
 }
 static_assert(TCACHE == 4096, "node cache slot uses 12 hash bits");
 

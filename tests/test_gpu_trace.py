@@ -154,3 +154,43 @@ def test_trace_weighted(nsg, cuda_device, n):
     got = nsg.trace_stats(kd, n_packets=torch.from_numpy(wt.view(np.int32)).to(cuda_device))
     want = oracle.window_stats_weighted(keys=keys, weights=wt, window=n)[0]
     assert got.cpu().numpy().view(np.uint64).tolist() == want.tolist()
+
+
+@pytest.mark.parametrize("dist", ["zipf", "uniform"])
+def test_trace_cas_first_inserts_on_small_inputs(nsg, cuda_device, dist):
+    """The CAS-as-probe inserts (used for DRAM-resident tables of >= 2^26 slots) forced on for every table
+    size (nsg_debug_trace_cas_first_slots, include/nsg_internal.h), including the sentinel keys."""
+    from paper_2509_03653_b200 import api
+
+    d = gen.Dist("zipf", 1.1, 1 << 16) if dist == "zipf" else gen.Dist("uniform")
+    keys = gen.generate_host(d, 72, 0, 300_007, packed=True)
+    keys[::97] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    keys[5::101] = np.uint64(0xFFFFFFFF00000003)
+    kd = torch.from_numpy(keys.view(np.int64)).to(cuda_device)
+    assert api._lib.nsg_debug_trace_cas_first_slots(1) == 0
+    try:
+        got = nsg.trace_stats(kd).cpu().numpy().view(np.uint64).tolist()
+    finally:
+        assert api._lib.nsg_debug_trace_cas_first_slots(0) == 0
+    assert got == whole(keys)
+
+
+@pytest.mark.parametrize("dist", ["zipf", "uniform"])
+def test_trace_at_2_25_keys(nsg, cuda_device, dist):
+    """2^25 packets: link and node tables of >= 2^26 slots, where the CAS-as-probe inserts and the
+    device-sized node tables run by default; checked against O2 (window = n)."""
+    d = gen.Dist("zipf", 1.1, 1 << 20) if dist == "zipf" else gen.Dist("uniform")
+    n = 1 << 25
+    kd = torch.empty(n, dtype=torch.int64, device=cuda_device)
+    gen.generate_device(d, 73, 0, n, keys=kd)
+    got = nsg.trace_stats(kd).cpu().numpy().view(np.uint64).tolist()
+    assert got == whole(kd.cpu().numpy().view(np.uint64))
+
+
+def test_trace_rejects_2_32_packets(nsg, cuda_device):
+    from paper_2509_03653_b200 import api
+
+    kd = torch.zeros(8, dtype=torch.int64, device=cuda_device)
+    out = torch.empty(9, dtype=torch.int64, device=cuda_device)
+    rc = api._lib.nsg_trace_stats(None, None, kd.data_ptr(), 1 << 32, out.data_ptr(), None, 0, None)
+    assert rc == 1  # NSG_ERR_INVALID_ARGUMENT before any allocation or launch
