@@ -61,7 +61,7 @@ struct Layout {
   // round-2 per-window kernels (nsg_flat.cuh), overlaid on the fast-path scratch
   bool flat;
   u32 flogB, fB, flogBs, fBs, fCP, fNB;  // fNB: windows per batch
-  size_t o_fws, o_fkscr, o_fkoff, o_frscr, o_froff, o_fend;
+  size_t o_fws, o_fkscr, o_fkoff, o_frscr, o_froff, o_fend, o_fipl, o_fipc;
   // global
   u64 LC;
   u32 G;
@@ -122,6 +122,8 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     L.o_frscr = q; q = align256(q + (size_t)L.fNB * L.fB * flat::RCAP * sizeof(u64));
     L.o_froff = q; q = align256(q + (size_t)L.fNB * L.fB * 2 * L.fBs * sizeof(u32));
     L.o_fend = q;
+    L.o_fipc = q; q = align256(q + (size_t)L.fNB * L.fBs * sizeof(u32));                 // IP sets (vectors)
+    L.o_fipl = q; q = align256(q + (size_t)L.fNB * L.fBs * flat::TS * sizeof(u32));
     if (q > o) o = q;
   }
   // L2-path table sets: the full path for large windows, the overflow hand-off otherwise.
@@ -283,7 +285,7 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
   if (cudaMemsetAsync(base, 0, L.memset_bytes, s) != cudaSuccess) return NSG_ERR_CUDA;
   u32* arrived = reinterpret_cast<u32*>(base + L.o_pw) + 5 * L.nw;
   cudaEvent_t ev_copied = nullptr;
-  const bool flat_path = L.flat && !(flags & (NSG_FLAG_FORCE_GLOBAL | NSG_FLAG_LEGACY_FAST)) && !vec && !wgt;
+  const bool flat_path = L.flat && !(flags & (NSG_FLAG_FORCE_GLOBAL | NSG_FLAG_LEGACY_FAST)) && !wgt;
   if (sin && flat_path) {  // the round-2 path copies per batch (below), after the work already on `s`
     cudaEvent_t ev0 = nullptr;
     if (cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming) != cudaSuccess) return NSG_ERR_CUDA;
@@ -351,6 +353,12 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
     g.diag = reinterpret_cast<u32*>(base + DIAG_OFFSET);
     g.mirror = mirror; g.n_mirror = n_mirror; g.mirror_row0 = mirror_row0;
     g.inject = ((flags & NSG_FLAG_INJECT_OVERFLOW) ? 1u : 0u) | ((flags & NSG_FLAG_INJECT_SELF_CHECK) ? 2u : 0u);
+    g.v_lkey = reinterpret_cast<u64*>(V.link_key); g.v_lpk = V.link_packets;
+    g.v_node[0] = V.src_node; g.v_pk[0] = V.src_packets; g.v_fan[0] = V.src_fanout;
+    g.v_node[1] = V.dst_node; g.v_pk[1] = V.dst_packets; g.v_fan[1] = V.dst_fanin;
+    g.v_ipsets = reinterpret_cast<u64*>(V.ip_sets);
+    g.ipl = reinterpret_cast<u32*>(base + L.o_fipl);
+    g.ipc = reinterpret_cast<u32*>(base + L.o_fipc);
     if (cudaMemsetAsync(base + L.o_fws, 0, (size_t)L.nw * sizeof(flat::WinState), s) != cudaSuccess) return NSG_ERR_CUDA;
     if (ev_before && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_before), s) != cudaSuccess) return NSG_ERR_CUDA;
     // Batches pipeline over two streams: part(i) runs on the side stream `a` as soon as link(i-1) has read
@@ -376,6 +384,8 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
         return NSG_ERR_CUDA;
       flat::link_kernel<<<g.nbw * g.B, flat::LTH, sizeof(flat::SmemL), s>>>(g);
       if (cudaEventRecord(ax->link_done, s) != cudaSuccess) return NSG_ERR_CUDA;
+      if (g.v_ipsets && cudaMemsetAsync(g.ipc, 0, (size_t)g.nbw * g.Bs * sizeof(u32), s) != cudaSuccess)
+        return NSG_ERR_CUDA;
       flat::side_kernel<<<g.nbw * 2 * g.Bs, flat::STH, sizeof(flat::SmemS), s>>>(g, out);
       g_last_launches += 3;
       if (cudaGetLastError() != cudaSuccess) return NSG_ERR_CUDA;

@@ -51,8 +51,8 @@ static_assert((RCAP * 8) % 128 == 0, "record rows are whole 128-B lines (16-B st
 
 // Per-window state (64 B), zeroed by the host before the launches.
 struct WinState {
-  u32 sdone, ovf, links, maxc, sumc, r0[3];
-  u32 nodes[2], maxp[2], maxf[2], r1[2];
+  u32 sdone, ovf, links, maxc, sumc, vfill[3];  // vfill: vector entries reserved (links, sources, destinations)
+  u32 nodes[2], maxp[2], maxf[2], both, r1;     // both: |S n D| (IP sets)
 };
 static_assert(sizeof(WinState) == 64, "WinState is 64 B");
 
@@ -72,6 +72,15 @@ struct FGeo {
   u64 mirror_row0;
   u32 inject;                      // bit 0 NSG_FLAG_INJECT_OVERFLOW: odd windows are handed to the L2 path;
                                    // bit 1 NSG_FLAG_INJECT_SELF_CHECK: window 0 counts a self-check failure
+  // nsg_window_vectors (NULL = not requested): window w's entries at [w*W, w*W + count) in reservation order
+  u64* v_lkey;
+  u32* v_lpk;
+  u32* v_node[2];
+  u32* v_pk[2];
+  u32* v_fan[2];
+  u64* v_ipsets;                   // [nw][4]
+  u32* ipl;                        // [nbw][Bs][TS] side-0 node lists (IP sets)
+  u32* ipc;                        // [nbw][Bs] side-0 list length + 1 (0 = not yet published) | esc << 31
 };
 
 __device__ __forceinline__ u32 link_bucket(u64 key, u32 logB) { return logB ? (u32)((key * MUL_L) >> (64 - logB)) : 0u; }
@@ -317,7 +326,7 @@ struct SmemL {
   uint16_t claim[FILL_L];          // the bucket's occupied slots
   u32 segscr[LTH / 32][64];
   u32 red[4][LTH / 32];
-  u32 ncl, esc, ovf, L0;
+  u32 ncl, esc, ovf, L0, vbase;
 };
 
 // Lockstep probe of two keys per lane: every lane advances its unfinished keys by one slot per
@@ -473,6 +482,7 @@ link_kernel(const FGeo g) {
       atomicAdd(&st->links, a);
       atomicMax(&st->maxc, m2);
       atomicAdd(&st->sumc, d);
+      if (g.v_lkey) s.vbase = atomicAdd(&st->vfill[0], a);  // this bucket's link-vector entries
     }
   }
   if (wid < 2) {  // side-0 records first, then side 1 from L0 = number of links (= sum of the side-0 counts)
@@ -499,10 +509,20 @@ link_kernel(const FGeo g) {
     const u32 p1 = atomicAdd(&s.offs[Bs + node_bucket((u32)key, logBs)], 1u);
     __stcg(reinterpret_cast<unsigned long long*>(rrow + p0), (key & 0xFFFFFFFF00000000ull) | c);
     __stcg(reinterpret_cast<unsigned long long*>(rrow + p1), (key << 32) | c);
+    if (g.v_lkey) {  // A_t(i,j) of the link
+      const u64 at = w * g.W + s.vbase + e;
+      g.v_lkey[at] = key;
+      g.v_lpk[at] = c;
+    }
   }
   if (t == 0 && esc) {
     rrow[atomicAdd(&s.offs[eb], 1u)] = ((u64)EMPTY32 << 32) | esc;
     rrow[atomicAdd(&s.offs[Bs + eb], 1u)] = ((u64)EMPTY32 << 32) | esc;
+    if (g.v_lkey) {
+      const u64 at = w * g.W + s.vbase + ncl;
+      g.v_lkey[at] = EMPTY64;
+      g.v_lpk[at] = esc;
+    }
   }
 }
 
@@ -515,7 +535,7 @@ struct SmemS {
   u32 wrap[WRAPCAP];
   u32 segscr[STH / 32][64];
   u32 red[3][STH / 32];
-  u32 escP, escF, ovf, nwrap, last;
+  u32 escP, escF, ovf, nwrap, last, vbase, n0;
 };
 
 // packets += c, fan += 1 for the node in slot `slot`.  An item with fewer than 4096 records cannot
@@ -559,6 +579,26 @@ __device__ __noinline__ void node_merge(SmemS& s, u32 node, u32 P, u32 F, u32 lo
   }
 }
 
+// Is `node` in the (complete) node table?
+__device__ __forceinline__ bool node_find(const SmemS& s, u32 node, u32 logBs) {
+  u32 sl = node_slot(node, logBs);
+  const u32 stp = node_step(node);
+  for (u32 probe = 0; probe < (u32)TS; ++probe) {
+    const u32 cur = s.nkey[sl];
+    if (cur == node) return true;
+    if (cur == EMPTY32) return false;
+    sl = (sl + stp) & (TS - 1);
+  }
+  return false;
+}
+
+// fan of the node in slot sl, with the wraps of its 12-bit field recorded in the wrap list
+__device__ __forceinline__ u32 node_fan(const SmemS& s, u32 sl, u32 pf, u32 nwrap) {
+  u32 cnt = 0;
+  for (u32 k = 0; k < nwrap; ++k) cnt += s.wrap[k] == sl;
+  return (pf >> PFS) + (FMAX + 1) * cnt;
+}
+
 __device__ void finalize(const FGeo& g, u64 w, u64* out) {
   WinState* st = &g.ws[w];
   u32 ovf = ldcg32(&st->ovf);
@@ -580,6 +620,11 @@ __device__ void finalize(const FGeo& g, u64 w, u64* out) {
   row[8] = ldcg32(&st->maxf[1]);
   if (row[0] != len || ((g.inject & 2u) && w == 0)) atomicAdd(&g.diag[1], 1u);  // self-check: the counts sum to the window's packets
   store_row(out + w * NSG_NUM_STATS, row);
+  if (g.v_ipsets) {  // |S u D|, |S \ D|, |D \ S|, |S n D| (reading R13)
+    const u64 b = ldcg32(&st->both);
+    u64* ip = g.v_ipsets + w * 4;
+    ip[0] = row[3] + row[6] - b; ip[1] = row[3] - b; ip[2] = row[6] - b; ip[3] = b;
+  }
   for (u32 m = 0; m < g.n_mirror; ++m) store_row(g.mirror[m] + (g.mirror_row0 + w) * NSG_NUM_STATS, row);
 }
 
@@ -668,11 +713,82 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
     for (int i = 0; i < 4; ++i)
       if (ps[i]) { nn += 1; mp = max(mp, ps[i] & PMASK); mf = max(mf, ps[i] >> PFS); }
   }
-  if (t == 0 && s.escF) { nn += 1; mp = max(mp, s.escP); mf = max(mf, s.escF); }
+  const u32 side = q >= Bs ? 1u : 0u;
+  const bool emit = g.v_node[side] != nullptr || (g.v_ipsets && side == 0);
+  u32 vpre = 0;  // vectors / IP sets: this thread's first entry among the item's table nodes
+  if (emit) {
+    u32 x = nn;
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+      const u32 y = __shfl_up_sync(0xffffffffu, x, k);
+      if (lane >= k) x += y;
+    }
+    vpre = x - nn;
+  }
+  const u32 escF = s.escF, escP = s.escP;
+  if (t == 0 && escF) { nn += 1; mp = max(mp, escP); mf = max(mf, escF); }
   u32 z = 0;
   warp_reduce4(nn, mp, mf, z);
   if (lane == 0) { s.red[0][wid] = nn; s.red[1][wid] = mp; s.red[2][wid] = mf; }
   __syncthreads();
+  if (emit) {  // the item's nodes (mirrors :173) and the side-0 node list
+    u32 ntab = 0;  // table nodes (warp 0's count includes the address ~0, which goes last)
+    for (u32 i = 0; i < NW; ++i) {
+      if (i == (u32)wid) vpre += ntab;
+      ntab += s.red[0][i] - (i == 0 && escF ? 1u : 0u);
+    }
+    const u32 tot = ntab + (escF ? 1u : 0u);
+    if (t == 0 && g.v_node[side]) s.vbase = atomicAdd(&g.ws[w].vfill[1 + side], tot);
+    __syncthreads();
+    const u64 vb = w * g.W + s.vbase;
+    u32* ipl = g.ipl + ((u64)wb * Bs + (q - side * Bs)) * TS;
+    u32 pos = vpre;
+    for (int j = 0; j < SPT; ++j) {
+      const u32 sl = t * SPT + j;
+      const u32 pf = s.npf[sl];
+      if (!pf) continue;
+      const u32 node = s.nkey[sl];
+      if (g.v_node[side]) {
+        g.v_node[side][vb + pos] = node;
+        g.v_pk[side][vb + pos] = pf & PMASK;
+        g.v_fan[side][vb + pos] = node_fan(s, sl, pf, nwrap);
+      }
+      if (g.v_ipsets && side == 0) ipl[pos] = node;
+      ++pos;
+    }
+    if (t == 0 && escF && g.v_node[side]) {
+      g.v_node[side][vb + ntab] = EMPTY32;
+      g.v_pk[side][vb + ntab] = escP;
+      g.v_fan[side][vb + ntab] = escF;
+    }
+    if (g.v_ipsets && side == 0) {  // publish the list for the side-1 item of the same node bucket
+      __syncthreads();
+      if (t == 0) {
+        __threadfence();
+        st_release32(&g.ipc[(u64)wb * Bs + q], (ntab + 1) | (escF ? 0x80000000u : 0u));
+      }
+    }
+  }
+  if (g.v_ipsets && side == 1) {  // |S n D| of this node bucket: the side-0 list probed in this table
+    if (t == 0) {
+      const u32* f = &g.ipc[(u64)wb * Bs + (q - Bs)];
+      u32 v;
+      while ((v = ld_acquire32(f)) == 0u) __nanosleep(64);  // side-0 items precede side-1 items in the grid
+      s.n0 = v;
+    }
+    __syncthreads();
+    const u32 n0 = (s.n0 & 0x7FFFFFFFu) - 1u;
+    const u32* ipl = g.ipl + ((u64)wb * Bs + (q - Bs)) * TS;
+    u32 both = 0;
+    for (u32 e = t; e < n0; e += STH) both += node_find(s, ldcg32(&ipl[e]), logBs) ? 1u : 0u;
+    if (t == 0 && (s.n0 >> 31) && escF) both += 1;  // the address ~0 is a source and a destination
+    both = warp_sum(both);
+    if (lane == 0 && both) {
+      atomicAdd(&g.ws[w].both, both);
+      __threadfence();  // before this item's count (below)
+    }
+    __syncthreads();
+  }
   if (wid == 0) {
     nn = lane < (int)NW ? s.red[0][lane] : 0u;
     mp = lane < (int)NW ? s.red[1][lane] : 0u;
@@ -680,7 +796,6 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
     warp_reduce4(nn, mp, mf, z);
     if (lane == 0) {
       WinState* st = &g.ws[w];
-      const u32 side = q >= Bs ? 1u : 0u;
       if (ovf) {
         st->ovf = 1;
       } else if (nn) {

@@ -8,8 +8,9 @@ the inputs follow the kernels if they are retuned; the expected values always co
 
 Capacities:
 - round-2 path (nsg_flat.cuh, W <= 2^17): a link bucket holds FILL_L distinct links (beyond that its
-  records would not fit the record row); a node bucket's table holds TS distinct nodes;
-- round-1 path (nsg_fast.cuh; NSG_FLAG_LEGACY_FAST, and nsg_window_vectors): a link bucket holds TCAP
+  records would not fit the record row); a node bucket's table holds TS distinct nodes (B = W / BK link
+  buckets, B / 2 node buckets per side);
+- round-1 path (nsg_fast.cuh; NSG_FLAG_LEGACY_FAST, windows 2^17 < W < 2^20, weighted rows): a link bucket holds TCAP
   distinct links, a side bucket TCAP_S distinct nodes.
 The key ~0 (both addresses 255.255.255.255) and the node ~0 are kept outside the tables and never count.
 """
