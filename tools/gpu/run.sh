@@ -4,6 +4,7 @@
 # Outputs land in gpurun_out/ (scratch); the summaries that are judged are copied into profiles/.
 #
 #   tests       pytest -m gpu (the parity suite)                       -> gpurun_out/gpu_tests.log
+#   (order matters: run `traffic` before `bench`, so that the bench line reports the traffic of its own build)
 #   bench       bench.py C2 line (200 steps)                           -> gpurun_out/bench_C2.json
 #   quick       parity spot set + C2 call time vs the round-1 kernel (tools/r2_quick.py), C1/C2/C3 call times
 #               (tools/c3_time.py)                                     -> gpurun_out/quick.log
@@ -43,7 +44,7 @@ for cmd in "$@"; do
       ncu -i gpurun_out/r02/full_C2.ncu-rep --page source --csv --print-source=cuda,sass -k regex:${k}_kernel \
         > gpurun_out/r02/src_${k}.csv 2>/dev/null
     done
-    python tools/r02_summaries.py gpurun_out/r02 profiles/r02 > /dev/null && cp -r profiles/r02 gpurun_out/r02_summaries ;;
+    python tools/r02_summaries.py gpurun_out/r02 gpurun_out/r02_summaries > /dev/null ;;
   traffic)
     for wl in C2 C3; do
       timeout 600 "${NCU_LIST[@]}" gpurun_out/traffic_$wl.csv python tools/traffic_case.py 12 $wl > /dev/null 2>&1
