@@ -35,7 +35,7 @@ constexpr int LTH = 256;                      // link CTA threads
 constexpr int STH = 256;                      // side CTA threads
 constexpr u64 BK = 1024;                      // target keys per link bucket / nodes per side bucket
 constexpr u64 MAX_W = 1ull << 17;             // windows this path takes (<= 128 link / side buckets)
-constexpr int MAXB = 256;
+constexpr int MAXB = (int)(MAX_W / BK);          // link buckets of the largest window (= 2 x node buckets)
 constexpr int LOG_TL = 11, TL = 1 << LOG_TL;  // link-table slots (load <= 5/8)
 constexpr int LOG_TS = 12, TS = 1 << LOG_TS;  // node-table slots
 constexpr u32 FILL_L = 1280, FILL_S = 1280;   // distinct entries before the window goes to the L2 path
@@ -322,7 +322,7 @@ part_kernel(const FGeo g, const u32* __restrict__ src, const u32* __restrict__ d
 struct SmemL {
   u64 lkey[TL];
   u32 lcnt[TL];
-  u32 hist[2 * MAXB], offs[2 * MAXB];
+  u32 hist[MAXB], offs[MAXB];      // per (side, node bucket): 2 * Bs <= MAXB
   uint16_t claim[FILL_L];          // the bucket's occupied slots
   u32 segscr[LTH / 32][64];
   u32 red[4][LTH / 32];
