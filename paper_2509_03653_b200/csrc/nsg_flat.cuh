@@ -1,27 +1,26 @@
-// nsg_flat.cuh — the per-window statistics kernels of libnsg (round 2), windows <= 2^18.
+// nsg_flat.cuh — the per-window statistics kernels of libnsg (round 2), windows <= 2^17.
 //
 // What it computes: for every window of W consecutive packets, the nine Table 2 scalars of the
 // traffic matrix A_t (destination mirrors, line 173): valid packets (:180),
 // unique links (:181), max link packets (:183), unique sources (:184), max source packets (:186), max
-// source fan-out (:188) and the three destination mirrors.  Readings: DESIGN.md §2.
+// source fan-out (:188) and the three destination mirrors; optionally the vector-valued rows (:182,
+// :185, :187) and the four IP-set counts (:209).  Readings: DESIGN.md §2.
 //
-// How: three flat kernels per batch of windows, one work item per CTA, several small
-// CTAs resident per SM so that the latency chains of independent items overlap (a measured property
-// of this work on B200: every item is a short chain of dependent shared-memory round trips, ~200-500
-// cycles each under load, and one item in flight per SM leaves the SM idle most of the time):
-//   part  (w, c)   4096 keys of window w (streaming 128-bit loads from HBM), counting-sorted by link
-//                  bucket (top bits of key * phi64) into the batch's key scratch; one row of segment
+// How: three flat kernels per batch of 32 windows, one work item per CTA, several CTAs
+// resident per SM so that the latency chains of independent items overlap:
+//   part  (w, c)   4096 keys of window w (128-bit loads, L2 evict-first), counting-sorted by link bucket
+//                  (top bits of key * phi64) into the batch's key scratch; one row of segment
 //                  descriptors per item;
-//   link  (w, b)   link bucket b: its segment of every chunk gathered into SMEM, group-by-count in an
-//                  SMEM open-addressing table (A_t restricted to the bucket: unique links, max link,
-//                  count sum -> window accumulators), then one record (node << 32 | count) per link and
-//                  side, counting-sorted by side bucket into the record scratch;
-//   side  (w,s,q)  side bucket q of side s: the records of every link bucket, merged per node in an
-//                  SMEM table of (node, packets | fan << 20): unique nodes, max packets, max fan ->
-//                  window accumulators; the last side item of a window writes its row.
+//   link  (w, b)   link bucket b (~1024 keys): each warp gathers its share of the chunks' segments
+//                  straight into registers and inserts two keys per lane in lockstep into a 2048-slot
+//                  SMEM table (A_t restricted to the bucket); the occupied slots, compacted, give unique
+//                  links, max link, count sum (-> window accumulators) and one record (node << 32 |
+//                  count) per link and side, stored by node bucket into the bucket's record row;
+//   side  (w,s,q)  node bucket q of side s: the records of every link bucket merged per node in a
+//                  4096-slot SMEM table of (node, packets | fan << 20): unique nodes, max packets, max
+//                  fan -> window accumulators; the last side item of a window writes its row.
 // Tables are probed with a plain load first (a hot key's repeats cost a broadcast read and an
-// aggregated increment, never a CAS); collisions probe on with double hashing; claimed slots are kept
-// in a dense claim list so that the final scans visit entries only.
+// aggregated increment, never a CAS); collisions probe on with double hashing (odd steps).
 #pragma once
 #include "nsg_internal.h"
 #include "nsg_common.cuh"
@@ -38,7 +37,7 @@ constexpr u64 MAX_W = 1ull << 17;             // windows this path takes (<= 128
 constexpr int MAXB = (int)(MAX_W / BK);          // link buckets of the largest window (= 2 x node buckets)
 constexpr int LOG_TL = 11, TL = 1 << LOG_TL;  // link-table slots (load <= 5/8)
 constexpr int LOG_TS = 12, TS = 1 << LOG_TS;  // node-table slots
-constexpr u32 FILL_L = 1280, FILL_S = 1280;   // distinct entries before the window goes to the L2 path
+constexpr u32 FILL_L = 1280;                  // distinct links of a bucket before the window goes to the L2 path
 constexpr u32 RCAP = (2 * (FILL_L + 1) + 15) & ~15u;  // records per link bucket (both sides), whole lines
 constexpr int PFS = 20;                       // node packets: 20-bit field (W < 2^20)
 constexpr u32 PMASK = (1u << PFS) - 1;
@@ -94,10 +93,6 @@ __device__ __forceinline__ u32 node_slot(u32 node, u32 logBs) {
 }
 __device__ __forceinline__ u32 node_step(u32 node) { return ((node * 0x85ebca6bu) >> 7) | 1u; }
 
-__device__ __forceinline__ void cp_async8(void* sdst, const void* gsrc) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((u32)__cvta_generic_to_shared(sdst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Input keys are read once: loaded with an L2 evict-first policy so that the stream does not push the
 // (dirty, L2-resident) scratch of the batch pipeline out to HBM.
@@ -138,20 +133,6 @@ __device__ __forceinline__ u32 warp_exscan(const u32* h, u32* o, u32 n, int lane
   return carry;
 }
 
-// Warp-wide reservation of n list entries (returns this thread's first position).
-__device__ __forceinline__ u32 warp_reserve(u32 n, u32* ctr) {
-  const int lane = threadIdx.x & 31;
-  u32 x = n;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const u32 y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  const u32 tot = __shfl_sync(0xffffffffu, x, 31);
-  u32 b = 0;
-  if (lane == 31 && tot) b = atomicAdd(ctr, tot);
-  return __shfl_sync(0xffffffffu, b, 31) + x - n;
-}
 
 __device__ __forceinline__ void warp_reduce4(u32& a, u32& b, u32& c, u32& d) {
 #pragma unroll
