@@ -61,7 +61,7 @@ struct Layout {
   // round-2 per-window kernels (nsg_flat.cuh), overlaid on the fast-path scratch
   bool flat;
   u32 flogB, fB, flogBs, fBs, fCP, fNB;  // fNB: windows per batch
-  size_t o_fws, o_fkscr, o_fkoff, o_frscr, o_froff, o_fend, o_fipl, o_fipc;
+  size_t o_fws, o_fkscr, o_fkoff, o_frscr, o_froff, o_fwscr, o_fend, o_fipl, o_fipc;
   // global
   u64 LC;
   u32 G;
@@ -121,6 +121,7 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     L.o_fkoff = q; q = align256(q + (size_t)L.fNB * L.fCP * L.fB * sizeof(u32));
     L.o_frscr = q; q = align256(q + (size_t)L.fNB * L.fB * flat::RCAP * sizeof(u64));
     L.o_froff = q; q = align256(q + (size_t)L.fNB * L.fB * 2 * L.fBs * sizeof(u32));
+    L.o_fwscr = q; q = align256(q + (size_t)L.fNB * L.fCP * flat::CH * sizeof(u32));   // weighted rows
     L.o_fend = q;
     L.o_fipc = q; q = align256(q + (size_t)L.fNB * L.fBs * sizeof(u32));                 // IP sets (vectors)
     L.o_fipl = q; q = align256(q + (size_t)L.fNB * L.fBs * flat::TS * sizeof(u32));
@@ -178,8 +179,10 @@ static nsg_status dev_info(DevInfo& out) {
       if (per_sm < 1 || per_sm_w < 1) return NSG_ERR_UNSUPPORTED_DEVICE;
       d.fast_blocks = per_sm * d.sms;
       d.fast_blocks_w = per_sm_w * d.sms;
-      if (cudaFuncSetAttribute(flat::part_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(flat::SmemP)) != cudaSuccess ||
-          cudaFuncSetAttribute(flat::link_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(flat::SmemL)) != cudaSuccess ||
+      if (cudaFuncSetAttribute(flat::part_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(flat::SmemP)) != cudaSuccess ||
+          cudaFuncSetAttribute(flat::part_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(flat::SmemP)) != cudaSuccess ||
+          cudaFuncSetAttribute(flat::link_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(flat::SmemL)) != cudaSuccess ||
+          cudaFuncSetAttribute(flat::link_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(flat::SmemL)) != cudaSuccess ||
           cudaFuncSetAttribute(flat::side_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(flat::SmemS)) != cudaSuccess)
         return NSG_ERR_CUDA;
     }
@@ -285,7 +288,7 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
   if (cudaMemsetAsync(base, 0, L.memset_bytes, s) != cudaSuccess) return NSG_ERR_CUDA;
   u32* arrived = reinterpret_cast<u32*>(base + L.o_pw) + 5 * L.nw;
   cudaEvent_t ev_copied = nullptr;
-  const bool flat_path = L.flat && !(flags & (NSG_FLAG_FORCE_GLOBAL | NSG_FLAG_LEGACY_FAST)) && !wgt;
+  const bool flat_path = L.flat && !(flags & (NSG_FLAG_FORCE_GLOBAL | NSG_FLAG_LEGACY_FAST));
   if (sin && flat_path) {  // the round-2 path copies per batch (below), after the work already on `s`
     cudaEvent_t ev0 = nullptr;
     if (cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming) != cudaSuccess) return NSG_ERR_CUDA;
@@ -358,6 +361,8 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
     g.v_node[1] = V.dst_node; g.v_pk[1] = V.dst_packets; g.v_fan[1] = V.dst_fanin;
     g.v_ipsets = reinterpret_cast<u64*>(V.ip_sets);
     g.ipl = reinterpret_cast<u32*>(base + L.o_fipl);
+    g.wgt = wgt;
+    g.wscr = reinterpret_cast<u32*>(base + L.o_fwscr);
     g.ipc = reinterpret_cast<u32*>(base + L.o_fipc);
     if (cudaMemsetAsync(base + L.o_fws, 0, (size_t)L.nw * sizeof(flat::WinState), s) != cudaSuccess) return NSG_ERR_CUDA;
     if (ev_before && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_before), s) != cudaSuccess) return NSG_ERR_CUDA;
@@ -379,10 +384,12 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
                         cudaStreamWaitEvent(ax->a, ax->copied, 0) == cudaSuccess;
         if (!ok) return NSG_ERR_CUDA;
       }
-      flat::part_kernel<<<g.nbw * g.CP, flat::PTH, sizeof(flat::SmemP), ax->a>>>(g, src, dst, keys);
+      if (wgt) flat::part_kernel<true><<<g.nbw * g.CP, flat::PTH, sizeof(flat::SmemP), ax->a>>>(g, src, dst, keys);
+      else flat::part_kernel<false><<<g.nbw * g.CP, flat::PTH, sizeof(flat::SmemP), ax->a>>>(g, src, dst, keys);
       if (cudaEventRecord(ax->part_done, ax->a) != cudaSuccess || cudaStreamWaitEvent(s, ax->part_done, 0) != cudaSuccess)
         return NSG_ERR_CUDA;
-      flat::link_kernel<<<g.nbw * g.B, flat::LTH, sizeof(flat::SmemL), s>>>(g);
+      if (wgt) flat::link_kernel<true><<<g.nbw * g.B, flat::LTH, sizeof(flat::SmemL), s>>>(g);
+      else flat::link_kernel<false><<<g.nbw * g.B, flat::LTH, sizeof(flat::SmemL), s>>>(g);
       if (cudaEventRecord(ax->link_done, s) != cudaSuccess) return NSG_ERR_CUDA;
       if (g.v_ipsets && cudaMemsetAsync(g.ipc, 0, (size_t)g.nbw * g.Bs * sizeof(u32), s) != cudaSuccess)
         return NSG_ERR_CUDA;

@@ -51,7 +51,7 @@ static_assert((RCAP * 8) % 128 == 0, "record rows are whole 128-B lines (16-B st
 // Per-window state (64 B), zeroed by the host before the launches.
 struct WinState {
   u32 sdone, ovf, links, maxc, sumc, vfill[3];  // vfill: vector entries reserved (links, sources, destinations)
-  u32 nodes[2], maxp[2], maxf[2], both, r1;     // both: |S n D| (IP sets)
+  u32 nodes[2], maxp[2], maxf[2], both, wtot;   // both: |S n D| (IP sets); wtot: sum of n_packets (weighted rows)
 };
 static_assert(sizeof(WinState) == 64, "WinState is 64 B");
 
@@ -62,6 +62,8 @@ struct FGeo {
   u32 logB, B, logBs, Bs, CP;
   WinState* ws;                    // [nw]
   u64* kscr;                       // [nbw][CP][CH]
+  const u32* wgt;                  // weighted rows: n_packets per row (NULL: raw packets, weight 1)
+  u32* wscr;                       // [nbw][CP][CH] the keys' weights, in kscr order (weighted rows)
   u32* koff;                       // [nbw][CP][B]    start << 16 | count of bucket b in chunk c
   u64* rscr;                       // [nbw][B][RCAP]
   u32* roff;                       // [nbw][B][2Bs]   start << 16 | count of side bucket (s,q) in link bucket b
@@ -133,6 +135,12 @@ __device__ __forceinline__ u32 warp_exscan(const u32* h, u32* o, u32 n, int lane
   return carry;
 }
 
+
+__device__ __forceinline__ u64 warp_sum64(u64 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
 __device__ __forceinline__ void warp_reduce4(u32& a, u32& b, u32& c, u32& d) {
 #pragma unroll
@@ -224,9 +232,12 @@ __device__ __forceinline__ void warp_seg_step(WarpSegs& ws, u32 e0, u32& oa, u32
 // ---------------------------------------------------------------------------------------------
 struct SmemP {
   u64 stage[CH];
+  u32 wraw[CH], wstage[CH];        // weighted rows: the chunk's weights in row order, then sorted
   u32 hist[MAXB], offs[MAXB];
 };
+constexpr u32 WTOT_MAX = 1u << 20;  // weighted windows summing to this or more go to the L2 path (20-bit packets)
 
+template <bool WT>
 __global__ void __launch_bounds__(PTH, 3)
 part_kernel(const FGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, const u64* __restrict__ keys) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -273,6 +284,23 @@ part_kernel(const FGeo g, const u32* __restrict__ src, const u32* __restrict__ d
       kk[2 * i + 1] = e + 1 < n ? ((u64)__ldcs(src + base + e + 1) << 32) | __ldcs(dst + base + e + 1) : 0ull;
     }
   }
+  u32 zero = 0;  // weighted rows: bit i = row of element i has n_packets 0 (it adds nothing: dropped)
+  if (WT) {
+    u64 wsum = 0;
+    for (u32 e = t; e < CH; e += PTH) {
+      const u32 x = e < n ? __ldcs(g.wgt + base + e) : 0u;
+      s.wraw[e] = x;
+      wsum += x;
+    }
+    wsum = warp_sum64(wsum);
+    if (lane == 0 && wsum) atomicAdd(&g.ws[w].wtot, (u32)min(wsum, (u64)WTOT_MAX));  // saturated per warp
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < KPT; ++i) {
+      const u32 e = 2 * ((i >> 1) * PTH + t) + (i & 1);
+      zero |= (e < n && s.wraw[e] == 0u ? 1u : 0u) << i;
+    }
+  }
   __syncthreads();  // histogram cleared
   u32 bk[KPT], rk[KPT];
 #pragma unroll
@@ -280,7 +308,7 @@ part_kernel(const FGeo g, const u32* __restrict__ src, const u32* __restrict__ d
 #pragma unroll
   for (int i = 0; i < KPT; ++i) {
     const u32 e = 2 * ((i >> 1) * PTH + t) + (i & 1);
-    rk[i] = e < n ? atomicAdd(&s.hist[bk[i]], 1u) : 0u;
+    rk[i] = e < n && !(zero >> i & 1u) ? atomicAdd(&s.hist[bk[i]], 1u) : 0u;
   }
   __syncthreads();
   if (wid == 0) {
@@ -291,10 +319,18 @@ part_kernel(const FGeo g, const u32* __restrict__ src, const u32* __restrict__ d
 #pragma unroll
   for (int i = 0; i < KPT; ++i) {
     const u32 e = 2 * ((i >> 1) * PTH + t) + (i & 1);
-    if (e < n) s.stage[s.offs[bk[i]] + rk[i]] = kk[i];
+    if (e < n && !(zero >> i & 1u)) {
+      s.stage[s.offs[bk[i]] + rk[i]] = kk[i];
+      if (WT) s.wstage[s.offs[bk[i]] + rk[i]] = s.wraw[e];
+    }
   }
   __syncthreads();
-  copy_out<PTH>(g.kscr + ((u64)wb * g.CP + c) * CH, s.stage, n);
+  const u32 nz = s.offs[B - 1] + s.hist[B - 1];  // rows kept (weighted rows of weight 0 are dropped)
+  copy_out<PTH>(g.kscr + ((u64)wb * g.CP + c) * CH, s.stage, nz);
+  if (WT) {
+    u32* wd = g.wscr + ((u64)wb * g.CP + c) * CH;
+    for (u32 e = t; e < nz; e += PTH) wd[e] = s.wstage[e];
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -348,6 +384,7 @@ __device__ __forceinline__ u32 probe2(T* keys, u32 mask, T ka, T kb, u32& sa, u3
   return claimed;
 }
 
+template <bool WT>
 __global__ void __launch_bounds__(LTH, 7)
 link_kernel(const FGeo g) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -360,7 +397,10 @@ link_kernel(const FGeo g) {
   for (u32 i = t; i < (u32)TL / 2; i += LTH) reinterpret_cast<ulonglong2*>(s.lkey)[i] = make_ulonglong2(EMPTY64, EMPTY64);
   for (u32 i = t; i < (u32)TL / 4; i += LTH) reinterpret_cast<uint4*>(s.lcnt)[i] = make_uint4(0u, 0u, 0u, 0u);
   for (u32 i = t; i < 2 * Bs; i += LTH) s.hist[i] = 0;
-  if (t == 0) { s.ncl = 0; s.esc = 0; s.ovf = 0; }
+  if (t == 0) {
+    s.ncl = 0; s.esc = 0;
+    s.ovf = WT && ldcg32(&g.ws[w].wtot) >= WTOT_MAX ? 1u : 0u;  // weighted: packets past the 20-bit fields
+  }
   // this warp's share of the bucket: its segment of chunks wid, wid + NW, ...
   const u32* ko = g.koff + (u64)wb * CP * B + b;
   WarpSegs ws = warp_segs(CP, NW, s.segscr[wid], [&](u32 c) { return ldcg32(ko + (u64)c * B); }, [&](u32 c) { return c * (u32)CH; });
@@ -370,27 +410,39 @@ link_kernel(const FGeo g) {
     u32 nesc = 0;
     // the next step's keys are loaded while this step's are inserted (L2 latency off the chain)
     u64 nxa = EMPTY64, nxc = EMPTY64;
+    u32 nwa = 1, nwc = 1;  // the keys' weights (weighted rows)
+    const u32* wsb = WT ? g.wscr + (u64)wb * CP * CH : nullptr;
     auto fetch = [&](u32 e0) {
       u32 oa, ob;
       warp_seg_step(ws, e0, oa, ob);
       nxa = e0 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(kb + oa)) : EMPTY64;
       nxc = e0 + 32 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(kb + ob)) : EMPTY64;
+      if (WT) {
+        nwa = e0 + lane < ws.n ? ldcg32(wsb + oa) : 0u;
+        nwc = e0 + 32 + lane < ws.n ? ldcg32(wsb + ob) : 0u;
+      }
     };
     if (ws.n) fetch(0);
     for (u32 e0 = 0; e0 < ws.n; e0 += 64) {
       const bool va = e0 + lane < ws.n, vb = e0 + 32 + lane < ws.n;
       const u64 ka = nxa, kc = nxc;
+      const u32 wa = nwa, wc = nwc;
       if (e0 + 64 < ws.n) fetch(e0 + 64);
       if (*reinterpret_cast<volatile u32*>(&s.ovf)) break;
       const bool aa = ka != EMPTY64, ab = kc != EMPTY64;  // the key ~0 is counted apart
-      nesc += (va && !aa) + (vb && !ab);
+      nesc += (va && !aa ? wa : 0u) + (vb && !ab ? wc : 0u);
       u32 sa = link_slot(ka, logB), sb = link_slot(kc, logB);
       const u64 ca = *reinterpret_cast<volatile u64*>(&s.lkey[sa]);
       const u64 cb = *reinterpret_cast<volatile u64*>(&s.lkey[sb]);
       probe2<unsigned long long>(reinterpret_cast<unsigned long long*>(s.lkey), TL - 1, ka, kc, sa, sb, ca, cb, aa, ab,
                                  &s.ovf, [](u64 k) { return link_step(k); });
-      if (aa) atomicAdd(&s.lcnt[sa], 1u);
-      if (ab) atomicAdd(&s.lcnt[sb], 1u);
+      if (WT) {
+        if (aa) atomicAdd(&s.lcnt[sa], wa);
+        if (ab) atomicAdd(&s.lcnt[sb], wc);
+      } else {
+        if (aa) atomicAdd(&s.lcnt[sa], 1u);
+        if (ab) atomicAdd(&s.lcnt[sb], 1u);
+      }
     }
     nesc = __reduce_add_sync(0xffffffffu, nesc);
     if (lane == 0 && nesc) atomicAdd(&s.esc, nesc);
@@ -588,7 +640,7 @@ __device__ void finalize(const FGeo& g, u64 w, u64* out) {
     atomicAdd(&g.diag[0], 1u);
     return;
   }
-  const u64 len = min(g.W, g.n - w * g.W);
+  const u64 len = g.wgt ? (u64)ldcg32(&st->wtot) : min(g.W, g.n - w * g.W);  // valid packets expected
   u64 row[NSG_NUM_STATS];
   row[0] = ldcg32(&st->sumc);
   row[1] = ldcg32(&st->links);

@@ -146,3 +146,20 @@ def test_weighted_vectors(nsg, cuda_device, flags):
         for f in ("link_key", "link_packets", "src_node", "src_packets", "src_fan", "dst_node", "dst_packets",
                   "dst_fan"):
             assert got[f].astype(np.uint64).tolist() == exp[f].astype(np.uint64).tolist(), (w, f)
+
+
+@pytest.mark.parametrize("delta", [-1, 0, 1])
+def test_window_weight_sum_at_the_20_bit_edge(nsg, cuda_device, delta):
+    """The round-2 kernels keep packets in 20-bit fields: a window whose weights sum to 2^20 or more is
+    handed to the L2 path.  Sums 2^20 - 1 / 2^20 / 2^20 + 1 (hand-over count 0 / 1 / 1), bit-exact."""
+    win = 4096
+    keys = gen.generate_host(gen.Dist("zipf", 1.1, 1 << 12), 66, 0, win, packed=True)
+    wt = np.full(win, 256, np.uint32)  # sum 2^20
+    wt[0] += np.uint32(delta) if delta >= 0 else np.uint32(0)
+    if delta < 0:
+        wt[0] -= np.uint32(1)
+    assert int(wt.sum()) == (1 << 20) + delta
+    want = oracle.window_stats_weighted(keys=keys, weights=wt, window=win)
+    got, diag = run_w(nsg, keys, wt, win, cuda_device, want_diag=True)
+    assert got.tolist() == want.tolist()
+    assert diag[0] == (0 if delta < 0 else 1) and diag[1] == 0
