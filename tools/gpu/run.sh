@@ -13,7 +13,7 @@
 #   traffic     per-kernel DRAM bytes over a sequence of C2 / C3 calls (ncu --cache-control none)
 #                                                                       -> profiles/ncu_traffic.json
 #   sanitize    compute-sanitizer memcheck / racecheck / synccheck on C1 and 4 windows of C2, three paths
-#               (round-2 kernels, round-1 kernel, vectors)            -> gpurun_out/sanitize_*.txt
+#               (round-2 kernels, round-1 kernel, vectors + IP sets, weighted rows) -> gpurun_out/sanitize_*.txt
 #   batch-sweep rebuild libnsg with NSG_FLAT_BATCH = 16 / 32 / 64: C2 call time and DRAM bytes per call
 #               (leaves the last build in place: rebuild afterwards)   -> gpurun_out/fb_*.csv
 set -u
@@ -56,7 +56,7 @@ for cmd in "$@"; do
     # bounds (torch's caching pool would hide overruns); tools/sanitizer_check/ is the positive control.
     for tool in memcheck racecheck synccheck; do
       for cs in C1 C2r; do
-        for p in flat legacy vectors; do
+        for p in flat legacy vectors weighted; do
           log=gpurun_out/sanitize_${tool}_${cs}_${p}.txt
           extra=""
           [ $tool = racecheck ] && extra="--racecheck-report all"

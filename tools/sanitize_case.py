@@ -1,5 +1,5 @@
 """One call of the per-window path for compute-sanitizer (memcheck / racecheck / synccheck), checked
-against the oracle.  usage: python tools/sanitize_case.py {C1|C2r} {flat|legacy|vectors}
+against the oracle.  usage: python tools/sanitize_case.py {C1|C2r} {flat|legacy|vectors|weighted}
 C2r = the first 4 windows of C2 (sanitizer replay is slow)."""
 import os
 import sys
@@ -22,6 +22,10 @@ kd = torch.from_numpy(keys.view(np.int64)).cuda()
 want = oracle.window_stats_sort(keys=keys, window=c.window)
 if path == "vectors":
     got = nsg.window_vectors(kd, c.window)["stats"]
+elif path == "weighted":
+    wt = (np.arange(n, dtype=np.uint32) % 7).astype(np.uint32)  # 0..6: rows of weight 0 included
+    want = oracle.window_stats_weighted(keys=keys, weights=wt, window=c.window)
+    got = nsg.window_stats_weighted(kd, torch.from_numpy(wt.view(np.int32)).cuda(), c.window)
 else:
     got = nsg.window_stats_packed(kd, c.window, flags=nsg.api._FLAG_LEGACY_FAST if path == "legacy" else 0)
 got = got.cpu().numpy().view(np.uint64)
