@@ -250,6 +250,10 @@ def main():
     ap.add_argument("--streams", type=int, default=2,
                     help="default path at N=1: consecutive batches alternate over this many CUDA streams with "
                          "their own workspaces, so a batch's pipeline fill overlaps the previous batch's drain")
+    ap.add_argument("--graphs", type=int, default=1,
+                    help="default path at N=1: each call of the hot path is captured once in a CUDA graph (one per "
+                         "ring batch and stream) and replayed every step (same kernels and work, lower launch "
+                         "overhead); 0 = plain calls")
     ap.add_argument("--transport", choices=["nccl", "p2p"], default="nccl",
                     help="N>1: NCCL collectives, or the kernels storing straight into the other ranks' "
                          "CUDA-IPC-mapped buffers over peer memory (windows: result rows from the epilogue; "
@@ -354,10 +358,29 @@ def main():
     wss = [ws] + [nsg.Workspace(n, WINDOW, dev) for _ in range(nstreams - 1)]
     vbufs = [vbuf] + ([nsg.window_vectors(ring[0], WINDOW, out=outs[1], workspace=wss[1]) for _ in range(nstreams - 1)]
                       if vec else [None] * (nstreams - 1))
-    streams = [torch.cuda.current_stream(dev)] + [torch.cuda.Stream(dev) for _ in range(nstreams - 1)]
+    use_graphs = bool(args.graphs) and world == 1 and not (vec or wtd or trace or anon or c4)
+    # (graphs are captured on non-default streams)
+    streams = ([] if use_graphs else [torch.cuda.current_stream(dev)])
+    streams += [torch.cuda.Stream(dev) for _ in range(nstreams - len(streams))]
+    cur_stream = torch.cuda.current_stream(dev)
     gstream = torch.cuda.Stream(dev) if (nstreams > 1 and world > 1) else None
 
+    graphs = []
+    last_out = [outs[0]]
+
     def step(i, evs=None):
+        if use_graphs and graphs:  # the captured call of batch (i mod ring) on stream (i mod nstreams)
+            j = i % len(graphs)
+            s_i = streams[j % nstreams]
+            with torch.cuda.stream(s_i):
+                if evs:
+                    evs[0].record()
+                graphs[j].replay()
+                if evs:
+                    evs[1].record()
+            last_out[0] = outs[j % RING]
+            return outs[j % RING]
+        last_out[0] = outs[i % RING]
         if nstreams > 1:
             s_i = streams[i % nstreams]
             with torch.cuda.stream(s_i):
@@ -434,6 +457,24 @@ def main():
     torch.cuda.synchronize(dev)
     launches = nsg.last_launches()
     diag = ws.diag()
+    if use_graphs:  # capture one call per (ring batch, stream) pair, after the warm-up initialised the library
+        import math
+
+        for j, s_j in enumerate(streams):  # the library's per-stream state exists before capture
+            with torch.cuda.stream(s_j):
+                nsg.window_stats_packed(ring[j % ring_n], WINDOW, out=outs[j % RING], workspace=wss[j], stream=s_j)
+        torch.cuda.synchronize(dev)
+        for j in range(ring_n * nstreams // math.gcd(ring_n, nstreams)):
+            s_j = streams[j % nstreams]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s_j):
+                nsg.window_stats_packed(ring[j % ring_n], WINDOW, out=outs[j % RING], workspace=wss[j % nstreams],
+                                        stream=s_j)
+            graphs.append(g)
+        launches = nsg.last_launches()
+        for i in range(len(graphs)):  # warm replays
+            step(i)
+        torch.cuda.synchronize(dev)
 
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -446,12 +487,14 @@ def main():
     torch.cuda.synchronize(dev)
     wall0 = time.perf_counter()
     start.record()
-    for s_ in streams[1:]:
-        s_.wait_event(start)
+    for s_ in streams:
+        if s_ != cur_stream:
+            s_.wait_event(start)
     for i in range(args.steps):
         step(i, kev[i])
-    for s_ in streams[1:] + ([gstream] if gstream is not None else []):
-        streams[0].wait_stream(s_)
+    for s_ in streams + ([gstream] if gstream is not None else []):
+        if s_ != cur_stream:
+            cur_stream.wait_stream(s_)
     if p2p_tab is not None:  # every rank's rows are in every table before the clock stops
         torch.cuda.synchronize(dev)
         tdist.barrier()
@@ -473,7 +516,7 @@ def main():
     total_pkts = pkts_per_step * args.steps
     value = total_pkts / (t_ms / 1e3)
     value_no_gather = pkts_per_step / (k_avg / 1e3)  # kernels only (per-step CUDA events, max over ranks)
-    last_rows = outs[(args.steps - 1) % RING].cpu().numpy()
+    last_rows = last_out[0].cpu().numpy()
 
     # ---- e2e: the public API from pinned host buffers (H2D of the keys + D2H of the result inside)
     host = ring[0].cpu().pin_memory()
@@ -559,7 +602,8 @@ def main():
             cpu = cpu_baseline(dist_, seed)
         spot = None
         if not (trace or anon or wtd):
-            spot = spot_check(dist_, seed, last_rows, first_packet(args.steps - 1), sorted({0, wps // 2, wps - 1}))
+            last_i = (args.steps - 1) % len(graphs) if graphs else args.steps - 1
+            spot = spot_check(dist_, seed, last_rows, first_packet(last_i), sorted({0, wps // 2, wps - 1}))
         suffix = "-vectors" if vec else "-weighted" if wtd else "-trace" if trace else "-anonymize" if anon else ""
         traffic, traffic_src = traffic_per_launch(args.workload + suffix)
         if c4:
@@ -586,7 +630,9 @@ def main():
                        "input": "device-resident packed u64 keys (src<<32|dst)",
                        "gather": (f"NCCL all_gather_into_tensor of the [{total_windows}, 9] rows inside the timed region"
                                   if world > 1 else "none (N=1)"),
-                       "streams": nstreams},
+                       "streams": nstreams,
+                       "cuda_graphs": (f"each step replays a captured call ({len(graphs)} graphs: one per ring batch "
+                                       "and stream)" if graphs else "no")},
             "value_without_gather": value_no_gather if world > 1 else None,
             "e2e": {"value": e2e_value, "unit": "rows/s" if wtd else UNIT, "h2d_bytes_per_step": n * (12 if wtd else 8),
                     "d2h_bytes_per_step": d2h_bytes, "steps": e2e_steps},
