@@ -46,7 +46,11 @@ want = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "smsp__issue_active
         "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio",
         "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "launch__grid_size",
-        "launch__block_size", "launch__occupancy_limit_shared_mem", "sm__throughput.avg.pct_of_peak_sustained_elapsed"]
+        "launch__block_size", "launch__occupancy_limit_shared_mem", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+        "smsp__sass_inst_executed_op_shared.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+        "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed"]
 idx = {h: i for i, h in enumerate(hdr)}
 PK = 64 * (1 << 17)  # packets per C2 call
 with open(os.path.join(OUT, "ncu_full_C2.txt"), "w") as f:
@@ -61,5 +65,10 @@ with open(os.path.join(OUT, "ncu_full_C2.txt"), "w") as f:
         if "smsp__inst_executed.sum" in idx:
             inst = float(r[idx["smsp__inst_executed.sum"]].replace(",", ""))
             f.write(f"  warp-instructions per packet (per launch / 2^22 packets): {inst / (PK / 2):.2f}\n")
+        for m, label in (("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared-memory wavefronts"),
+                         ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", "  of which atomics")):
+            if m in idx:
+                v = float(r[idx[m]].replace(",", ""))
+                f.write(f"  {label} per packet: {v / (PK / 2):.2f}\n")
 print(open(os.path.join(OUT, "launches_C2.txt")).read())
 print(open(os.path.join(OUT, "ncu_full_C2.txt")).read())
