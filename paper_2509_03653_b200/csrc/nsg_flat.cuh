@@ -13,12 +13,15 @@
 //                  descriptors per item;
 //   link  (w, b)   link bucket b (~1024 keys): each warp gathers its share of the chunks' segments
 //                  straight into registers and inserts two keys per lane in lockstep into a 2048-slot
-//                  SMEM table (A_t restricted to the bucket); the occupied slots, compacted, give unique
-//                  links, max link, count sum (-> window accumulators) and one record (node << 32 |
-//                  count) per link and side, stored by node bucket into the bucket's record row;
+//                  SMEM table (A_t restricted to the bucket); a key that claims a free slot is a new link:
+//                  it is listed (claim list) and counted in its two node buckets' histograms right then.
+//                  The list gives unique links, max link, count sum (-> window accumulators) and one
+//                  record (node << 32 | count) per link and side, stored by node bucket into the
+//                  bucket's record row;
 //   side  (w,s,q)  node bucket q of side s: the records of every link bucket merged per node in a
-//                  4096-slot SMEM table of (node, packets | fan << 20): unique nodes, max packets, max
-//                  fan -> window accumulators; the last side item of a window writes its row.
+//                  4096-slot SMEM table of (node, packets | fan << 20); unique nodes (claimed slots), max
+//                  packets and max fan come from the adds' return values (no table scan) -> window
+//                  accumulators; the last side item of a window writes its row.
 // Tables are probed with a plain load first (a hot key's repeats cost a broadcast read and an
 // aggregated increment, never a CAS); collisions probe on with double hashing (odd steps).
 #pragma once
@@ -31,7 +34,10 @@ namespace flat {
 constexpr int CH = 4096;                      // keys per partition item
 constexpr int PTH = 256;                      // partition CTA threads
 constexpr int LTH = 256;                      // link CTA threads
-constexpr int STH = 256;                      // side CTA threads
+#ifndef NSG_STH
+#define NSG_STH 256
+#endif
+constexpr int STH = NSG_STH;                  // side CTA threads
 constexpr u64 BK = 1024;                      // target keys per link bucket / nodes per side bucket
 constexpr u64 MAX_W = 1ull << 17;             // windows this path takes (<= 128 link / side buckets)
 constexpr int MAXB = (int)(MAX_W / BK);          // link buckets of the largest window (= 2 x node buckets)
@@ -340,17 +346,16 @@ struct SmemL {
   u64 lkey[TL];
   u32 lcnt[TL];
   u32 hist[MAXB], offs[MAXB];      // per (side, node bucket): 2 * Bs <= MAXB
-  uint16_t claim[FILL_L];          // the bucket's occupied slots
+  uint16_t claim[FILL_L];          // the bucket's occupied slots, listed as they are claimed
   u32 segscr[LTH / 32][64];
-  u32 red[4][LTH / 32];
-  u32 ncl, esc, ovf, L0, vbase;
+  u32 ncl, esc, ovf, vbase;
 };
 
 // Lockstep probe of two keys per lane: every lane advances its unfinished keys by one slot per
 // iteration (a found key, or a free slot claimed by CAS, finishes it), so the warp runs as many short
 // iterations as its longest probe sequence and never serialises divergent probe loops.
 // In: slot = home slot, cur = its content, act = key valid.  Out: slot = the key's slot.
-// Returns the number of slots claimed by this lane.
+// Returns which keys this lane inserted as new (bit 0: key a claimed a free slot, bit 1: key b).
 template <class T, class Step>
 __device__ __forceinline__ u32 probe2(T* keys, u32 mask, T ka, T kb, u32& sa, u32& sb, T ca, T cb, bool aa, bool ab,
                                       u32* ovf, Step step) {
@@ -363,12 +368,12 @@ __device__ __forceinline__ u32 probe2(T* keys, u32 mask, T ka, T kb, u32& sa, u3
   for (u32 it = 0;; ++it) {
     if (aa && ca == EMPTY) {
       const T o = atomicCAS(&keys[sa], EMPTY, ka);
-      claimed += o == EMPTY;
+      claimed |= o == EMPTY ? 1u : 0u;
       ca = o == EMPTY ? ka : o;
     }
     if (ab && cb == EMPTY) {
       const T o = atomicCAS(&keys[sb], EMPTY, kb);
-      claimed += o == EMPTY;
+      claimed |= o == EMPTY ? 2u : 0u;
       cb = o == EMPTY ? kb : o;
     }
     aa = aa && ca != ka;
@@ -434,8 +439,8 @@ link_kernel(const FGeo g) {
       u32 sa = link_slot(ka, logB), sb = link_slot(kc, logB);
       const u64 ca = *reinterpret_cast<volatile u64*>(&s.lkey[sa]);
       const u64 cb = *reinterpret_cast<volatile u64*>(&s.lkey[sb]);
-      probe2<unsigned long long>(reinterpret_cast<unsigned long long*>(s.lkey), TL - 1, ka, kc, sa, sb, ca, cb, aa, ab,
-                                 &s.ovf, [](u64 k) { return link_step(k); });
+      const u32 cl = probe2<unsigned long long>(reinterpret_cast<unsigned long long*>(s.lkey), TL - 1, ka, kc, sa, sb,
+                                                ca, cb, aa, ab, &s.ovf, [](u64 k) { return link_step(k); });
       if (WT) {
         if (aa) atomicAdd(&s.lcnt[sa], wa);
         if (ab) atomicAdd(&s.lcnt[sb], wc);
@@ -443,101 +448,63 @@ link_kernel(const FGeo g) {
         if (aa) atomicAdd(&s.lcnt[sa], 1u);
         if (ab) atomicAdd(&s.lcnt[sb], 1u);
       }
+      // a new link: counted in its two node buckets' histograms and listed, when its slot is claimed
+      if (cl & 1u) {
+        atomicAdd(&s.hist[node_bucket((u32)(ka >> 32), logBs)], 1u);
+        atomicAdd(&s.hist[Bs + node_bucket((u32)ka, logBs)], 1u);
+      }
+      if (cl & 2u) {
+        atomicAdd(&s.hist[node_bucket((u32)(kc >> 32), logBs)], 1u);
+        atomicAdd(&s.hist[Bs + node_bucket((u32)kc, logBs)], 1u);
+      }
+      const u32 ma = __ballot_sync(0xffffffffu, cl & 1u), mb = __ballot_sync(0xffffffffu, cl & 2u);
+      if (ma | mb) {
+        u32 p = 0;
+        if (lane == 0) p = atomicAdd(&s.ncl, __popc(ma) + __popc(mb));
+        p = __shfl_sync(0xffffffffu, p, 0);
+        const u32 lt = (1u << lane) - 1u;
+        const u32 pa = p + __popc(ma & lt), pb = p + __popc(ma) + __popc(mb & lt);
+        if ((cl & 1u) && pa < FILL_L) s.claim[pa] = (uint16_t)sa;
+        if ((cl & 2u) && pb < FILL_L) s.claim[pb] = (uint16_t)sb;
+      }
     }
     nesc = __reduce_add_sync(0xffffffffu, nesc);
     if (lane == 0 && nesc) atomicAdd(&s.esc, nesc);
   }
-  __syncthreads();  // every key of the bucket is counted
-  // ---- final: the occupied slots compacted into the claim list, then visited densely
-  constexpr int SPT = TL / LTH;  // slots per thread: [t * SPT, t * SPT + SPT)
-  static_assert(SPT % 4 == 0 && SPT <= 32, "slots are scanned 4 at a time");
-  {
-    u32 occ = 0;
-#pragma unroll
-    for (int j = 0; j < SPT; j += 4) {
-      const uint4 c4 = *reinterpret_cast<const uint4*>(&s.lcnt[t * SPT + j]);
-      occ |= (c4.x ? 1u : 0u) << j | (c4.y ? 2u : 0u) << j | (c4.z ? 4u : 0u) << j | (c4.w ? 8u : 0u) << j;
-    }
-    const u32 c = __popc(occ);
-    u32 x = c;
-#pragma unroll
-    for (int k = 1; k < 32; k <<= 1) {
-      const u32 y = __shfl_up_sync(0xffffffffu, x, k);
-      if (lane >= k) x += y;
-    }
-    u32 base = 0;
-    if (lane == 31 && x) base = atomicAdd(&s.ncl, x);
-    u32 p = __shfl_sync(0xffffffffu, base, 31) + x - c;
-#pragma unroll
-    for (int j = 0; j < SPT; ++j)
-      if (occ >> j & 1u) {
-        if (p < FILL_L) s.claim[p] = (uint16_t)(t * SPT + j);
-        ++p;
-      }
-  }
-  __syncthreads();
-  const bool ovf = s.ovf != 0 || s.ncl > FILL_L;  // more links than the records take: L2 path
-  const u32 ncl = ovf ? 0u : s.ncl;
-  u32 nl = 0, mx = 0, sm = 0;
-  for (u32 e = t; e < ncl; e += LTH) {
-    const u32 sl = s.claim[e];
-    const u32 c = s.lcnt[sl];
-    const u64 key = s.lkey[sl];
-    nl += 1; mx = max(mx, c); sm += c;
-    atomicAdd(&s.hist[node_bucket((u32)(key >> 32), logBs)], 1u);
-    atomicAdd(&s.hist[Bs + node_bucket((u32)key, logBs)], 1u);
-  }
-  const u32 esc = s.esc;
+  __syncthreads();  // every key of the bucket is counted, listed and histogrammed
+  const u32 ncl = s.ncl, esc = s.esc;
   const u32 eb = node_bucket(EMPTY32, logBs);
-  if (t == 0 && esc && !ovf) {  // the key ~0 (kept out of the table) is one more link
-    nl += 1; mx = max(mx, esc); sm += esc;
-    atomicAdd(&s.hist[eb], 1u);
-    atomicAdd(&s.hist[Bs + eb], 1u);
-  }
-  {
-    u32 z = 0;
-    warp_reduce4(nl, mx, z, sm);
-    if (lane == 0) { s.red[0][wid] = nl; s.red[1][wid] = mx; s.red[3][wid] = sm; }
-  }
-  __syncthreads();
   u32* ro = g.roff + ((u64)wb * B + b) * 2 * Bs;  // this item's own row
-  if (ovf) {
+  if (s.ovf != 0 || ncl > FILL_L) {  // more links than the records take (or a full table): L2 path
     if (t == 0) g.ws[w].ovf = 1;
     for (u32 i = t; i < 2 * Bs; i += LTH) ro[i] = 0;
     return;
   }
-  if (wid == 0) {
-    u32 a = lane < (int)NW ? s.red[0][lane] : 0u, m2 = lane < (int)NW ? s.red[1][lane] : 0u, z = 0,
-        d = lane < (int)NW ? s.red[3][lane] : 0u;
-    warp_reduce4(a, m2, z, d);
-    if (lane == 0 && a) {
-      WinState* st = &g.ws[w];
-      atomicAdd(&st->links, a);
-      atomicMax(&st->maxc, m2);
-      atomicAdd(&st->sumc, d);
-      if (g.v_lkey) s.vbase = atomicAdd(&st->vfill[0], a);  // this bucket's link-vector entries
-    }
-  }
-  if (wid < 2) {  // side-0 records first, then side 1 from L0 = number of links (= sum of the side-0 counts)
-    u32 L0 = 0;
-    if (wid == 1)
-      for (u32 i = lane; i < Bs; i += 32) L0 += s.hist[i];
-    L0 = warp_sum(L0);
+  const u32 nl = ncl + (esc ? 1u : 0u);  // the key ~0 (kept out of the table) is one more link
+  if (wid < 2) {  // side-0 records first, then side 1 from nl (= the number of side-0 records)
+    if (lane == 0 && esc) atomicAdd(&s.hist[wid * Bs + eb], 1u);
+    __syncwarp();
     u32* r = ro + wid * Bs;
-    const u32 tot = warp_exscan(s.hist + wid * Bs, s.offs + wid * Bs, Bs, lane, [&](u32 i, u32 ex, u32 v) {
-      r[i] = ((L0 + ex) << 16) | v;
-      s.offs[wid * Bs + i] = L0 + ex;
+    const u32 o0 = wid ? nl : 0u;
+    warp_exscan(s.hist + wid * Bs, s.offs + wid * Bs, Bs, lane, [&](u32 i, u32 ex, u32 v) {
+      r[i] = ((o0 + ex) << 16) | v;
+      s.offs[wid * Bs + i] = o0 + ex;
     });
-    if (wid == 0 && lane == 0) s.L0 = tot;
+    if (t == 0) {
+      atomicAdd(&g.ws[w].links, nl);
+      if (g.v_lkey) s.vbase = atomicAdd(&g.ws[w].vfill[0], nl);  // this bucket's link-vector entries
+    }
   }
   __syncthreads();
   // records (node << 32 | count) straight to the item's record row, placed by side bucket with a
-  // cursor per bucket (side 0 first, then side 1 from L0)
+  // cursor per bucket (side 0 first, then side 1 from nl); max / sum of the link counts on the way
   u64* rrow = g.rscr + ((u64)wb * B + b) * RCAP;
+  u32 mx = 0, sm = 0;
   for (u32 e = t; e < ncl; e += LTH) {
     const u32 sl = s.claim[e];
     const u32 c = s.lcnt[sl];
     const u64 key = s.lkey[sl];
+    mx = max(mx, c); sm += c;
     const u32 p0 = atomicAdd(&s.offs[node_bucket((u32)(key >> 32), logBs)], 1u);
     const u32 p1 = atomicAdd(&s.offs[Bs + node_bucket((u32)key, logBs)], 1u);
     __stcg(reinterpret_cast<unsigned long long*>(rrow + p0), (key & 0xFFFFFFFF00000000ull) | c);
@@ -549,6 +516,7 @@ link_kernel(const FGeo g) {
     }
   }
   if (t == 0 && esc) {
+    mx = max(mx, esc); sm += esc;
     rrow[atomicAdd(&s.offs[eb], 1u)] = ((u64)EMPTY32 << 32) | esc;
     rrow[atomicAdd(&s.offs[Bs + eb], 1u)] = ((u64)EMPTY32 << 32) | esc;
     if (g.v_lkey) {
@@ -556,6 +524,12 @@ link_kernel(const FGeo g) {
       g.v_lkey[at] = EMPTY64;
       g.v_lpk[at] = esc;
     }
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  sm = __reduce_add_sync(0xffffffffu, sm);
+  if (lane == 0 && sm) {
+    atomicMax(&g.ws[w].maxc, mx);
+    atomicAdd(&g.ws[w].sumc, sm);
   }
 }
 
@@ -574,42 +548,50 @@ struct SmemS {
 // packets += c, fan += 1 for the node in slot `slot`.  An item with fewer than 4096 records cannot
 // carry a fan past the 12-bit field: a fire-and-forget add.  Otherwise a fan field that passes 4095 is
 // noted in the wrap list.
-__device__ __forceinline__ void node_add(SmemS& s, u32 slot, u32 c, bool wrapcheck) {
-  if (!wrapcheck) { atomicAdd(&s.npf[slot], c | (1u << PFS)); return; }
-  const u32 o = atomicAdd(&s.npf[slot], c | (1u << PFS));
-  if ((o >> PFS) == FMAX) {
+__device__ __forceinline__ u32 node_add(SmemS& s, u32 slot, u32 c, bool wrapcheck) {
+  const u32 a = c | (1u << PFS);
+  const u32 o = atomicAdd(&s.npf[slot], a);
+  if (wrapcheck && (o >> PFS) == FMAX) {
     const u32 i = atomicAdd(&s.nwrap, 1u);
     if (i < (u32)WRAPCAP) s.wrap[i] = slot;
     else s.ovf = 1;
   }
+  return o + a;  // the slot's packets | fan << 20 after this record (fan modulo 4096)
 }
 
 // One lane merges a cached node's totals (packets P, fan F, F possibly > 4095) into the table: probe to
 // its slot, then add in steps of at most 4095 fan so that every wrap of the 12-bit field is recorded.
-__device__ __noinline__ void node_merge(SmemS& s, u32 node, u32 P, u32 F, u32 logBs) {
+// Returns 1 if the node was new to the table; folds the slot's final packets / fan (mod 4096) into mp, mf.
+__device__ __noinline__ u32 node_merge(SmemS& s, u32 node, u32 P, u32 F, u32 logBs, u32& mp, u32& mf) {
   u32 sl = node_slot(node, logBs);
   const u32 stp = node_step(node);
+  u32 fresh = 0;
   for (u32 probe = 0;; ++probe) {
     const u32 cur = *reinterpret_cast<volatile u32*>(&s.nkey[sl]);
     if (cur == node) break;
     if (cur == EMPTY32) {
       const u32 o = atomicCAS(&s.nkey[sl], EMPTY32, node);
-      if (o == EMPTY32 || o == node) break;
+      if (o == EMPTY32) { fresh = 1; break; }
+      if (o == node) break;
       continue;  // re-read this slot
     }
-    if (probe >= (u32)TS) { s.ovf = 1; return; }
+    if (probe >= (u32)TS) { s.ovf = 1; return 0; }
     sl = (sl + stp) & (TS - 1);
   }
   for (bool first = true; F; first = false) {
     const u32 a = min(F, FMAX);
-    const u32 o = atomicAdd(&s.npf[sl], (first ? P : 0u) | (a << PFS));
+    const u32 add = (first ? P : 0u) | (a << PFS);
+    const u32 o = atomicAdd(&s.npf[sl], add);
     if ((o >> PFS) + a > FMAX) {
       const u32 i = atomicAdd(&s.nwrap, 1u);
       if (i < (u32)WRAPCAP) s.wrap[i] = sl;
       else s.ovf = 1;
     }
+    mp = max(mp, (o + add) & PMASK);
+    mf = max(mf, (o + add) >> PFS);
     F -= a;
   }
+  return fresh;
 }
 
 // Is `node` in the (complete) node table?
@@ -661,7 +643,7 @@ __device__ void finalize(const FGeo& g, u64 w, u64* out) {
   for (u32 m = 0; m < g.n_mirror; ++m) store_row(g.mirror[m] + (g.mirror_row0 + w) * NSG_NUM_STATS, row);
 }
 
-__global__ void __launch_bounds__(STH, 6)
+__global__ void __launch_bounds__(STH, 1536 / STH)
 side_kernel(const FGeo g, u64* __restrict__ out) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemS& s = *reinterpret_cast<SmemS*>(smem_raw);
@@ -685,6 +667,9 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
   const bool wrapcheck = ntot > FMAX;
   const bool heavy = ntot > HEAVY_S;
   const u64* rb = g.rscr + (u64)wb * B * RCAP;
+  // unique nodes (slots this thread claimed), max packets and max fan (mod 4096) of the table, taken from
+  // the adds' return values (every slot's final value is the largest of its returns)
+  u32 nn = 0, mp = 0, mf = 0;
   {
     u32 escP = 0, escF = 0;
     u64 nxa = ~0ull, nxc = ~0ull;  // the next step's records, loaded while this step's are merged
@@ -713,13 +698,20 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
       if (ab && nb == hot) { hP += (u32)rc; ++hF; ab = false; }
       const u32 ca = aa ? *reinterpret_cast<volatile u32*>(&s.nkey[sa]) : 0u;
       const u32 cb = ab ? *reinterpret_cast<volatile u32*>(&s.nkey[sb]) : 0u;
-      probe2<u32>(s.nkey, TS - 1, na, nb, sa, sb, ca, cb, aa, ab, &s.ovf, [](u32 k) { return node_step(k); });
-      if (aa) node_add(s, sa, (u32)ra, wrapcheck);
-      if (ab) node_add(s, sb, (u32)rc, wrapcheck);
+      const u32 cl = probe2<u32>(s.nkey, TS - 1, na, nb, sa, sb, ca, cb, aa, ab, &s.ovf, [](u32 k) { return node_step(k); });
+      nn += __popc(cl);
+      if (aa) {
+        const u32 v = node_add(s, sa, (u32)ra, wrapcheck);
+        mp = max(mp, v & PMASK); mf = max(mf, v >> PFS);
+      }
+      if (ab) {
+        const u32 v = node_add(s, sb, (u32)rc, wrapcheck);
+        mp = max(mp, v & PMASK); mf = max(mf, v >> PFS);
+      }
     }
     hP = __reduce_add_sync(0xffffffffu, hP);
     hF = __reduce_add_sync(0xffffffffu, hF);
-    if (lane == 0 && hF) node_merge(s, hot, hP, hF, logBs);
+    if (lane == 0 && hF) nn += node_merge(s, hot, hP, hF, logBs, mp, mf);
     escF = __reduce_add_sync(0xffffffffu, escF);
     escP = __reduce_add_sync(0xffffffffu, escP);
     if (lane == 0 && escF) { atomicAdd(&s.escP, escP); atomicAdd(&s.escF, escF); }
@@ -737,19 +729,16 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
   const bool ovf = s.ovf != 0;
   constexpr int SPT = TS / STH;
   static_assert(SPT % 4 == 0, "slots are scanned 4 at a time");
-  u32 nn = 0, mp = 0, mf = wrapmax;
-#pragma unroll
-  for (int j = 0; j < SPT; j += 4) {
-    const uint4 p4 = *reinterpret_cast<const uint4*>(&s.npf[t * SPT + j]);
-    const u32 ps[4] = {p4.x, p4.y, p4.z, p4.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (ps[i]) { nn += 1; mp = max(mp, ps[i] & PMASK); mf = max(mf, ps[i] >> PFS); }
-  }
   const u32 side = q >= Bs ? 1u : 0u;
   const bool emit = g.v_node[side] != nullptr || (g.v_ipsets && side == 0);
   u32 vpre = 0;  // vectors / IP sets: this thread's first entry among the item's table nodes
-  if (emit) {
+  if (emit) {  // the nodes are listed in slot order: this thread's slots [t * SPT, t * SPT + SPT)
+    nn = 0;
+#pragma unroll
+    for (int j = 0; j < SPT; j += 4) {
+      const uint4 p4 = *reinterpret_cast<const uint4*>(&s.npf[t * SPT + j]);
+      nn += (p4.x ? 1u : 0u) + (p4.y ? 1u : 0u) + (p4.z ? 1u : 0u) + (p4.w ? 1u : 0u);
+    }
     u32 x = nn;
 #pragma unroll
     for (int k = 1; k < 32; k <<= 1) {
@@ -758,6 +747,7 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
     }
     vpre = x - nn;
   }
+  mf = max(mf, wrapmax);
   const u32 escF = s.escF, escP = s.escP;
   if (t == 0 && escF) { nn += 1; mp = max(mp, escP); mf = max(mf, escF); }
   u32 z = 0;
