@@ -247,7 +247,7 @@ def main():
     ap.add_argument("--l2", choices=["cold", "warm"], default="cold",
                     help="cold: steps cycle through a 1 GiB ring of batches (never L2-resident; the default and the "
                          "headline); warm: one 64 MiB batch reused every step (L2-resident input, SURVEY §8(d))")
-    ap.add_argument("--streams", type=int, default=2,
+    ap.add_argument("--streams", type=int, default=3,
                     help="default path at N=1: consecutive batches alternate over this many CUDA streams with "
                          "their own workspaces, so a batch's pipeline fill overlaps the previous batch's drain")
     ap.add_argument("--graphs", type=int, default=1,
@@ -560,6 +560,22 @@ def main():
             r = nsg.window_stats_weighted(keys_dev, wdev, WINDOW, out=outs[0], workspace=ws)
             out_host.copy_(r, non_blocking=True)
         d2h_bytes = WINDOWS_PER_STEP * 9 * 8
+    elif world == 1 and nstreams > 1:
+        # Consecutive steps overlap: step i runs on lane i mod L (its own stream, device buffers, workspace and
+        # pinned result), every step still copies its keys host -> device and its result back; the H2D copies
+        # of all lanes share one copy stream, so the PCIe link is never idle while a lane computes.
+        lanes = min(nstreams, 2)
+        lane_s = [torch.cuda.Stream(dev) for _ in range(lanes)]
+        lane_keys = [keys_dev] + [torch.empty(n, dtype=torch.int64, device=dev) for _ in range(lanes - 1)]
+        lane_oh = [out_host] + [torch.empty((wps, 9), dtype=torch.int64, pin_memory=True) for _ in range(lanes - 1)]
+        lane_i = [0]
+
+        def e2e_once():
+            j = lane_i[0] % lanes
+            lane_i[0] += 1
+            nsg.window_stats_from_host(host, WINDOW, device=dev, keys_dev=lane_keys[j], out=outs[j],
+                                       out_host=lane_oh[j], workspace=wss[j], stream=lane_s[j], synchronize=False)
+        d2h_bytes = wps * 9 * 8
     else:
         def e2e_once():
             nsg.window_stats_from_host(host, WINDOW, device=dev, keys_dev=keys_dev, out=outs[0], out_host=out_host,
@@ -574,8 +590,12 @@ def main():
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    for s_ in (lane_s if world == 1 and nstreams > 1 and not (vec or anon or trace or wtd) else []):
+        s_.wait_event(e0)  # the lanes start after e0
     for _ in range(e2e_steps):
         e2e_once()
+    for s_ in (lane_s if world == 1 and nstreams > 1 and not (vec or anon or trace or wtd) else []):
+        torch.cuda.current_stream(dev).wait_stream(s_)  # e1 after every lane's last D2H
     e1.record()
     torch.cuda.synchronize(dev)
     e2e_ms = e0.elapsed_time(e1)
@@ -635,7 +655,9 @@ def main():
                                        "and stream)" if graphs else "no")},
             "value_without_gather": value_no_gather if world > 1 else None,
             "e2e": {"value": e2e_value, "unit": "rows/s" if wtd else UNIT, "h2d_bytes_per_step": n * (12 if wtd else 8),
-                    "d2h_bytes_per_step": d2h_bytes, "steps": e2e_steps},
+                    "d2h_bytes_per_step": d2h_bytes, "steps": e2e_steps,
+                    "overlap": ("consecutive steps on 2 streams (H2D of one step while the previous one computes)"
+                                if world == 1 and nstreams > 1 and not (vec or anon or trace or wtd) else "none")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "frac_vs_nominal_8000": achieved / 8000.0,
                          "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,

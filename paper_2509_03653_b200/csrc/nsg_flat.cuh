@@ -351,31 +351,51 @@ struct SmemL {
   u32 ncl, esc, ovf, vbase;
 };
 
+// Shared-memory slot operations on 32-bit shared-window addresses, predicated (no branch, no reconvergence
+// bookkeeping around each one): p ? op : keep the register's value.
+__device__ __forceinline__ u32 smem_addr(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void sld_if(bool p, u32 a, u64& v) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.volatile.shared.u64 %0, [%1]; }"
+               : "+l"(v) : "r"(a), "r"((u32)p) : "memory");
+}
+__device__ __forceinline__ void sld_if(bool p, u32 a, u32& v) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q ld.volatile.shared.u32 %0, [%1]; }"
+               : "+r"(v) : "r"(a), "r"((u32)p) : "memory");
+}
+__device__ __forceinline__ void scas_if(bool p, u32 a, u64 cmp, u64 val, u64& old) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %4, 0; @q atom.shared.cas.b64 %0, [%1], %2, %3; }"
+               : "+l"(old) : "r"(a), "l"(cmp), "l"(val), "r"((u32)p) : "memory");
+}
+__device__ __forceinline__ void scas_if(bool p, u32 a, u32 cmp, u32 val, u32& old) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %4, 0; @q atom.shared.cas.b32 %0, [%1], %2, %3; }"
+               : "+r"(old) : "r"(a), "r"(cmp), "r"(val), "r"((u32)p) : "memory");
+}
+
 // Lockstep probe of two keys per lane: every lane advances its unfinished keys by one slot per
 // iteration (a found key, or a free slot claimed by CAS, finishes it), so the warp runs as many short
-// iterations as its longest probe sequence and never serialises divergent probe loops.
-// In: slot = home slot, cur = its content, act = key valid.  Out: slot = the key's slot.
-// Returns which keys this lane inserted as new (bit 0: key a claimed a free slot, bit 1: key b).
+// iterations as its longest probe sequence and never serialises divergent probe loops.  Every slot
+// operation is predicated on the lane's key still being unfinished.
+// In: tab = shared address of slot 0, slot = home slot, cur = its content, act = key valid.
+// Out: slot = the key's slot.  Returns which keys this lane inserted as new (bit 0: key a claimed a free
+// slot, bit 1: key b).
 template <class T, class Step>
-__device__ __forceinline__ u32 probe2(T* keys, u32 mask, T ka, T kb, u32& sa, u32& sb, T ca, T cb, bool aa, bool ab,
+__device__ __forceinline__ u32 probe2(u32 tab, u32 mask, T ka, T kb, u32& sa, u32& sb, T ca, T cb, bool aa, bool ab,
                                       u32* ovf, Step step) {
   constexpr T EMPTY = ~T(0);
+  constexpr u32 SZ = sizeof(T);
   u32 claimed = 0;
   aa = aa && ca != ka;
   ab = ab && cb != kb;
   if (!__any_sync(0xffffffffu, aa || ab)) return 0;
   const u32 pa = step(ka), pb = step(kb);
   for (u32 it = 0;; ++it) {
-    if (aa && ca == EMPTY) {
-      const T o = atomicCAS(&keys[sa], EMPTY, ka);
-      claimed |= o == EMPTY ? 1u : 0u;
-      ca = o == EMPTY ? ka : o;
-    }
-    if (ab && cb == EMPTY) {
-      const T o = atomicCAS(&keys[sb], EMPTY, kb);
-      claimed |= o == EMPTY ? 2u : 0u;
-      cb = o == EMPTY ? kb : o;
-    }
+    const bool xa = aa && ca == EMPTY, xb = ab && cb == EMPTY;  // a free slot: claim it
+    T oa = ca, ob = cb;
+    scas_if(xa, tab + sa * SZ, EMPTY, ka, oa);
+    scas_if(xb, tab + sb * SZ, EMPTY, kb, ob);
+    claimed |= (xa && oa == EMPTY ? 1u : 0u) | (xb && ob == EMPTY ? 2u : 0u);
+    ca = oa == EMPTY ? ka : oa;  // (not claimed: oa = ca)
+    cb = ob == EMPTY ? kb : ob;
     aa = aa && ca != ka;
     ab = ab && cb != kb;
     if (!__any_sync(0xffffffffu, aa || ab)) break;
@@ -383,14 +403,19 @@ __device__ __forceinline__ u32 probe2(T* keys, u32 mask, T ka, T kb, u32& sa, u3
       if (aa || ab) *ovf = 1;
       break;
     }
-    if (aa) { sa = (sa + pa) & mask; ca = *reinterpret_cast<volatile T*>(&keys[sa]); }
-    if (ab) { sb = (sb + pb) & mask; cb = *reinterpret_cast<volatile T*>(&keys[sb]); }
+    sa = aa ? (sa + pa) & mask : sa;
+    sb = ab ? (sb + pb) & mask : sb;
+    sld_if(aa, tab + sa * SZ, ca);
+    sld_if(ab, tab + sb * SZ, cb);
   }
   return claimed;
 }
 
+#ifndef NSG_LINK_MINB
+#define NSG_LINK_MINB 7  // link CTAs per SM (7 x 30 KB shared memory; 32 registers)
+#endif
 template <bool WT>
-__global__ void __launch_bounds__(LTH, 7)
+__global__ void __launch_bounds__(LTH, NSG_LINK_MINB)
 link_kernel(const FGeo g) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemL& s = *reinterpret_cast<SmemL*>(smem_raw);
@@ -439,8 +464,8 @@ link_kernel(const FGeo g) {
       u32 sa = link_slot(ka, logB), sb = link_slot(kc, logB);
       const u64 ca = *reinterpret_cast<volatile u64*>(&s.lkey[sa]);
       const u64 cb = *reinterpret_cast<volatile u64*>(&s.lkey[sb]);
-      const u32 cl = probe2<unsigned long long>(reinterpret_cast<unsigned long long*>(s.lkey), TL - 1, ka, kc, sa, sb,
-                                                ca, cb, aa, ab, &s.ovf, [](u64 k) { return link_step(k); });
+      const u32 cl = probe2<u64>(smem_addr(s.lkey), TL - 1, ka, kc, sa, sb, ca, cb, aa, ab, &s.ovf,
+                                 [](u64 k) { return link_step(k); });
       if (WT) {
         if (aa) atomicAdd(&s.lcnt[sa], wa);
         if (ab) atomicAdd(&s.lcnt[sb], wc);
@@ -698,7 +723,8 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
       if (ab && nb == hot) { hP += (u32)rc; ++hF; ab = false; }
       const u32 ca = aa ? *reinterpret_cast<volatile u32*>(&s.nkey[sa]) : 0u;
       const u32 cb = ab ? *reinterpret_cast<volatile u32*>(&s.nkey[sb]) : 0u;
-      const u32 cl = probe2<u32>(s.nkey, TS - 1, na, nb, sa, sb, ca, cb, aa, ab, &s.ovf, [](u32 k) { return node_step(k); });
+      const u32 cl = probe2<u32>(smem_addr(s.nkey), TS - 1, na, nb, sa, sb, ca, cb, aa, ab, &s.ovf,
+                                 [](u32 k) { return node_step(k); });
       nn += __popc(cl);
       if (aa) {
         const u32 v = node_add(s, sa, (u32)ra, wrapcheck);

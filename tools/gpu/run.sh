@@ -6,6 +6,8 @@
 #   tests       pytest -m gpu (the parity suite)                       -> gpurun_out/gpu_tests.log
 #   (order matters: run `traffic` before `bench`, so that the bench line reports the traffic of its own build)
 #   bench       bench.py C2 line (200 steps)                           -> gpurun_out/bench_C2.json
+#   benches     the C1 / C3 / vectors / weighted / L2-warm / Zipf-exponent lines and the reference arm
+#                                                                       -> gpurun_out/bench_*.json
 #   quick       parity spot set + C2 call time vs the round-1 kernel (tools/r2_quick.py), C1/C2/C3 call times
 #               (tools/c3_time.py)                                     -> gpurun_out/quick.log
 #   profiles    launch list of a bench run + ncu --set full of part/link/side on a C2 call, summarised by
@@ -28,6 +30,15 @@ for cmd in "$@"; do
   bench)
     timeout 900 python bench.py --steps 200 --warmup 10 > gpurun_out/bench_C2.json 2> gpurun_out/bench_C2.err
     tail -c 400 gpurun_out/bench_C2.json ;;
+  benches)  # the other bench lines of profiles/r02/ (workloads, output modes, the reference arm)
+    for spec in "C1:--workload C1" "C3:--workload C3" "C2_vectors:--outputs vectors" "C2_weighted:--input weighted" \
+                "C2_l2warm:--l2 warm" "Z08:--workload Z08" "Z13:--workload Z13" "Z15:--workload Z15"; do
+      name=${spec%%:*}; a=${spec#*:}
+      timeout 600 python bench.py --steps 200 --warmup 10 $a > gpurun_out/bench_$name.json 2> gpurun_out/bench_$name.err
+      echo "$name: $(tail -c 300 gpurun_out/bench_$name.json | head -c 300)"
+    done
+    timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
+    tail -c 200 gpurun_out/bench_reference.json ;;
   quick)
     { timeout 300 python tools/r2_quick.py --reps 20; timeout 300 python tools/c3_time.py; } > gpurun_out/quick.log 2>&1
     grep -v "parity OK" gpurun_out/quick.log ;;
