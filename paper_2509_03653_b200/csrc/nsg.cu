@@ -397,12 +397,14 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
       g_last_launches += 3;
       if (cudaGetLastError() != cudaSuccess) return NSG_ERR_CUDA;
     }
+#ifndef NSG_NO_DISCARD
     {  // the scratch is dead: drop it from L2 (no write-back of dirty scratch lines to HBM)
       const u64 bytes = (u64)(L.o_fend - L.o_fkscr);
       const u32 blocks = (u32)std::min<u64>((bytes / 128 + 255) / 256, (u64)4 * 148);
       flat::discard_kernel<<<blocks, 256, 0, s>>>(base + L.o_fkscr, bytes);
       g_last_launches++;
     }
+#endif
     if (ev_after && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_after), s) != cudaSuccess) return NSG_ERR_CUDA;
     if (ev_copied && cudaStreamWaitEvent(s, ev_copied, 0) != cudaSuccess) return NSG_ERR_CUDA;
     if (!(flags & NSG_FLAG_NO_FALLBACK_CHECK)) {
