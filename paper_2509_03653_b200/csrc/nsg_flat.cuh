@@ -50,6 +50,12 @@ constexpr u32 PMASK = (1u << PFS) - 1;
 constexpr u32 FMAX = 0xFFFu;                  // fan field: 12 bits; items with >= 4096 records track wraps
 constexpr int WRAPCAP = 64;
 constexpr u32 HEAVY_S = 8192;                 // side items with more records cache a hot node per warp
+#ifndef NSG_AGG_T
+#define NSG_AGG_T 128
+#endif
+constexpr u32 AGG_T = NSG_AGG_T;              // a link bucket's node-bucket group with this many links sends one
+                                              // record per node (P, F) instead of one per link (heavy hitters)
+constexpr int LOG_TA = 7, TA = 1 << LOG_TA;   // per-side aggregation table slots of a link item
 constexpr u64 MUL_L = 0x9E3779B97F4A7C15ull;  // link hash: top bits of key * phi64
 constexpr u32 MUL_N = 0x9E3779B9u;            // node hash: top bits of node * phi32
 static_assert((RCAP * 8) % 128 == 0, "record rows are whole 128-B lines (16-B stores, L2 discards)");
@@ -347,9 +353,14 @@ struct SmemL {
   u32 lcnt[TL];
   u32 hist[MAXB], offs[MAXB];      // per (side, node bucket): 2 * Bs <= MAXB
   uint16_t claim[FILL_L];          // the bucket's occupied slots, listed as they are claimed
-  u32 segscr[LTH / 32][64];
+  union {
+    u32 segscr[LTH / 32][64];      // warp_segs (before the table is initialised)
+    u32 agg[2][2][TA];             // then per side: node, packets | links << 20 of the heavy groups' nodes
+  };
+  u32 hmask[MAXB / 32];            // heavy groups (side * Bs + node bucket with >= AGG_T links)
   u32 ncl, esc, ovf, vbase;
 };
+static_assert(sizeof(u32) * 2 * 2 * TA <= sizeof(u32) * (LTH / 32) * 64, "aggregation tables fit the segment scratch");
 
 // Shared-memory slot operations on 32-bit shared-window addresses, predicated (no branch, no reconvergence
 // bookkeeping around each one): p ? op : keep the register's value.
@@ -411,6 +422,25 @@ __device__ __forceinline__ u32 probe2(u32 tab, u32 mask, T ka, T kb, u32& sa, u3
   return claimed;
 }
 
+// A heavy group's link: add (packets | 1 << 20) to its node's entry in the side's aggregation table (probing at most
+// 8 slots); false if the table has no room (the link then sends its own record).
+__device__ __forceinline__ bool agg_add(u32 (*tab)[TA], u32 node, u32 pf) {
+  if (node == EMPTY32) return false;  // the address ~0 is the empty marker (its records go as they are)
+  u32 sl = (node * MUL_N) >> (32 - LOG_TA);
+  for (int k = 0; k < 8; ++k, sl = (sl + 1) & (TA - 1)) {
+    u32 cur = *reinterpret_cast<volatile u32*>(&tab[0][sl]);
+    if (cur == EMPTY32) {
+      cur = atomicCAS(&tab[0][sl], EMPTY32, node);
+      if (cur == EMPTY32) cur = node;
+    }
+    if (cur == node) {
+      atomicAdd(&tab[1][sl], pf);
+      return true;
+    }
+  }
+  return false;
+}
+
 #ifndef NSG_LINK_MINB
 #define NSG_LINK_MINB 7  // link CTAs per SM (7 x 30 KB shared memory; 32 registers)
 #endif
@@ -427,6 +457,7 @@ link_kernel(const FGeo g) {
   for (u32 i = t; i < (u32)TL / 2; i += LTH) reinterpret_cast<ulonglong2*>(s.lkey)[i] = make_ulonglong2(EMPTY64, EMPTY64);
   for (u32 i = t; i < (u32)TL / 4; i += LTH) reinterpret_cast<uint4*>(s.lcnt)[i] = make_uint4(0u, 0u, 0u, 0u);
   for (u32 i = t; i < 2 * Bs; i += LTH) s.hist[i] = 0;
+  if (t < MAXB / 32) s.hmask[t] = 0;
   if (t == 0) {
     s.ncl = 0; s.esc = 0;
     s.ovf = WT && ldcg32(&g.ws[w].wtot) >= WTOT_MAX ? 1u : 0u;  // weighted: packets past the 20-bit fields
@@ -506,6 +537,10 @@ link_kernel(const FGeo g) {
     return;
   }
   const u32 nl = ncl + (esc ? 1u : 0u);  // the key ~0 (kept out of the table) is one more link
+  for (u32 i = t; i < 2 * TA; i += LTH) {  // the aggregation tables (the segment scratch is dead)
+    s.agg[i / TA][0][i % TA] = EMPTY32;
+    s.agg[i / TA][1][i % TA] = 0u;
+  }
   if (wid < 2) {  // side-0 records first, then side 1 from nl (= the number of side-0 records)
     if (lane == 0 && esc) atomicAdd(&s.hist[wid * Bs + eb], 1u);
     __syncwarp();
@@ -514,6 +549,10 @@ link_kernel(const FGeo g) {
     warp_exscan(s.hist + wid * Bs, s.offs + wid * Bs, Bs, lane, [&](u32 i, u32 ex, u32 v) {
       r[i] = ((o0 + ex) << 16) | v;
       s.offs[wid * Bs + i] = o0 + ex;
+      if (v >= AGG_T) {  // a heavy group: its row descriptor is rewritten after the aggregation
+        atomicOr(&s.hmask[(wid * Bs + i) >> 5], 1u << ((wid * Bs + i) & 31));
+        s.hist[wid * Bs + i] = o0 + ex;  // its start
+      }
     });
     if (t == 0) {
       atomicAdd(&g.ws[w].links, nl);
@@ -524,16 +563,19 @@ link_kernel(const FGeo g) {
   // records (node << 32 | count) straight to the item's record row, placed by side bucket with a
   // cursor per bucket (side 0 first, then side 1 from nl); max / sum of the link counts on the way
   u64* rrow = g.rscr + ((u64)wb * B + b) * RCAP;
+  const bool anyh = (s.hmask[0] | s.hmask[1] | s.hmask[2] | s.hmask[3]) != 0;  // some group is heavy
   u32 mx = 0, sm = 0;
   for (u32 e = t; e < ncl; e += LTH) {
     const u32 sl = s.claim[e];
     const u32 c = s.lcnt[sl];
     const u64 key = s.lkey[sl];
     mx = max(mx, c); sm += c;
-    const u32 p0 = atomicAdd(&s.offs[node_bucket((u32)(key >> 32), logBs)], 1u);
-    const u32 p1 = atomicAdd(&s.offs[Bs + node_bucket((u32)key, logBs)], 1u);
-    __stcg(reinterpret_cast<unsigned long long*>(rrow + p0), (key & 0xFFFFFFFF00000000ull) | c);
-    __stcg(reinterpret_cast<unsigned long long*>(rrow + p1), (key << 32) | c);
+    const u32 g0 = node_bucket((u32)(key >> 32), logBs), g1 = Bs + node_bucket((u32)key, logBs);
+    const u32 pf = c | (1u << PFS);  // a record: packets | links << 20 (one link)
+    if (!anyh || !(s.hmask[g0 >> 5] >> (g0 & 31) & 1u) || !agg_add(s.agg[0], (u32)(key >> 32), pf))
+      __stcg(reinterpret_cast<unsigned long long*>(rrow + atomicAdd(&s.offs[g0], 1u)), (key & 0xFFFFFFFF00000000ull) | pf);
+    if (!anyh || !(s.hmask[g1 >> 5] >> (g1 & 31) & 1u) || !agg_add(s.agg[1], (u32)key, pf))
+      __stcg(reinterpret_cast<unsigned long long*>(rrow + atomicAdd(&s.offs[g1], 1u)), (key << 32) | pf);
     if (g.v_lkey) {  // A_t(i,j) of the link
       const u64 at = w * g.W + s.vbase + e;
       g.v_lkey[at] = key;
@@ -542,8 +584,8 @@ link_kernel(const FGeo g) {
   }
   if (t == 0 && esc) {
     mx = max(mx, esc); sm += esc;
-    rrow[atomicAdd(&s.offs[eb], 1u)] = ((u64)EMPTY32 << 32) | esc;
-    rrow[atomicAdd(&s.offs[Bs + eb], 1u)] = ((u64)EMPTY32 << 32) | esc;
+    rrow[atomicAdd(&s.offs[eb], 1u)] = ((u64)EMPTY32 << 32) | esc | (1u << PFS);
+    rrow[atomicAdd(&s.offs[Bs + eb], 1u)] = ((u64)EMPTY32 << 32) | esc | (1u << PFS);
     if (g.v_lkey) {
       const u64 at = w * g.W + s.vbase + ncl;
       g.v_lkey[at] = EMPTY64;
@@ -555,6 +597,18 @@ link_kernel(const FGeo g) {
   if (lane == 0 && sm) {
     atomicMax(&g.ws[w].maxc, mx);
     atomicAdd(&g.ws[w].sumc, sm);
+  }
+  if (anyh) {  // heavy groups: one record (node, packets | links << 20) per aggregated node, then their counts
+    __syncthreads();
+    for (u32 i = t; i < 2 * TA; i += LTH) {
+      const u32 side = i / TA, node = s.agg[side][0][i % TA];
+      if (node != EMPTY32)
+        __stcg(reinterpret_cast<unsigned long long*>(rrow + atomicAdd(&s.offs[side * Bs + node_bucket(node, logBs)], 1u)),
+               ((u64)node << 32) | s.agg[side][1][i % TA]);
+    }
+    __syncthreads();
+    for (u32 q = t; q < 2 * Bs; q += LTH)
+      if (s.hmask[q >> 5] >> (q & 31) & 1u) ro[q] = (s.hist[q] << 16) | (s.offs[q] - s.hist[q]);
   }
 }
 
@@ -573,10 +627,11 @@ struct SmemS {
 // packets += c, fan += 1 for the node in slot `slot`.  An item with fewer than 4096 records cannot
 // carry a fan past the 12-bit field: a fire-and-forget add.  Otherwise a fan field that passes 4095 is
 // noted in the wrap list.
-__device__ __forceinline__ u32 node_add(SmemS& s, u32 slot, u32 c, bool wrapcheck) {
-  const u32 a = c | (1u << PFS);
+// Record (packets | links << 20) into the node's slot; a fan field that passes 4095 is noted in the wrap list
+// (a record adds at most 1281 links, so at most one wrap).
+__device__ __forceinline__ u32 node_add(SmemS& s, u32 slot, u32 a) {
   const u32 o = atomicAdd(&s.npf[slot], a);
-  if (wrapcheck && (o >> PFS) == FMAX) {
+  if ((o >> PFS) + (a >> PFS) > FMAX) {
     const u32 i = atomicAdd(&s.nwrap, 1u);
     if (i < (u32)WRAPCAP) s.wrap[i] = slot;
     else s.ovf = 1;
@@ -689,7 +744,6 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
   u32 ntot = 0;
 #pragma unroll
   for (u32 i = 0; i < NW; ++i) ntot += s.red[0][i];
-  const bool wrapcheck = ntot > FMAX;
   const bool heavy = ntot > HEAVY_S;
   const u64* rb = g.rscr + (u64)wb * B * RCAP;
   // unique nodes (slots this thread claimed), max packets and max fan (mod 4096) of the table, taken from
@@ -717,21 +771,21 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
       const u32 na = (u32)(ra >> 32), nb = (u32)(rc >> 32);
       u32 sa = node_slot(na, logBs), sb = node_slot(nb, logBs);
       bool aa = na != EMPTY32, ab = nb != EMPTY32;  // the node ~0 is merged apart
-      if (va && !aa) { escP += (u32)ra; ++escF; }
-      if (vb && !ab) { escP += (u32)rc; ++escF; }
-      if (aa && na == hot) { hP += (u32)ra; ++hF; aa = false; }
-      if (ab && nb == hot) { hP += (u32)rc; ++hF; ab = false; }
+      if (va && !aa) { escP += (u32)ra & PMASK; escF += (u32)ra >> PFS; }
+      if (vb && !ab) { escP += (u32)rc & PMASK; escF += (u32)rc >> PFS; }
+      if (aa && na == hot) { hP += (u32)ra & PMASK; hF += (u32)ra >> PFS; aa = false; }
+      if (ab && nb == hot) { hP += (u32)rc & PMASK; hF += (u32)rc >> PFS; ab = false; }
       const u32 ca = aa ? *reinterpret_cast<volatile u32*>(&s.nkey[sa]) : 0u;
       const u32 cb = ab ? *reinterpret_cast<volatile u32*>(&s.nkey[sb]) : 0u;
       const u32 cl = probe2<u32>(smem_addr(s.nkey), TS - 1, na, nb, sa, sb, ca, cb, aa, ab, &s.ovf,
                                  [](u32 k) { return node_step(k); });
       nn += __popc(cl);
       if (aa) {
-        const u32 v = node_add(s, sa, (u32)ra, wrapcheck);
+        const u32 v = node_add(s, sa, (u32)ra);
         mp = max(mp, v & PMASK); mf = max(mf, v >> PFS);
       }
       if (ab) {
-        const u32 v = node_add(s, sb, (u32)rc, wrapcheck);
+        const u32 v = node_add(s, sb, (u32)rc);
         mp = max(mp, v & PMASK); mf = max(mf, v >> PFS);
       }
     }
