@@ -310,7 +310,9 @@ nsg_status nsg_trace_stats_weighted(const uint32_t* src, const uint32_t* dst, co
  * completed the call): byte offset inside the workspace of a u32[4] =
  *   {windows the fast path handed to the L2 path because an SMEM table would overflow,
  *    windows whose self-check failed (sum of link counts != window length, or != the sum of n_packets;
- *    0 unless there is a bug), weighted windows whose n_packets sum to >= 2^32 (unsupported), reserved}. */
+ *    0 unless there is a bug), weighted windows whose n_packets sum to >= 2^32 (unsupported),
+ *    heavy groups: (link bucket, node bucket) pairs of the windows <= 2^17 path whose links were merged into
+ *    one record per node (heavy hitters; performance information, results are exact either way)}. */
 size_t nsg_diag_offset(void);
 
 /* Number of kernels the calling host thread's most recent nsg_window_stats* call launched. */

@@ -79,7 +79,8 @@ struct FGeo {
   u32* koff;                       // [nbw][CP][B]    start << 16 | count of bucket b in chunk c
   u64* rscr;                       // [nbw][B][RCAP]
   u32* roff;                       // [nbw][B][2Bs]   start << 16 | count of side bucket (s,q) in link bucket b
-  u32* diag;                       // [0] windows handed to the L2 path, [1] self-check failures
+  u32* diag;                       // [0] windows handed to the L2 path, [1] self-check failures,
+                                   // [3] heavy groups aggregated
   u64* const* mirror;
   u32 n_mirror;
   u64 mirror_row0;
@@ -599,6 +600,8 @@ link_kernel(const FGeo g) {
     atomicAdd(&g.ws[w].sumc, sm);
   }
   if (anyh) {  // heavy groups: one record (node, packets | links << 20) per aggregated node, then their counts
+    if (t == 0)
+      atomicAdd(&g.diag[3], __popc(s.hmask[0]) + __popc(s.hmask[1]) + __popc(s.hmask[2]) + __popc(s.hmask[3]));
     __syncthreads();
     for (u32 i = t; i < 2 * TA; i += LTH) {
       const u32 side = i / TA, node = s.agg[side][0][i % TA];
