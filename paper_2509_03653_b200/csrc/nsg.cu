@@ -384,8 +384,8 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
                         cudaStreamWaitEvent(ax->a, ax->copied, 0) == cudaSuccess;
         if (!ok) return NSG_ERR_CUDA;
       }
-      if (wgt) flat::part_kernel<true><<<g.nbw * g.CP, flat::PTH, sizeof(flat::SmemP), ax->a>>>(g, src, dst, keys);
-      else flat::part_kernel<false><<<g.nbw * g.CP, flat::PTH, sizeof(flat::SmemP), ax->a>>>(g, src, dst, keys);
+      if (wgt) flat::part_kernel<true><<<g.nbw * g.CP, flat::PTH, flat::part_smem(true), ax->a>>>(g, src, dst, keys);
+      else flat::part_kernel<false><<<g.nbw * g.CP, flat::PTH, flat::part_smem(false), ax->a>>>(g, src, dst, keys);
       if (cudaEventRecord(ax->part_done, ax->a) != cudaSuccess || cudaStreamWaitEvent(s, ax->part_done, 0) != cudaSuccess)
         return NSG_ERR_CUDA;
       if (wgt) flat::link_kernel<true><<<g.nbw * g.B, flat::LTH, sizeof(flat::SmemL), s>>>(g);

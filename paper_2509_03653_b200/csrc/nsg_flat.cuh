@@ -245,13 +245,18 @@ __device__ __forceinline__ void warp_seg_step(WarpSegs& ws, u32 e0, u32& oa, u32
 // ---------------------------------------------------------------------------------------------
 struct SmemP {
   u64 stage[CH];
-  u32 wraw[CH], wstage[CH];        // weighted rows: the chunk's weights in row order, then sorted
   u32 hist[MAXB], offs[MAXB];
+  u32 wraw[CH], wstage[CH];        // weighted rows only: the chunk's weights in row order, then sorted
 };
+// part_kernel<false> is launched with only the shared memory before wraw (33 KB instead of 66 KB)
+__host__ __device__ constexpr size_t part_smem(bool wt) { return wt ? sizeof(SmemP) : offsetof(SmemP, wraw); }
 constexpr u32 WTOT_MAX = 1u << 20;  // weighted windows summing to this or more go to the L2 path (20-bit packets)
 
 template <bool WT>
-__global__ void __launch_bounds__(PTH, 3)
+#ifndef NSG_PART_MINB
+#define NSG_PART_MINB 3
+#endif
+__global__ void __launch_bounds__(PTH, NSG_PART_MINB)
 part_kernel(const FGeo g, const u32* __restrict__ src, const u32* __restrict__ dst, const u64* __restrict__ keys) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   SmemP& s = *reinterpret_cast<SmemP*>(smem_raw);
