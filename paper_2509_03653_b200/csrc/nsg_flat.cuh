@@ -196,13 +196,15 @@ struct WarpSegs {
 };
 
 // desc(i) = start << 16 | count of segment i (i < nall), row(i) = element offset of segment i's row;
-// scr: 64 words of this warp's shared memory (the non-empty segments are compacted through it).
-template <class D, class R>
-__device__ __forceinline__ WarpSegs warp_segs(u32 nall, u32 nwarps, u32* scr, D desc, R row) {
+// scr: 64 words of this warp's shared memory (the non-empty segments are compacted through it); mid()
+// runs while the descriptors are loading (the item's table initialisation hides their L2 latency).
+template <class D, class R, class M>
+__device__ __forceinline__ WarpSegs warp_segs(u32 nall, u32 nwarps, u32* scr, D desc, R row, M mid) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const u32 nraw = nall > (u32)wid ? (nall - 1 - wid) / nwarps + 1 : 0u;  // <= 32 by construction
   const u32 i = wid + lane * nwarps;
   const u32 v = (u32)lane < nraw ? desc(i) : 0u;
+  mid();
   const u32 cnt = v & 0xFFFFu;
   u32 x = cnt;
 #pragma unroll
@@ -460,17 +462,21 @@ link_kernel(const FGeo g) {
   const u32 wb = blockIdx.x / g.B, b = blockIdx.x % g.B;
   const u64 w = g.w0 + wb;
   const u32 CP = g.CP, B = g.B, Bs = g.Bs, logBs = g.logBs, logB = g.logB;
-  for (u32 i = t; i < (u32)TL / 2; i += LTH) reinterpret_cast<ulonglong2*>(s.lkey)[i] = make_ulonglong2(EMPTY64, EMPTY64);
-  for (u32 i = t; i < (u32)TL / 4; i += LTH) reinterpret_cast<uint4*>(s.lcnt)[i] = make_uint4(0u, 0u, 0u, 0u);
-  for (u32 i = t; i < 2 * Bs; i += LTH) s.hist[i] = 0;
   if (t < MAXB / 32) s.hmask[t] = 0;
   if (t == 0) {
     s.ncl = 0; s.esc = 0;
     s.ovf = WT && ldcg32(&g.ws[w].wtot) >= WTOT_MAX ? 1u : 0u;  // weighted: packets past the 20-bit fields
   }
-  // this warp's share of the bucket: its segment of chunks wid, wid + NW, ...
+  // this warp's share of the bucket: its segment of chunks wid, wid + NW, ...; the table is initialised
+  // while the segment descriptors load
   const u32* ko = g.koff + (u64)wb * CP * B + b;
-  WarpSegs ws = warp_segs(CP, NW, s.segscr[wid], [&](u32 c) { return ldcg32(ko + (u64)c * B); }, [&](u32 c) { return c * (u32)CH; });
+  WarpSegs ws = warp_segs(CP, NW, s.segscr[wid], [&](u32 c) { return ldcg32(ko + (u64)c * B); }, [&](u32 c) { return c * (u32)CH; },
+                          [&] {
+                            for (u32 i = t; i < (u32)TL / 2; i += LTH)
+                              reinterpret_cast<ulonglong2*>(s.lkey)[i] = make_ulonglong2(EMPTY64, EMPTY64);
+                            for (u32 i = t; i < (u32)TL / 4; i += LTH) reinterpret_cast<uint4*>(s.lcnt)[i] = make_uint4(0u, 0u, 0u, 0u);
+                            for (u32 i = t; i < 2 * Bs; i += LTH) s.hist[i] = 0;
+                          });
   const u64* kb = g.kscr + (u64)wb * CP * CH;
   __syncthreads();  // table initialised
   {
@@ -740,13 +746,15 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
   const u32 Bs = g.Bs, B = g.B, logBs = g.logBs;
   const u32 wb = blockIdx.x / (2 * Bs), q = blockIdx.x % (2 * Bs);
   const u64 w = g.w0 + wb;
-  for (u32 i = t; i < (u32)TS / 4; i += STH) {
-    reinterpret_cast<uint4*>(s.nkey)[i] = make_uint4(EMPTY32, EMPTY32, EMPTY32, EMPTY32);
-    reinterpret_cast<uint4*>(s.npf)[i] = make_uint4(0u, 0u, 0u, 0u);
-  }
   if (t == 0) { s.escP = 0; s.escF = 0; s.ovf = 0; s.nwrap = 0; }
   const u32* ro = g.roff + (u64)wb * B * 2 * Bs + q;
-  WarpSegs ws = warp_segs(B, NW, s.segscr[wid], [&](u32 b) { return ldcg32(ro + (u64)b * 2 * Bs); }, [&](u32 b) { return b * RCAP; });
+  WarpSegs ws = warp_segs(B, NW, s.segscr[wid], [&](u32 b) { return ldcg32(ro + (u64)b * 2 * Bs); }, [&](u32 b) { return b * RCAP; },
+                          [&] {  // the node table, while the descriptors load
+                            for (u32 i = t; i < (u32)TS / 4; i += STH) {
+                              reinterpret_cast<uint4*>(s.nkey)[i] = make_uint4(EMPTY32, EMPTY32, EMPTY32, EMPTY32);
+                              reinterpret_cast<uint4*>(s.npf)[i] = make_uint4(0u, 0u, 0u, 0u);
+                            }
+                          });
   if (lane == 0) s.red[0][wid] = ws.n;
   __syncthreads();  // table initialised, per-warp counts visible
   u32 ntot = 0;
