@@ -478,24 +478,25 @@ link_kernel(const FGeo g) {
                             for (u32 i = t; i < 2 * Bs; i += LTH) s.hist[i] = 0;
                           });
   const u64* kb = g.kscr + (u64)wb * CP * CH;
+  // the next step's keys are loaded while this step's are inserted (L2 latency off the chain); the first
+  // step's load is issued before the barrier
+  u64 nxa = EMPTY64, nxc = EMPTY64;
+  u32 nwa = 1, nwc = 1;  // the keys' weights (weighted rows)
+  const u32* wsb = WT ? g.wscr + (u64)wb * CP * CH : nullptr;
+  auto fetch = [&](u32 e0) {
+    u32 oa, ob;
+    warp_seg_step(ws, e0, oa, ob);
+    nxa = e0 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(kb + oa)) : EMPTY64;
+    nxc = e0 + 32 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(kb + ob)) : EMPTY64;
+    if (WT) {
+      nwa = e0 + lane < ws.n ? ldcg32(wsb + oa) : 0u;
+      nwc = e0 + 32 + lane < ws.n ? ldcg32(wsb + ob) : 0u;
+    }
+  };
+  if (ws.n) fetch(0);
   __syncthreads();  // table initialised
   {
     u32 nesc = 0;
-    // the next step's keys are loaded while this step's are inserted (L2 latency off the chain)
-    u64 nxa = EMPTY64, nxc = EMPTY64;
-    u32 nwa = 1, nwc = 1;  // the keys' weights (weighted rows)
-    const u32* wsb = WT ? g.wscr + (u64)wb * CP * CH : nullptr;
-    auto fetch = [&](u32 e0) {
-      u32 oa, ob;
-      warp_seg_step(ws, e0, oa, ob);
-      nxa = e0 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(kb + oa)) : EMPTY64;
-      nxc = e0 + 32 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(kb + ob)) : EMPTY64;
-      if (WT) {
-        nwa = e0 + lane < ws.n ? ldcg32(wsb + oa) : 0u;
-        nwc = e0 + 32 + lane < ws.n ? ldcg32(wsb + ob) : 0u;
-      }
-    };
-    if (ws.n) fetch(0);
     for (u32 e0 = 0; e0 < ws.n; e0 += 64) {
       const bool va = e0 + lane < ws.n, vb = e0 + 32 + lane < ws.n;
       const u64 ka = nxa, kc = nxc;
@@ -756,25 +757,25 @@ side_kernel(const FGeo g, u64* __restrict__ out) {
                             }
                           });
   if (lane == 0) s.red[0][wid] = ws.n;
+  const u64* rb = g.rscr + (u64)wb * B * RCAP;
+  u64 nxa = ~0ull, nxc = ~0ull;  // the next step's records, loaded while this step's are merged (the first
+  auto fetch = [&](u32 e0) {     // step's before the barrier)
+    u32 oa, ob;
+    warp_seg_step(ws, e0, oa, ob);
+    nxa = e0 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(rb + oa)) : ~0ull;
+    nxc = e0 + 32 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(rb + ob)) : ~0ull;
+  };
+  if (ws.n) fetch(0);
   __syncthreads();  // table initialised, per-warp counts visible
   u32 ntot = 0;
 #pragma unroll
   for (u32 i = 0; i < NW; ++i) ntot += s.red[0][i];
   const bool heavy = ntot > HEAVY_S;
-  const u64* rb = g.rscr + (u64)wb * B * RCAP;
   // unique nodes (slots this thread claimed), max packets and max fan (mod 4096) of the table, taken from
   // the adds' return values (every slot's final value is the largest of its returns)
   u32 nn = 0, mp = 0, mf = 0;
   {
     u32 escP = 0, escF = 0;
-    u64 nxa = ~0ull, nxc = ~0ull;  // the next step's records, loaded while this step's are merged
-    auto fetch = [&](u32 e0) {
-      u32 oa, ob;
-      warp_seg_step(ws, e0, oa, ob);
-      nxa = e0 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(rb + oa)) : ~0ull;
-      nxc = e0 + 32 + lane < ws.n ? __ldcg(reinterpret_cast<const unsigned long long*>(rb + ob)) : ~0ull;
-    };
-    if (ws.n) fetch(0);
     // A heavy item (a heavy hitter's bucket) caches one node per warp in lane registers: its records are
     // summed there instead of in one contended table slot, and merged once at the end.
     const u32 hot = heavy && ws.n ? __shfl_sync(0xffffffffu, (u32)(nxa >> 32), 0) : EMPTY32;
