@@ -430,6 +430,41 @@ __device__ __forceinline__ u32 probe2(u32 tab, u32 mask, T ka, T kb, u32& sa, u3
   return claimed;
 }
 
+// The same lockstep probe with a branch around each slot operation (the link table's 64-bit keys: measured
+// faster there than the predicated form, which the side table's 32-bit keys prefer).
+template <class T, class Step>
+__device__ __forceinline__ u32 probe2b(T* keys, u32 mask, T ka, T kb, u32& sa, u32& sb, T ca, T cb, bool aa, bool ab,
+                                       u32* ovf, Step step) {
+  constexpr T EMPTY = ~T(0);
+  u32 claimed = 0;
+  aa = aa && ca != ka;
+  ab = ab && cb != kb;
+  if (!__any_sync(0xffffffffu, aa || ab)) return 0;
+  const u32 pa = step(ka), pb = step(kb);
+  for (u32 it = 0;; ++it) {
+    if (aa && ca == EMPTY) {
+      const T o = atomicCAS(&keys[sa], EMPTY, ka);
+      claimed |= o == EMPTY ? 1u : 0u;
+      ca = o == EMPTY ? ka : o;
+    }
+    if (ab && cb == EMPTY) {
+      const T o = atomicCAS(&keys[sb], EMPTY, kb);
+      claimed |= o == EMPTY ? 2u : 0u;
+      cb = o == EMPTY ? kb : o;
+    }
+    aa = aa && ca != ka;
+    ab = ab && cb != kb;
+    if (!__any_sync(0xffffffffu, aa || ab)) break;
+    if (it >= mask) {  // table full (adversarial keys only)
+      if (aa || ab) *ovf = 1;
+      break;
+    }
+    if (aa) { sa = (sa + pa) & mask; ca = *reinterpret_cast<volatile T*>(&keys[sa]); }
+    if (ab) { sb = (sb + pb) & mask; cb = *reinterpret_cast<volatile T*>(&keys[sb]); }
+  }
+  return claimed;
+}
+
 // A heavy group's link: add (packets | 1 << 20) to its node's entry in the side's aggregation table (probing at most
 // 8 slots); false if the table has no room (the link then sends its own record).
 __device__ __forceinline__ bool agg_add(u32 (*tab)[TA], u32 node, u32 pf) {
@@ -508,8 +543,13 @@ link_kernel(const FGeo g) {
       u32 sa = link_slot(ka, logB), sb = link_slot(kc, logB);
       const u64 ca = *reinterpret_cast<volatile u64*>(&s.lkey[sa]);
       const u64 cb = *reinterpret_cast<volatile u64*>(&s.lkey[sb]);
+#if NSG_LINK_PTX_PROBE
       const u32 cl = probe2<u64>(smem_addr(s.lkey), TL - 1, ka, kc, sa, sb, ca, cb, aa, ab, &s.ovf,
                                  [](u64 k) { return link_step(k); });
+#else
+      const u32 cl = probe2b<unsigned long long>(reinterpret_cast<unsigned long long*>(s.lkey), TL - 1, ka, kc, sa, sb,
+                                                 ca, cb, aa, ab, &s.ovf, [](u64 k) { return link_step(k); });
+#endif
       if (WT) {
         if (aa) atomicAdd(&s.lcnt[sa], wa);
         if (ab) atomicAdd(&s.lcnt[sb], wc);
