@@ -49,7 +49,10 @@ constexpr int PFS = 20;                       // node packets: 20-bit field (W <
 constexpr u32 PMASK = (1u << PFS) - 1;
 constexpr u32 FMAX = 0xFFFu;                  // fan field: 12 bits; items with >= 4096 records track wraps
 constexpr int WRAPCAP = 64;
-constexpr u32 HEAVY_S = 8192;                 // side items with more records cache a hot node per warp
+#ifndef NSG_HEAVY_S
+#define NSG_HEAVY_S 8192
+#endif
+constexpr u32 HEAVY_S = NSG_HEAVY_S;          // side items with more records cache a hot node per warp
 #ifndef NSG_AGG_T
 #define NSG_AGG_T 128
 #endif
