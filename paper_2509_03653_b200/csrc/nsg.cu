@@ -62,6 +62,8 @@ struct Layout {
   bool flat;
   u32 flogB, fB, flogBs, fBs, fCP, fNB;  // fNB: windows per batch
   size_t o_fws, o_fkscr, o_fkoff, o_frscr, o_froff, o_fwscr, o_fend, o_fipl, o_fipc;
+  u32 fLanes;        // scratch sets [o_fkscr, o_fend): 2 when the call has more than two batches
+  size_t o_fset1;    // the second set (its offsets = the first's + o_fset1 - o_fkscr)
   // global
   u64 LC;
   u32 G;
@@ -125,6 +127,15 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     L.o_fend = q;
     L.o_fipc = q; q = align256(q + (size_t)L.fNB * L.fBs * sizeof(u32));                 // IP sets (vectors)
     L.o_fipl = q; q = align256(q + (size_t)L.fNB * L.fBs * flat::TS * sizeof(u32));
+    // A call of more than two batches runs them on two lanes (each its own scratch set and stream pair), so
+    // that one lane's batch fills the SMs while the other's drains (the kernels' tails, part's low
+    // occupancy); calls of one or two batches keep one set (its write-back is the DRAM traffic of C2).
+#ifndef NSG_LANES_FROM_BATCHES
+#define NSG_LANES_FROM_BATCHES 3  // calls of at least this many batches run on two lanes
+#endif
+    L.fLanes = L.nw > (u64)(NSG_LANES_FROM_BATCHES - 1) * L.fNB ? 2u : 1u;
+    L.o_fset1 = q;
+    if (L.fLanes == 2) q = align256(q + (L.o_fend - L.o_fkscr));
     if (q > o) o = q;
   }
   // L2-path table sets: the full path for large windows, the overflow hand-off otherwise.
@@ -228,6 +239,8 @@ static WriteValue32Fn write_value32() {
 struct Aux {
   cudaStream_t a;
   cudaEvent_t part_done, link_done, copied;
+  cudaStream_t a1, s1;                           // lane 1 of a call's batches: part stream, link/side stream
+  cudaEvent_t part_done1, link_done1, start1, lane1_done;
 };
 static Aux* aux_for(cudaStream_t s) {
   static std::mutex mu;
@@ -241,7 +254,13 @@ static Aux* aux_for(cudaStream_t s) {
   if (cudaStreamCreateWithFlags(&x->a, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&x->part_done, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&x->link_done, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&x->copied, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&x->copied, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&x->a1, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&x->s1, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x->part_done1, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x->link_done1, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x->start1, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&x->lane1_done, cudaEventDisableTiming) != cudaSuccess) {
     delete x;
     return nullptr;
   }
@@ -366,42 +385,65 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
     g.ipc = reinterpret_cast<u32*>(base + L.o_fipc);
     if (cudaMemsetAsync(base + L.o_fws, 0, (size_t)L.nw * sizeof(flat::WinState), s) != cudaSuccess) return NSG_ERR_CUDA;
     if (ev_before && cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev_before), s) != cudaSuccess) return NSG_ERR_CUDA;
-    // Batches pipeline over two streams: part(i) runs on the side stream `a` as soon as link(i-1) has read
-    // the key scratch (so it overlaps side(i-1)); link(i) waits for part(i) and follows side(i-1) on `s`
-    // (the record scratch).  One scratch set of FLAT_BATCH windows stays L2-resident.
+    // Batches pipeline over two streams per lane: part(i) runs on the lane's side stream as soon as the lane's
+    // previous link has read the key scratch (so it overlaps that batch's side kernel); link(i) waits for
+    // part(i) and follows the lane's previous side kernel (the record scratch).  One scratch set of
+    // FLAT_BATCH windows per lane stays L2-resident; with two lanes (calls of more than two batches, no IP
+    // sets — their side-0 lists are one per batch slot) batch i runs on lane i mod 2.
     Aux* ax = aux_for(s);
     if (!ax) return NSG_ERR_CUDA;
+    const u32 lanes = (L.fLanes == 2 && !g.v_ipsets) ? 2u : 1u;
     if (cudaEventRecord(ax->link_done, s) != cudaSuccess) return NSG_ERR_CUDA;  // the reset above
-    for (u64 w0 = 0; w0 < L.nw; w0 += L.fNB) {
+    if (lanes == 2 && (cudaEventRecord(ax->start1, s) != cudaSuccess || cudaStreamWaitEvent(ax->s1, ax->start1, 0) != cudaSuccess ||
+                       cudaEventRecord(ax->link_done1, ax->s1) != cudaSuccess))
+      return NSG_ERR_CUDA;
+    const flat::FGeo g0 = g;
+    const ptrdiff_t d1 = (ptrdiff_t)L.o_fset1 - (ptrdiff_t)L.o_fkscr;  // lane 1's scratch set
+    u64 bi = 0;
+    for (u64 w0 = 0; w0 < L.nw; w0 += L.fNB, ++bi) {
+      const bool l1 = lanes == 2 && (bi & 1);
+      cudaStream_t sa = l1 ? ax->a1 : ax->a, ss = l1 ? ax->s1 : s;
+      cudaEvent_t pd = l1 ? ax->part_done1 : ax->part_done, ld = l1 ? ax->link_done1 : ax->link_done;
+      if (l1) {
+        g.kscr = reinterpret_cast<u64*>(reinterpret_cast<unsigned char*>(g0.kscr) + d1);
+        g.koff = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.koff) + d1);
+        g.rscr = reinterpret_cast<u64*>(reinterpret_cast<unsigned char*>(g0.rscr) + d1);
+        g.roff = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.roff) + d1);
+        g.wscr = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.wscr) + d1);
+      } else {
+        g.kscr = g0.kscr; g.koff = g0.koff; g.rscr = g0.rscr; g.roff = g0.roff; g.wscr = g0.wscr;
+      }
       g.w0 = w0;
       g.nbw = (u32)(L.nw - w0 < (u64)L.fNB ? L.nw - w0 : (u64)L.fNB);
-      if (cudaStreamWaitEvent(ax->a, ax->link_done, 0) != cudaSuccess) return NSG_ERR_CUDA;
+      if (cudaStreamWaitEvent(sa, ld, 0) != cudaSuccess) return NSG_ERR_CUDA;
       if (sin) {  // this batch's keys arrive on the copy stream
         const u64 p0 = w0 * W, p1 = (w0 + g.nbw) * W < n ? (w0 + g.nbw) * W : n;
         const bool ok = cudaMemcpyAsync(const_cast<u64*>(keys) + p0, sin->host + p0, (p1 - p0) * sizeof(u64),
                                         cudaMemcpyHostToDevice, sin->cs) == cudaSuccess &&
                         cudaEventRecord(ax->copied, sin->cs) == cudaSuccess &&
-                        cudaStreamWaitEvent(ax->a, ax->copied, 0) == cudaSuccess;
+                        cudaStreamWaitEvent(sa, ax->copied, 0) == cudaSuccess;
         if (!ok) return NSG_ERR_CUDA;
       }
-      if (wgt) flat::part_kernel<true><<<g.nbw * g.CP, flat::PTH, flat::part_smem(true), ax->a>>>(g, src, dst, keys);
-      else flat::part_kernel<false><<<g.nbw * g.CP, flat::PTH, flat::part_smem(false), ax->a>>>(g, src, dst, keys);
-      if (cudaEventRecord(ax->part_done, ax->a) != cudaSuccess || cudaStreamWaitEvent(s, ax->part_done, 0) != cudaSuccess)
+      if (wgt) flat::part_kernel<true><<<g.nbw * g.CP, flat::PTH, flat::part_smem(true), sa>>>(g, src, dst, keys);
+      else flat::part_kernel<false><<<g.nbw * g.CP, flat::PTH, flat::part_smem(false), sa>>>(g, src, dst, keys);
+      if (cudaEventRecord(pd, sa) != cudaSuccess || cudaStreamWaitEvent(ss, pd, 0) != cudaSuccess)
         return NSG_ERR_CUDA;
-      if (wgt) flat::link_kernel<true><<<g.nbw * g.B, flat::LTH, sizeof(flat::SmemL), s>>>(g);
-      else flat::link_kernel<false><<<g.nbw * g.B, flat::LTH, sizeof(flat::SmemL), s>>>(g);
-      if (cudaEventRecord(ax->link_done, s) != cudaSuccess) return NSG_ERR_CUDA;
-      if (g.v_ipsets && cudaMemsetAsync(g.ipc, 0, (size_t)g.nbw * g.Bs * sizeof(u32), s) != cudaSuccess)
+      if (wgt) flat::link_kernel<true><<<g.nbw * g.B, flat::LTH, sizeof(flat::SmemL), ss>>>(g);
+      else flat::link_kernel<false><<<g.nbw * g.B, flat::LTH, sizeof(flat::SmemL), ss>>>(g);
+      if (cudaEventRecord(ld, ss) != cudaSuccess) return NSG_ERR_CUDA;
+      if (g.v_ipsets && cudaMemsetAsync(g.ipc, 0, (size_t)g.nbw * g.Bs * sizeof(u32), ss) != cudaSuccess)
         return NSG_ERR_CUDA;
-      flat::side_kernel<<<g.nbw * 2 * g.Bs, flat::STH, sizeof(flat::SmemS), s>>>(g, out);
+      flat::side_kernel<<<g.nbw * 2 * g.Bs, flat::STH, sizeof(flat::SmemS), ss>>>(g, out);
       g_last_launches += 3;
       if (cudaGetLastError() != cudaSuccess) return NSG_ERR_CUDA;
     }
+    if (lanes == 2 && (cudaEventRecord(ax->lane1_done, ax->s1) != cudaSuccess || cudaStreamWaitEvent(s, ax->lane1_done, 0) != cudaSuccess))
+      return NSG_ERR_CUDA;  // lane 1 joins the caller's stream
 #ifndef NSG_NO_DISCARD
-    {  // the scratch is dead: drop it from L2 (no write-back of dirty scratch lines to HBM)
+    for (u32 l = 0; l < lanes; ++l) {  // the scratch is dead: drop it from L2 (no write-back of dirty scratch lines to HBM)
       const u64 bytes = (u64)(L.o_fend - L.o_fkscr);
       const u32 blocks = (u32)std::min<u64>((bytes / 128 + 255) / 256, (u64)4 * 148);
-      flat::discard_kernel<<<blocks, 256, 0, s>>>(base + L.o_fkscr, bytes);
+      flat::discard_kernel<<<blocks, 256, 0, s>>>(base + (l ? L.o_fset1 : L.o_fkscr), bytes);
       g_last_launches++;
     }
 #endif
