@@ -62,8 +62,8 @@ struct Layout {
   bool flat;
   u32 flogB, fB, flogBs, fBs, fCP, fNB;  // fNB: windows per batch
   size_t o_fws, o_fkscr, o_fkoff, o_frscr, o_froff, o_fwscr, o_fend, o_fipl, o_fipc;
-  u32 fLanes;        // scratch sets [o_fkscr, o_fend): 2 when the call has more than two batches
-  size_t o_fset1;    // the second set (its offsets = the first's + o_fset1 - o_fkscr)
+  u32 fLanes;        // scratch sets [o_fkscr, o_fend): one per lane of the call's batches
+  size_t o_fset[3];  // set l starts at o_fset[l] (its offsets = the first's + o_fset[l] - o_fkscr)
   // global
   u64 LC;
   u32 G;
@@ -131,11 +131,19 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     // that one lane's batch fills the SMs while the other's drains (the kernels' tails, part's low
     // occupancy); calls of one or two batches keep one set (its write-back is the DRAM traffic of C2).
 #ifndef NSG_LANES_FROM_BATCHES
-#define NSG_LANES_FROM_BATCHES 3  // calls of at least this many batches run on two lanes
+#define NSG_LANES_FROM_BATCHES 3  // calls of at least this many batches run on NSG_LANES lanes
 #endif
-    L.fLanes = L.nw > (u64)(NSG_LANES_FROM_BATCHES - 1) * L.fNB ? 2u : 1u;
-    L.o_fset1 = q;
-    if (L.fLanes == 2) q = align256(q + (L.o_fend - L.o_fkscr));
+#ifndef NSG_LANES
+#define NSG_LANES 2
+#endif
+    static_assert(NSG_LANES >= 1 && NSG_LANES <= 3, "1..3 lanes");
+    const u64 nbat = (L.nw + L.fNB - 1) / L.fNB;
+    L.fLanes = nbat >= (u64)NSG_LANES_FROM_BATCHES ? (u32)std::min<u64>(NSG_LANES, nbat) : 1u;
+    L.o_fset[0] = L.o_fkscr;
+    for (u32 l = 1; l < 3; ++l) {
+      L.o_fset[l] = q;
+      if (l < L.fLanes) q = align256(q + (L.o_fend - L.o_fkscr));
+    }
     if (q > o) o = q;
   }
   // L2-path table sets: the full path for large windows, the overflow hand-off otherwise.
@@ -239,8 +247,8 @@ static WriteValue32Fn write_value32() {
 struct Aux {
   cudaStream_t a;
   cudaEvent_t part_done, link_done, copied;
-  cudaStream_t a1, s1;                           // lane 1 of a call's batches: part stream, link/side stream
-  cudaEvent_t part_done1, link_done1, start1, lane1_done;
+  cudaStream_t la[3], ls[3];                     // lanes 1, 2 of a call's batches: part stream, link/side stream
+  cudaEvent_t lpart[3], llink[3], start, ldone[3];
 };
 static Aux* aux_for(cudaStream_t s) {
   static std::mutex mu;
@@ -255,12 +263,18 @@ static Aux* aux_for(cudaStream_t s) {
       cudaEventCreateWithFlags(&x->part_done, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&x->link_done, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&x->copied, cudaEventDisableTiming) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&x->a1, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&x->s1, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&x->part_done1, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&x->link_done1, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&x->start1, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&x->lane1_done, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&x->start, cudaEventDisableTiming) != cudaSuccess) {
+    delete x;
+    return nullptr;
+  }
+  bool ok = true;
+  for (int l = 1; l < 3; ++l)
+    ok = ok && cudaStreamCreateWithFlags(&x->la[l], cudaStreamNonBlocking) == cudaSuccess &&
+         cudaStreamCreateWithFlags(&x->ls[l], cudaStreamNonBlocking) == cudaSuccess &&
+         cudaEventCreateWithFlags(&x->lpart[l], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&x->llink[l], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&x->ldone[l], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
     delete x;
     return nullptr;
   }
@@ -388,31 +402,30 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
     // Batches pipeline over two streams per lane: part(i) runs on the lane's side stream as soon as the lane's
     // previous link has read the key scratch (so it overlaps that batch's side kernel); link(i) waits for
     // part(i) and follows the lane's previous side kernel (the record scratch).  One scratch set of
-    // FLAT_BATCH windows per lane stays L2-resident; with two lanes (calls of more than two batches, no IP
-    // sets — their side-0 lists are one per batch slot) batch i runs on lane i mod 2.
+    // FLAT_BATCH windows per lane stays L2-resident.  Calls of NSG_LANES_FROM_BATCHES or more batches run
+    // on L.fLanes lanes, batch i on lane i mod lanes (not with IP sets: their side-0 lists are one per batch
+    // slot); the lanes join the caller's stream at the end.
     Aux* ax = aux_for(s);
     if (!ax) return NSG_ERR_CUDA;
-    const u32 lanes = (L.fLanes == 2 && !g.v_ipsets) ? 2u : 1u;
+    const u32 lanes = g.v_ipsets ? 1u : L.fLanes;
+    ax->la[0] = ax->a; ax->ls[0] = s; ax->lpart[0] = ax->part_done; ax->llink[0] = ax->link_done;
     if (cudaEventRecord(ax->link_done, s) != cudaSuccess) return NSG_ERR_CUDA;  // the reset above
-    if (lanes == 2 && (cudaEventRecord(ax->start1, s) != cudaSuccess || cudaStreamWaitEvent(ax->s1, ax->start1, 0) != cudaSuccess ||
-                       cudaEventRecord(ax->link_done1, ax->s1) != cudaSuccess))
-      return NSG_ERR_CUDA;
+    if (lanes > 1 && cudaEventRecord(ax->start, s) != cudaSuccess) return NSG_ERR_CUDA;
+    for (u32 l = 1; l < lanes; ++l)
+      if (cudaStreamWaitEvent(ax->ls[l], ax->start, 0) != cudaSuccess || cudaEventRecord(ax->llink[l], ax->ls[l]) != cudaSuccess)
+        return NSG_ERR_CUDA;
     const flat::FGeo g0 = g;
-    const ptrdiff_t d1 = (ptrdiff_t)L.o_fset1 - (ptrdiff_t)L.o_fkscr;  // lane 1's scratch set
     u64 bi = 0;
     for (u64 w0 = 0; w0 < L.nw; w0 += L.fNB, ++bi) {
-      const bool l1 = lanes == 2 && (bi & 1);
-      cudaStream_t sa = l1 ? ax->a1 : ax->a, ss = l1 ? ax->s1 : s;
-      cudaEvent_t pd = l1 ? ax->part_done1 : ax->part_done, ld = l1 ? ax->link_done1 : ax->link_done;
-      if (l1) {
-        g.kscr = reinterpret_cast<u64*>(reinterpret_cast<unsigned char*>(g0.kscr) + d1);
-        g.koff = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.koff) + d1);
-        g.rscr = reinterpret_cast<u64*>(reinterpret_cast<unsigned char*>(g0.rscr) + d1);
-        g.roff = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.roff) + d1);
-        g.wscr = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.wscr) + d1);
-      } else {
-        g.kscr = g0.kscr; g.koff = g0.koff; g.rscr = g0.rscr; g.roff = g0.roff; g.wscr = g0.wscr;
-      }
+      const u32 l = (u32)(bi % lanes);
+      cudaStream_t sa = ax->la[l], ss = ax->ls[l];
+      cudaEvent_t pd = ax->lpart[l], ld = ax->llink[l];
+      const ptrdiff_t d = (ptrdiff_t)L.o_fset[l] - (ptrdiff_t)L.o_fkscr;  // this lane's scratch set
+      g.kscr = reinterpret_cast<u64*>(reinterpret_cast<unsigned char*>(g0.kscr) + d);
+      g.koff = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.koff) + d);
+      g.rscr = reinterpret_cast<u64*>(reinterpret_cast<unsigned char*>(g0.rscr) + d);
+      g.roff = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.roff) + d);
+      g.wscr = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.wscr) + d);
       g.w0 = w0;
       g.nbw = (u32)(L.nw - w0 < (u64)L.fNB ? L.nw - w0 : (u64)L.fNB);
       if (cudaStreamWaitEvent(sa, ld, 0) != cudaSuccess) return NSG_ERR_CUDA;
@@ -437,13 +450,14 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
       g_last_launches += 3;
       if (cudaGetLastError() != cudaSuccess) return NSG_ERR_CUDA;
     }
-    if (lanes == 2 && (cudaEventRecord(ax->lane1_done, ax->s1) != cudaSuccess || cudaStreamWaitEvent(s, ax->lane1_done, 0) != cudaSuccess))
-      return NSG_ERR_CUDA;  // lane 1 joins the caller's stream
+    for (u32 l = 1; l < lanes; ++l)  // the lanes join the caller's stream
+      if (cudaEventRecord(ax->ldone[l], ax->ls[l]) != cudaSuccess || cudaStreamWaitEvent(s, ax->ldone[l], 0) != cudaSuccess)
+        return NSG_ERR_CUDA;
 #ifndef NSG_NO_DISCARD
     for (u32 l = 0; l < lanes; ++l) {  // the scratch is dead: drop it from L2 (no write-back of dirty scratch lines to HBM)
       const u64 bytes = (u64)(L.o_fend - L.o_fkscr);
       const u32 blocks = (u32)std::min<u64>((bytes / 128 + 255) / 256, (u64)4 * 148);
-      flat::discard_kernel<<<blocks, 256, 0, s>>>(base + (l ? L.o_fset1 : L.o_fkscr), bytes);
+      flat::discard_kernel<<<blocks, 256, 0, s>>>(base + L.o_fset[l], bytes);
       g_last_launches++;
     }
 #endif
