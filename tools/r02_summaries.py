@@ -52,23 +52,26 @@ want = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "smsp__issue_active
         "smsp__sass_inst_executed_op_shared.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
         "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed"]
 idx = {h: i for i, h in enumerate(hdr)}
-PK = 64 * (1 << 17)  # packets per C2 call
+W = 1 << 17
 with open(os.path.join(OUT, "ncu_full_C2.txt"), "w") as f:
-    f.write("# ncu --set full --clock-control none on one C2 call (64 windows x 2^17 packets = 2^23 packets, two "
-            "32-window batches;\n# the capture holds one launch of each kernel = one batch = 2^22 packets)\n")
+    f.write("# ncu --set full --clock-control none on one C2 call (64 windows x 2^17 packets = 2^23 packets); the "
+            "capture holds one launch of each kernel = one batch\n# (8 windows for this call size; the packets of a "
+            "launch follow from its grid: part 32 CTAs, link and side 128 CTAs per window)\n")
     for r in rows[2:]:
         name = r[idx["Kernel Name"]].split("(")[0]
+        grid = int(float(r[idx["launch__grid_size"]].replace(",", "")))
+        pk = grid // (32 if "part" in name else 128) * W  # packets of this launch
         f.write(f"\n== {name}\n")
         for m in want:
             if m in idx:
                 f.write(f"  {m:75s} {r[idx[m]]:>16s} {units[idx[m]]}\n")
         if "smsp__inst_executed.sum" in idx:
             inst = float(r[idx["smsp__inst_executed.sum"]].replace(",", ""))
-            f.write(f"  warp-instructions per packet (per launch / 2^22 packets): {inst / (PK / 2):.2f}\n")
+            f.write(f"  warp-instructions per packet (per launch / {pk} packets): {inst / pk:.2f}\n")
         for m, label in (("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared-memory wavefronts"),
                          ("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_atom.sum", "  of which atomics")):
             if m in idx:
                 v = float(r[idx[m]].replace(",", ""))
-                f.write(f"  {label} per packet: {v / (PK / 2):.2f}\n")
+                f.write(f"  {label} per packet: {v / pk:.2f}\n")
 print(open(os.path.join(OUT, "launches_C2.txt")).read())
 print(open(os.path.join(OUT, "ncu_full_C2.txt")).read())
