@@ -27,9 +27,17 @@ for arg in [a for a in sys.argv[1:] if a != "--print-only"]:
             d = launches.setdefault(int(x["ID"]), {"kernel": x["Kernel Name"].split("(")[0]})
             d[x["Metric Name"]] = float(x["Metric Value"].replace(",", ""))
     seq = [launches[k] for k in sorted(launches)]
-    # one call of C2 = two 32-window batches (part, link, side) + the scratch discard (LAUNCHES_PER_CALL otherwise)
-    per_call = int(os.environ.get("LAUNCHES_PER_CALL", "7"))
-    calls = [seq[i:i + per_call] for i in range(0, len(seq) - per_call + 1, per_call)]
+    # one call = its batches' (part, link, side) launches, closed by the scratch discards (one per batch lane)
+    def is_discard(L):
+        return L["kernel"].split("::")[-1].startswith("discard_kernel")
+
+    calls, cur = [], []
+    for i, L in enumerate(seq):
+        cur.append(L)
+        if is_discard(L) and (i + 1 == len(seq) or not is_discard(seq[i + 1])):
+            calls.append(cur)
+            cur = []
+    per_call = len(calls[-1])
     tail = calls[len(calls) // 2:]
 
     def tot(c, m):
