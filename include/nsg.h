@@ -285,7 +285,9 @@ nsg_status nsg_trace_stats(const uint32_t* src, const uint32_t* dst, const uint6
  * the gather: src_out[p] = pi(rank(src_p)), dst_out[p] = pi(rank(dst_p)).  Every Table 2
  * quantity of the relabelled stream equals the original's (the paper's anonymisation argument).
  *   src_out, dst_out  device u32[n_packets]; n_unique device u64[1] (N).  Input as nsg_window_stats_ex.
- *   workspace         device, 256 B aligned, nsg_anonymize_workspace_bytes() (a 2^32-bit bitmap + prefixes).
+ *   workspace         device, 256 B aligned, nsg_anonymize_workspace_bytes() (a 2^32-bit bitmap of which only
+ *                     the 128-bit groups holding input addresses are touched, a 4 MiB summary of those groups,
+ *                     rank prefixes); contents on entry are irrelevant (the summary is zeroed by each call).
  * Asynchronous on `stream`; errors as nsg_window_stats_ex. */
 size_t nsg_anonymize_workspace_bytes(void);
 nsg_status nsg_anonymize(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,

@@ -1051,7 +1051,7 @@ static nsg_status trace_stats_impl(const uint32_t* src, const uint32_t* dst, con
 
 size_t nsg_anonymize_workspace_bytes(void) {
   return nsg::ANON_WORDS * 4 + nsg::ANON_BLOCKS * 4 + nsg::ANON_SCAN_CTAS * 4 + nsg::ANON_TABLE_SLOTS * 8 +
-         nsg::ANON_TABLE_MAX * 4;
+         nsg::ANON_TABLE_MAX * 4 + nsg::ANON_SWORDS * 4 * 2;
 }
 
 nsg_status nsg_anonymize(const uint32_t* src, const uint32_t* dst, const uint64_t* keys, uint64_t n_packets,
@@ -1075,22 +1075,27 @@ nsg_status nsg_anonymize(const uint32_t* src, const uint32_t* dst, const uint64_
   nsg::u32* ctot = bpre + nsg::ANON_BLOCKS;
   nsg::u64* table = reinterpret_cast<nsg::u64*>(ctot + nsg::ANON_SCAN_CTAS);  // 8 B aligned: offsets are multiples of 4 KiB
   nsg::u32* U = reinterpret_cast<nsg::u32*>(table + nsg::ANON_TABLE_SLOTS);
+  nsg::u32* summ = U + nsg::ANON_TABLE_MAX;
+  nsg::u32* wcnt = summ + nsg::ANON_SWORDS;
   nsg::u64* nu = reinterpret_cast<nsg::u64*>(n_unique);
   const nsg::u64* k = reinterpret_cast<const nsg::u64*>(keys);
-  if (cudaMemsetAsync(bitmap, 0, nsg::ANON_WORDS * 4, s) != cudaSuccess) return NSG_ERR_CUDA;
+  if (cudaMemsetAsync(summ, 0, nsg::ANON_SWORDS * 4, s) != cudaSuccess) return NSG_ERR_CUDA;
   const unsigned grid = (unsigned)(d.sms * (2048 / nsg::AT));
-  if (n_packets) nsg::anon_mark_kernel<<<grid, nsg::AT, 0, s>>>(k, src, dst, n_packets, bitmap);
-  nsg::anon_block_count<<<nsg::ANON_SCAN_CTAS, nsg::AT, 0, s>>>(bitmap, bpre, ctot);
-  nsg::anon_scan_totals<<<1, 1024, 0, s>>>(ctot, nu);
-  nsg::anon_block_prefix<<<nsg::ANON_SCAN_CTAS, nsg::AT, 0, s>>>(bpre, ctot);
   if (n_packets) {
+    nsg::anon_touch_kernel<<<grid, nsg::AT, 0, s>>>(k, src, dst, n_packets, summ);
+    nsg::anon_clear_groups<<<grid, nsg::AT, 0, s>>>(summ, bitmap);
+    nsg::anon_mark_kernel<<<grid, nsg::AT, 0, s>>>(k, src, dst, n_packets, bitmap);
+  }
+  nsg::anon_word_count<<<nsg::ANON_SCAN_CTAS, nsg::AT, 0, s>>>(summ, bitmap, wcnt, ctot);
+  nsg::anon_scan_totals<<<1, 1024, 0, s>>>(ctot, nu);
+  if (n_packets) {
+    nsg::anon_enumerate<<<nsg::ANON_SCAN_CTAS, nsg::AT, 0, s>>>(summ, bitmap, wcnt, ctot, nu, bpre, U);
     nsg::anon_table_fill<<<grid, nsg::AT, 0, s>>>(table, nu);
-    nsg::anon_enumerate<<<grid, nsg::AT, 0, s>>>(bitmap, bpre, nu, U);
     nsg::anon_table_label<<<grid, nsg::AT, 0, s>>>(U, nu, seed, rounds, table);
     nsg::anon_relabel_kernel<<<grid, nsg::AT, 0, s>>>(k, src, dst, n_packets, bitmap, bpre, table, nu, seed, rounds,
                                                       src_out, dst_out);
   }
-  nsg::g_last_launches = n_packets ? 8 : 3;
+  nsg::g_last_launches = n_packets ? 9 : 2;
   return cudaGetLastError() == cudaSuccess ? NSG_OK : NSG_ERR_CUDA;
 }
 

@@ -12,9 +12,12 @@
 //            place of the host shuffle; it is deterministic and needs no table, cf. the deterministic
 //            HashGraph permutation the paper cites)
 //   src'_p = pi(rank(src_p)), dst'_p = pi(rank(dst_p))                                 ("gather")
-// U is never materialised: membership is a 2^32-bit bitmap (512 MiB) in the workspace and rank(a) is the
-// number of set bits below a: an exclusive prefix per 128-bit group (128 MiB) plus the popcounts inside
-// a's group (one 128-bit load).  When N <= ANON_TABLE_MAX the labels pi(rank(a)) are computed once per
+// Membership is a 2^32-bit bitmap (512 MiB) in the workspace, of which only the 128-bit groups that hold
+// an address of the input are ever touched: a summary bitmap (one bit per group, 4 MiB, zeroed per call)
+// is marked first, the marked groups are zeroed, then the addresses' bits are set.  Counting, ranking and
+// enumeration visit the marked groups only (the 4 MiB summary drives them), so a call moves
+// O(input + marked groups) bytes instead of scanning 512 MiB three times.  rank(a) = the number of set
+// bits below a: an exclusive prefix per marked 128-bit group plus the popcounts inside a's group.  When N <= ANON_TABLE_MAX the labels pi(rank(a)) are computed once per
 // distinct address (a scan of the bitmap) into an address -> label hash table of next_pow2(2N) slots,
 // small enough to stay in L2, and the gather is one table probe per address; otherwise every address
 // is ranked and permuted directly.
@@ -27,11 +30,14 @@ namespace nsg {
 constexpr int AT = 512;                          // threads per CTA
 constexpr u64 ANON_WORDS = 1ull << 27;           // u32 words of the 2^32-bit bitmap
 constexpr u64 ANON_BLOCKS = ANON_WORDS / 4;      // 128-bit groups (2^25)
-constexpr u32 ANON_SCAN_PER_CTA = 32768;         // groups per CTA in the prefix scan
-constexpr u32 ANON_SCAN_CTAS = (u32)(ANON_BLOCKS / ANON_SCAN_PER_CTA);  // 1024
+constexpr u64 ANON_SWORDS = ANON_BLOCKS / 32;     // u32 words of the summary bitmap (one bit per group)
+constexpr u32 ANON_SCAN_PER_CTA = 2 * AT;        // summary words per CTA in the count / prefix (2 per thread)
+constexpr u32 ANON_SCAN_CTAS = (u32)(ANON_SWORDS / ANON_SCAN_PER_CTA);  // 1024
+static_assert(ANON_SCAN_CTAS == 1024, "anon_scan_totals scans one total per thread of one 1024-thread CTA");
 constexpr u64 ANON_TABLE_SLOTS = 1ull << 24;     // label table capacity (u64 slots: address << 32 | label)
 constexpr u64 ANON_TABLE_MAX = ANON_TABLE_SLOTS / 2;  // largest N served by the table (load <= 1/2)
-// workspace: bitmap | group prefix | CTA totals | label table | U (the distinct addresses in rank order)
+// workspace: bitmap | group prefix | CTA totals | label table | U (the distinct addresses in rank order) |
+// summary bitmap | set bits per summary word
 
 __device__ __forceinline__ u64 anon_mix(u64 z) {  // splitmix64
   z += 0x9E3779B97F4A7C15ull;
@@ -65,37 +71,69 @@ __device__ __forceinline__ u64 anon_perm(u64 r, u64 N, u64 seed, u32 rounds) {
   return r;
 }
 
-__device__ __forceinline__ void anon_mark(u32* bitmap, u32 a) {
-  u32* w = &bitmap[a >> 5];
-  const u32 bit = 1u << (a & 31);
+__device__ __forceinline__ void anon_set(u32* bits, u32 i) {
+  u32* w = &bits[i >> 5];
+  const u32 bit = 1u << (i & 31);
   if (!(ldcg32(w) & bit)) atomicOr(w, bit);  // read first: repeated addresses cost no atomic
 }
 
+// Pass 1: mark the summary bit of every address's 128-bit group.
+__global__ void __launch_bounds__(AT) anon_touch_kernel(const u64* __restrict__ keys, const u32* __restrict__ src,
+                                                        const u32* __restrict__ dst, u64 n, u32* __restrict__ summ) {
+  for (u64 i = (u64)blockIdx.x * AT + threadIdx.x; i < n; i += (u64)gridDim.x * AT) {
+    const u32 s = keys ? (u32)(keys[i] >> 32) : src[i];
+    const u32 d = keys ? (u32)keys[i] : dst[i];
+    anon_set(summ, s >> 7);
+    anon_set(summ, d >> 7);
+  }
+}
+
+// Pass 2: zero the marked groups (the rest of the bitmap is never read).
+__global__ void __launch_bounds__(AT) anon_clear_groups(const u32* __restrict__ summ, u32* __restrict__ bitmap) {
+  uint4* g4 = reinterpret_cast<uint4*>(bitmap);
+  for (u64 w = (u64)blockIdx.x * AT + threadIdx.x; w < ANON_SWORDS; w += (u64)gridDim.x * AT) {
+    u32 bits = summ[w];
+    while (bits) {
+      const u32 b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      g4[w * 32 + b] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  }
+}
+
+// Pass 3: set every address's bit.
 __global__ void __launch_bounds__(AT) anon_mark_kernel(const u64* __restrict__ keys, const u32* __restrict__ src,
                                                        const u32* __restrict__ dst, u64 n, u32* __restrict__ bitmap) {
   for (u64 i = (u64)blockIdx.x * AT + threadIdx.x; i < n; i += (u64)gridDim.x * AT) {
     const u32 s = keys ? (u32)(keys[i] >> 32) : src[i];
     const u32 d = keys ? (u32)keys[i] : dst[i];
-    anon_mark(bitmap, s);
-    anon_mark(bitmap, d);
+    anon_set(bitmap, s);
+    anon_set(bitmap, d);
   }
 }
 
-// Set bits per 128-bit group, then the exclusive prefix over groups: per-CTA totals, a one-CTA scan of
-// the totals (N = their sum), per-CTA downsweep.
-__global__ void __launch_bounds__(AT) anon_block_count(const u32* __restrict__ bitmap, u32* __restrict__ bcnt,
-                                                       u32* __restrict__ ctot) {
+__device__ __forceinline__ u32 popc4(const uint4 v) { return __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w); }
+
+// Set bits per summary word (its marked groups' popcounts; 2 words per thread), and per CTA.
+__global__ void __launch_bounds__(AT) anon_word_count(const u32* __restrict__ summ, const u32* __restrict__ bitmap,
+                                                      u32* __restrict__ wcnt, u32* __restrict__ ctot) {
   __shared__ u32 red[AT / 32];
-  const u64 b0 = (u64)blockIdx.x * ANON_SCAN_PER_CTA;
-  const uint4* p = reinterpret_cast<const uint4*>(bitmap);
-  u32 mine = 0;
-  for (u32 j = threadIdx.x; j < ANON_SCAN_PER_CTA; j += AT) {
-    const uint4 v = __ldcg(p + b0 + j);  // kept in L2 for the relabel kernel
-    const u32 c = __popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w);
-    bcnt[b0 + j] = c;
-    mine += c;
+  const u64 w0 = (u64)blockIdx.x * ANON_SCAN_PER_CTA + 2 * threadIdx.x;
+  const uint4* g4 = reinterpret_cast<const uint4*>(bitmap);
+  const uint2 sw = *reinterpret_cast<const uint2*>(summ + w0);
+  u32 c[2] = {0u, 0u};
+  const u32 sv[2] = {sw.x, sw.y};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    u32 bits = sv[k];
+    while (bits) {
+      const u32 b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      c[k] += popc4(__ldcg(g4 + (w0 + k) * 32 + b));
+    }
   }
-  mine = warp_sum(mine);
+  *reinterpret_cast<uint2*>(wcnt + w0) = make_uint2(c[0], c[1]);
+  u32 mine = warp_sum(c[0] + c[1]);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mine;
   __syncthreads();
   if (threadIdx.x < 32) {
@@ -132,17 +170,19 @@ __global__ void __launch_bounds__(1024) anon_scan_totals(u32* __restrict__ ctot,
   if (t == 1023) *n_unique = (u64)(incl - v) + v;  // the exclusive prefix fits 32 bits even when N = 2^32
 }
 
-__global__ void __launch_bounds__(AT) anon_block_prefix(u32* __restrict__ bcnt, const u32* __restrict__ ctot) {
-  // in-CTA exclusive scan of this CTA's group counts (PER contiguous per thread), offset by the CTA prefix
+// The rank of each marked group's first address (CTA prefix + in-CTA exclusive scan of the words' counts +
+// the groups before it in its word): stored per group (bpre, read by anon_rank) when N is above the table
+// range; with the table (N <= ANON_TABLE_MAX) the distinct addresses are enumerated instead, U[rank] = a.
+__global__ void __launch_bounds__(AT) anon_enumerate(const u32* __restrict__ summ, const u32* __restrict__ bitmap,
+                                                     const u32* __restrict__ wcnt, const u32* __restrict__ ctot,
+                                                     const u64* __restrict__ n_unique, u32* __restrict__ bpre,
+                                                     u32* __restrict__ U) {
   __shared__ u32 wsum[AT / 32];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  constexpr int PER = ANON_SCAN_PER_CTA / AT;
-  u32* b = bcnt + (u64)blockIdx.x * ANON_SCAN_PER_CTA + t * PER;
-  u32 s = 0;
-  for (int q = 0; q < PER; q += 4) {
-    const uint4 v = *reinterpret_cast<const uint4*>(b + q);
-    s += v.x + v.y + v.z + v.w;
-  }
+  const bool tab = *n_unique <= ANON_TABLE_MAX;
+  const u64 w0 = (u64)blockIdx.x * ANON_SCAN_PER_CTA + 2 * t;
+  const uint2 cc = *reinterpret_cast<const uint2*>(wcnt + w0);
+  const u32 s = cc.x + cc.y;
   u32 x = s;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -161,15 +201,33 @@ __global__ void __launch_bounds__(AT) anon_block_prefix(u32* __restrict__ bcnt, 
     if (lane < AT / 32) wsum[lane] = w;
   }
   __syncthreads();
-  u32 run = ctot[blockIdx.x] + (x - s) + (wid ? wsum[wid - 1] : 0u);
-  for (int q = 0; q < PER; q += 4) {
-    uint4 v = *reinterpret_cast<const uint4*>(b + q);
-    uint4 o;
-    o.x = run; run += v.x;
-    o.y = run; run += v.y;
-    o.z = run; run += v.z;
-    o.w = run; run += v.w;
-    *reinterpret_cast<uint4*>(b + q) = o;
+  u32 r = ctot[blockIdx.x] + (x - s) + (wid ? wsum[wid - 1] : 0u);
+  const uint4* g4 = reinterpret_cast<const uint4*>(bitmap);
+  const uint2 sw = *reinterpret_cast<const uint2*>(summ + w0);
+  const u32 sv[2] = {sw.x, sw.y};
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    u32 gb = sv[k];
+    while (gb) {
+      const u32 gi = (u32)((w0 + k) * 32) + (__ffs(gb) - 1);
+      gb &= gb - 1;
+      const uint4 g = __ldcg(g4 + gi);
+      if (!tab) {
+        bpre[gi] = r;
+        r += popc4(g);
+        continue;
+      }
+      const u32 wv[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        u32 bits = wv[q];
+        while (bits) {
+          const u32 b = __ffs(bits) - 1;
+          bits &= bits - 1;
+          U[r++] = gi * 128 + q * 32 + b;
+        }
+      }
+    }
   }
 }
 
@@ -199,30 +257,6 @@ __global__ void __launch_bounds__(AT) anon_table_fill(u64* __restrict__ table, c
   if (N > ANON_TABLE_MAX) return;
   const u64 cap = anon_table_cap(N);
   for (u64 i = (u64)blockIdx.x * AT + threadIdx.x; i < cap; i += (u64)gridDim.x * AT) table[i] = EMPTY64;
-}
-
-// Enumerate the distinct addresses in ascending order, U[rank] = a (one thread per 128-bit group of the
-// bitmap, the granularity of the rank prefix; the work per set bit is one store), then label them densely
-// (anon_table_label: full warps for the permutation arithmetic).
-__global__ void __launch_bounds__(AT) anon_enumerate(const u32* __restrict__ bitmap, const u32* __restrict__ bpre,
-                                                     const u64* __restrict__ n_unique, u32* __restrict__ U) {
-  if (*n_unique > ANON_TABLE_MAX) return;
-  const uint4* g4 = reinterpret_cast<const uint4*>(bitmap);
-  for (u64 gi = (u64)blockIdx.x * AT + threadIdx.x; gi < ANON_BLOCKS; gi += (u64)gridDim.x * AT) {
-    const uint4 g = __ldcs(g4 + gi);
-    if ((g.x | g.y | g.z | g.w) == 0) continue;
-    u32 r = bpre[gi];
-    const u32 wv[4] = {g.x, g.y, g.z, g.w};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      u32 bits = wv[q];
-      while (bits) {
-        const u32 b = __ffs(bits) - 1;
-        bits &= bits - 1;
-        U[r++] = (u32)(gi * 128 + q * 32 + b);
-      }
-    }
-  }
 }
 
 __global__ void __launch_bounds__(AT) anon_table_label(const u32* __restrict__ U, const u64* __restrict__ n_unique,
