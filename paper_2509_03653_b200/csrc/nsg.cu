@@ -138,9 +138,9 @@ static Layout make_layout(u64 n, u64 W, int sms) {
     L.o_frscr = q; q = align256(q + (size_t)L.fNB * L.fB * flat::RCAP * sizeof(u64));
     L.o_froff = q; q = align256(q + (size_t)L.fNB * L.fB * 2 * L.fBs * sizeof(u32));
     L.o_fwscr = q; q = align256(q + (size_t)L.fNB * L.fCP * flat::CH * sizeof(u32));   // weighted rows
-    L.o_fend = q;
     L.o_fipc = q; q = align256(q + (size_t)L.fNB * L.fBs * sizeof(u32));                 // IP sets (vectors)
     L.o_fipl = q; q = align256(q + (size_t)L.fNB * L.fBs * flat::TS * sizeof(u32));
+    L.o_fend = q;
     // A call of more than two batches runs them on two lanes (each its own scratch set and stream pair), so
     // that one lane's batch fills the SMs while the other's drains (the kernels' tails, part's low
     // occupancy); calls of one or two batches keep one set (its write-back is the DRAM traffic of C2).
@@ -417,11 +417,11 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
     // previous link has read the key scratch (so it overlaps that batch's side kernel); link(i) waits for
     // part(i) and follows the lane's previous side kernel (the record scratch).  One scratch set of
     // FLAT_BATCH windows per lane stays L2-resident.  Calls of NSG_LANES_FROM_BATCHES or more batches run
-    // on L.fLanes lanes, batch i on lane i mod lanes (not with IP sets: their side-0 lists are one per batch
-    // slot); the lanes join the caller's stream at the end.
+    // on L.fLanes lanes, batch i on lane i mod lanes (each lane's set includes its own side-0 node lists for the
+    // IP sets); the lanes join the caller's stream at the end.
     Aux* ax = aux_for(s);
     if (!ax) return NSG_ERR_CUDA;
-    const u32 lanes = g.v_ipsets ? 1u : L.fLanes;
+    const u32 lanes = L.fLanes;
     ax->la[0] = ax->a; ax->ls[0] = s; ax->lpart[0] = ax->part_done; ax->llink[0] = ax->link_done;
     if (cudaEventRecord(ax->link_done, s) != cudaSuccess) return NSG_ERR_CUDA;  // the reset above
     if (lanes > 1 && cudaEventRecord(ax->start, s) != cudaSuccess) return NSG_ERR_CUDA;
@@ -440,6 +440,8 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
       g.rscr = reinterpret_cast<u64*>(reinterpret_cast<unsigned char*>(g0.rscr) + d);
       g.roff = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.roff) + d);
       g.wscr = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.wscr) + d);
+      g.ipl = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.ipl) + d);
+      g.ipc = reinterpret_cast<u32*>(reinterpret_cast<unsigned char*>(g0.ipc) + d);
       g.w0 = w0;
       g.nbw = (u32)(L.nw - w0 < (u64)L.fNB ? L.nw - w0 : (u64)L.fNB);
       if (cudaStreamWaitEvent(sa, ld, 0) != cudaSuccess) return NSG_ERR_CUDA;
@@ -469,7 +471,7 @@ static nsg_status run_impl(const u32* src, const u32* dst, const u64* keys, u64 
         return NSG_ERR_CUDA;
 #ifndef NSG_NO_DISCARD
     for (u32 l = 0; l < lanes; ++l) {  // the scratch is dead: drop it from L2 (no write-back of dirty scratch lines to HBM)
-      const u64 bytes = (u64)(L.o_fend - L.o_fkscr);
+      const u64 bytes = (u64)((g.v_ipsets ? L.o_fend : L.o_fipc) - L.o_fkscr);  // the IP-set lists only when used
       const u32 blocks = (u32)std::min<u64>((bytes / 128 + 255) / 256, (u64)4 * 148);
       flat::discard_kernel<<<blocks, 256, 0, s>>>(base + L.o_fset[l], bytes);
       g_last_launches++;
